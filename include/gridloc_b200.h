@@ -1,0 +1,210 @@
+/*
+ * gridloc_b200 — C-ABI of the B200-native belief-tensor filter.
+ *
+ * Drop-in boundary for the reference `gridloc` C++ library's hot path
+ * (/root/reference/proj/include/gridloc/*.hpp). The reference has no FFI; its
+ * boundary is the C++ API, so each entry point below names the reference
+ * function it replaces (file:line). `include/gridloc_b200.hpp` re-exposes the
+ * same calls with the reference's C++ signatures, and INTEGRATION.md shows the
+ * switch a maintainer makes.
+ *
+ * Plain C types only (no torch / CUDA types in the signatures). Every call is
+ * synchronous unless its name ends in _async; errors map 1:1 onto the
+ * reference's exceptions (see gl_status). Objects are single-threaded, like
+ * the reference's ThreadPool (thread_pool.hpp:47); distinct objects may be
+ * used from different threads and devices.
+ *
+ * The belief tensor is device-resident FP64, layout [k][j][i] exactly as
+ * BeliefTensor (belief_tensor.hpp:55-60,74).
+ */
+#ifndef GRIDLOC_B200_H
+#define GRIDLOC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes <-> reference exceptions. */
+typedef enum {
+  GL_OK = 0,
+  GL_E_EXTINGUISHED = 1, /* gridloc::BeliefExtinguishedError (belief_tensor.hpp:22-25) */
+  GL_E_INVALID = 2,      /* std::invalid_argument */
+  GL_E_MAP_PARSE = 3,    /* gridloc::MapParseError (occupancy_map.hpp:22-30) */
+  GL_E_RUNTIME = 4,      /* std::runtime_error (I/O etc.) */
+  GL_E_CUDA = 5,         /* CUDA runtime / driver failure (no reference analogue) */
+} gl_status;
+
+typedef struct gl_context gl_context;       /* replaces ThreadPool& + StepScratch& */
+typedef struct gl_map gl_map;               /* OccupancyMap (occupancy_map.hpp:35-81) */
+typedef struct gl_field gl_field;           /* DistanceField (occupancy_map.hpp:85-101) */
+typedef struct gl_kernels gl_kernels;       /* KernelSet (belief_tensor.hpp:79-89) */
+typedef struct gl_activation gl_activation; /* Activation (belief_tensor.hpp:93-96) */
+typedef struct gl_tensor gl_tensor;         /* BeliefTensor (belief_tensor.hpp:30-75) */
+
+/* Thread-local message for the last non-OK status. */
+const char* gl_last_error(void);
+/* Library / build identification: "gridloc_b200 <ver> sm_100a". */
+const char* gl_version(void);
+
+/* ---- context ------------------------------------------------------------
+ * One CUDA device + one stream. Replaces the reference's ThreadPool (the
+ * parallel substrate, thread_pool.hpp:15-50) and StepScratch
+ * (belief_tensor.hpp:121-128). */
+gl_status gl_context_create(int device, gl_context** out);
+gl_status gl_context_destroy(gl_context* ctx);
+gl_status gl_context_synchronize(gl_context* ctx);
+/* Device-time of the last gl_step (ms), measured with CUDA events on the
+ * context stream: the fused kernel has no phase boundaries, so the total is
+ * reported as t_motion and t_diffusion = t_masking = 0. */
+gl_status gl_context_last_step_ms(gl_context* ctx, double* ms);
+/* Path selection (GL_PATH_AUTO = fused when the kernel set allows it). */
+enum { GL_PATH_AUTO = 0, GL_PATH_FUSED = 1, GL_PATH_GENERIC = 2 };
+gl_status gl_context_set_path(gl_context* ctx, int path);
+/* Number of kernels this context launched since creation. */
+gl_status gl_context_launch_count(gl_context* ctx, uint64_t* n);
+
+/* ---- maps ------------------------------------------------------------- */
+/* load_map (occupancy_map.hpp:106-108, occupancy_map.cpp:148-165): PGM P2/P5
+ * decode, gray >= threshold is free, boundary ring forced occupied. Host-only
+ * call: with occ == NULL writes dims only. PNG input -> GL_E_MAP_PARSE. */
+gl_status gl_load_map(const uint8_t* bytes, size_t n, int threshold, int* width,
+                      int* height, uint8_t* occ);
+/* OccupancyMap ctor (occupancy_map.cpp:14-42): occ is copied, ring forced. */
+gl_status gl_map_create(gl_context* ctx, int width, int height,
+                        double resolution, double origin_x, double origin_y,
+                        const uint8_t* occ, gl_map** out);
+gl_status gl_map_destroy(gl_map* map);
+gl_status gl_map_info(const gl_map* map, int* width, int* height,
+                      double* resolution, double* origin_x, double* origin_y,
+                      int* free_count);
+gl_status gl_map_cells(const gl_map* map, uint8_t* occ_out);
+/* distance_field (occupancy_map.hpp:117, occupancy_map.cpp:231-271). */
+gl_status gl_field_create(gl_context* ctx, const gl_map* map, gl_field** out);
+gl_status gl_field_destroy(gl_field* f);
+gl_status gl_field_values(const gl_field* f, double* out);
+
+/* ---- kernels / activation ------------------------------------------------
+ * build_kernels (belief_tensor.cpp:243-338), evaluated on the host with the
+ * same libm calls as the reference. */
+typedef struct {
+  int channels;   /* number of per-channel spatial kernels */
+  int radius;     /* spatial half-width r */
+  int separable;  /* isotropic: one 1-D tap vector */
+  int degenerate_spatial;
+  int degenerate_angular;
+  int n_angular;  /* number of (offset, weight) angular taps */
+} gl_kernel_info;
+
+gl_status gl_build_kernels(double sigma_x, double sigma_y, double sigma_theta,
+                           int channels, double cell_size, double delta_theta,
+                           gl_kernels** out);
+/* Wrap an explicit KernelSet (e.g. one built by the reference). sep has
+ * 2r+1 taps (separable) ; spatial has channels*(2r+1)^2 weights (may be NULL
+ * when separable); angular taps in list order. */
+gl_status gl_kernels_create(gl_context* ctx, const gl_kernel_info* info,
+                            const double* sep, const double* spatial,
+                            const int* ang_off, const double* ang_w,
+                            gl_kernels** out);
+gl_status gl_kernels_destroy(gl_kernels* k);
+gl_status gl_kernels_info(const gl_kernels* k, gl_kernel_info* info);
+/* Copy taps out (any pointer may be NULL). */
+gl_status gl_kernels_get(const gl_kernels* k, double* sep, double* spatial,
+                         int* ang_off, double* ang_w);
+
+/* make_activation (belief_tensor.cpp:354-394), computed on the device. */
+gl_status gl_make_activation(gl_context* ctx, const gl_map* map,
+                             const gl_kernels* kernels, int channels,
+                             gl_activation** out);
+gl_status gl_activation_destroy(gl_activation* a);
+/* values / inverse are channels*W*H (either may be NULL). */
+gl_status gl_activation_get(gl_context* ctx, const gl_activation* a,
+                            double* values, double* inverse);
+
+/* ---- tensors ---------------------------------------------------------- */
+/* BeliefTensor ctor (belief_tensor.cpp:20-33): zero-filled. */
+gl_status gl_tensor_create(gl_context* ctx, int width, int height,
+                           int channels, double cell_size, double origin_x,
+                           double origin_y, gl_tensor** out);
+/* init_uniform (belief_tensor.cpp:35-53). */
+gl_status gl_init_uniform(gl_context* ctx, const gl_map* map, int channels,
+                          gl_tensor** out);
+gl_status gl_tensor_destroy(gl_tensor* t);
+gl_status gl_tensor_info(const gl_tensor* t, int* width, int* height,
+                         int* channels, double* cell_size, double* origin_x,
+                         double* origin_y);
+gl_status gl_tensor_theta(const gl_tensor* t, double* theta_t);
+gl_status gl_tensor_set_theta(gl_tensor* t, double theta_t);
+/* Host <-> device copies of the whole tensor, [k][j][i] FP64. */
+gl_status gl_tensor_upload(gl_context* ctx, gl_tensor* t, const double* host);
+gl_status gl_tensor_download(gl_context* ctx, gl_tensor* t, double* host);
+/* 64-bit FNV-1a over the tensor's bytes, computed on the device (parity). */
+gl_status gl_tensor_hash(gl_context* ctx, gl_tensor* t, uint64_t* hash);
+/* Raw device pointer of the current buffer (for NCCL halo exchange). */
+gl_status gl_tensor_device_ptr(gl_context* ctx, gl_tensor* t, double** dptr);
+
+/* ---- the hot path --------------------------------------------------------
+ * step (belief_tensor.hpp:134-136, belief_tensor.cpp:396-498): Algorithm 1
+ * in place. Returns GL_E_EXTINGUISHED exactly when the reference throws
+ * BeliefExtinguishedError (tensor and theta_t already updated, as there). */
+gl_status gl_step(gl_context* ctx, gl_tensor* t, double u, double v, double w,
+                  const gl_map* map, const gl_kernels* kernels,
+                  const gl_activation* act);
+/* Same work, enqueued only: no host sync, no status read-back. The status of
+ * the most recent async step is returned by the next gl_tensor_status(). */
+gl_status gl_step_async(gl_context* ctx, gl_tensor* t, double u, double v,
+                        double w, const gl_map* map, const gl_kernels* kernels,
+                        const gl_activation* act);
+gl_status gl_tensor_status(gl_context* ctx, gl_tensor* t);
+/* apply_motion (belief_tensor.cpp:340-352): shift only, no mask/diffusion. */
+gl_status gl_apply_motion(gl_context* ctx, gl_tensor* t, double u, double v,
+                          double w);
+
+/* belief_map (belief_tensor.cpp:500-510): W*H doubles to host. */
+gl_status gl_belief_map(gl_context* ctx, gl_tensor* t, double* host_out);
+
+/* argmax_state (belief_tensor.cpp:512-541). */
+typedef struct {
+  double x, y, theta;  /* Pose2 */
+  double confidence;   /* max / total mass */
+  int i, j, k;
+} gl_pose_estimate;
+gl_status gl_argmax(gl_context* ctx, gl_tensor* t, gl_pose_estimate* out);
+
+/* dither_samples (observation.cpp:11-71) on a host belief map. cells gets
+ * (i, j) pairs in emission order; at most cap pairs are written, *n is the
+ * full count. */
+gl_status gl_dither(gl_context* ctx, const double* belief_map, int width,
+                    int height, int budget, int32_t* cells, int cap, int* n,
+                    double* source_mass);
+/* dither_samples(belief_map(tensor), budget) without a host round trip. */
+gl_status gl_dither_tensor(gl_context* ctx, gl_tensor* t, int budget,
+                           int32_t* cells, int cap, int* n,
+                           double* source_mass);
+
+/* scan_likelihood / observation_update (observation.cpp:73-170). */
+typedef struct {
+  double sigma_hit;     /* LikelihoodParams (observation.hpp:21-25) */
+  double weight_floor;
+  int beam_stride;
+} gl_likelihood;
+gl_status gl_scan_likelihood(gl_context* ctx, const gl_map* map,
+                             const gl_field* field, double x, double y,
+                             double theta, const double* angles,
+                             const double* ranges, int n_beams,
+                             double max_range, gl_likelihood params,
+                             double* out);
+gl_status gl_observation_update(gl_context* ctx, gl_tensor* t,
+                                const int32_t* cells, int n,
+                                const double* angles, const double* ranges,
+                                int n_beams, double max_range,
+                                const gl_map* map, const gl_field* field,
+                                gl_likelihood params);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GRIDLOC_B200_H */

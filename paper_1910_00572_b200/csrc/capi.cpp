@@ -1,0 +1,1133 @@
+// C-ABI implementation (include/gridloc_b200.h): host runtime that owns the
+// device objects, computes the per-step host inputs (motion vectors with the
+// reference's libm) and dispatches the sm_100a kernels. No CPU compute
+// fallback exists: every tensor operation is a kernel launch, and a missing
+// or failing device is reported as GL_E_CUDA.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gl_internal.hpp"
+#include "gridloc_b200.h"
+#include "host_math.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+  gl_status code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(gl_status code, const std::string& msg) {
+  throw Fail{code, msg};
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    fail(GL_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+#define CK(call) cuda_check((call), #call)
+
+template <class F>
+gl_status guard(F&& f) {
+  try {
+    f();
+    return GL_OK;
+  } catch (const Fail& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const glb::MapParseFailure& e) {
+    g_err = e.what();
+    return GL_E_MAP_PARSE;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return GL_E_INVALID;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return GL_E_RUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return GL_E_RUNTIME;
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void need(bool ok, const char* msg) {
+  if (!ok) fail(GL_E_INVALID, msg);
+}
+
+// ------------------------------------------------------------ TMA encoding
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
+                                 void*, const cuuint64_t*, const cuuint64_t*,
+                                 const cuuint32_t*, const cuuint32_t*,
+                                 CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion,
+                                 CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+  static EncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault,
+                                &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) {
+      fn = reinterpret_cast<EncodeTiled>(p);
+    }
+  });
+  return fn;
+}
+
+// 3-D [C][H][W] FP64 view of a belief buffer, box (bw, bh, 1), zero OOB fill.
+bool make_tmap(CUtensorMap* m, double* base, int w, int h, int c, int bw,
+               int bh) {
+  EncodeTiled enc = encode_fn();
+  if (!enc) return false;
+  if ((static_cast<size_t>(w) * sizeof(double)) % 16 != 0) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(w),
+                              static_cast<cuuint64_t>(h),
+                              static_cast<cuuint64_t>(c)};
+  const cuuint64_t strides[2] = {
+      static_cast<cuuint64_t>(w) * sizeof(double),
+      static_cast<cuuint64_t>(w) * h * sizeof(double)};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(bw),
+                             static_cast<cuuint32_t>(bh), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Tensor-map cache per (tensor buffer, box) lives on the tensor.
+struct TmapCache {
+  double* base = nullptr;
+  int bw = 0, bh = 0;
+  CUtensorMap map;
+};
+
+const CUtensorMap* tensor_tmap(gl_tensor* t, int buf, int bw, int bh);
+
+// ------------------------------------------------------------- helpers
+size_t plane_of(const gl_tensor* t) { return static_cast<size_t>(t->w) * t->h; }
+size_t elems_of(const gl_tensor* t) { return plane_of(t) * t->c; }
+
+void* ensure_misc(gl_context* ctx, size_t bytes) {
+  if (ctx->misc_bytes < bytes) {
+    if (ctx->d_misc) {
+      CK(cudaStreamSynchronize(ctx->stream));
+      CK(cudaFree(ctx->d_misc));
+    }
+    ctx->d_misc = nullptr;
+    CK(cudaMalloc(&ctx->d_misc, bytes));
+    ctx->misc_bytes = bytes;
+  }
+  return ctx->d_misc;
+}
+
+void* ensure_host_misc(gl_context* ctx, size_t bytes) {
+  if (ctx->h_misc_bytes < bytes) {
+    if (ctx->h_misc) {
+      CK(cudaStreamSynchronize(ctx->stream));
+      CK(cudaFreeHost(ctx->h_misc));
+    }
+    ctx->h_misc = nullptr;
+    CK(cudaMallocHost(&ctx->h_misc, bytes));
+    ctx->h_misc_bytes = bytes;
+  }
+  return ctx->h_misc;
+}
+
+void ensure_scratch(gl_context* ctx, size_t elems) {
+  if (ctx->scratch_elems < elems) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->d_s) CK(cudaFree(ctx->d_s));
+    if (ctx->d_d) CK(cudaFree(ctx->d_d));
+    ctx->d_s = ctx->d_d = nullptr;
+    CK(cudaMalloc(&ctx->d_s, elems * sizeof(double)));
+    CK(cudaMalloc(&ctx->d_d, elems * sizeof(double)));
+    ctx->scratch_elems = elems;
+  }
+}
+
+// Host motion vectors for one step -> device ring slot.
+const double2* upload_motion(gl_context* ctx, const gl_tensor* t, double u,
+                             double v) {
+  if (ctx->ring_cap < t->c) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->h_motion) CK(cudaFreeHost(ctx->h_motion));
+    if (ctx->d_motion) CK(cudaFree(ctx->d_motion));
+    ctx->h_motion = nullptr;
+    ctx->d_motion = nullptr;
+    const size_t n = static_cast<size_t>(gl_context::kRing) * t->c * 2;
+    CK(cudaMallocHost(&ctx->h_motion, n * sizeof(double)));
+    CK(cudaMalloc(&ctx->d_motion, n * sizeof(double)));
+    ctx->ring_cap = t->c;
+  }
+  const int slot = ctx->ring_next;
+  ctx->ring_next = (slot + 1) % gl_context::kRing;
+  CK(cudaEventSynchronize(ctx->ring_ev[slot]));  // host slot free again
+  double* h = ctx->h_motion + static_cast<size_t>(slot) * ctx->ring_cap * 2;
+  double* d = ctx->d_motion + static_cast<size_t>(slot) * ctx->ring_cap * 2;
+  const double dtheta = 2.0 * M_PI / t->c;
+  glb::motion_table(u, v, 0, t->c, t->theta_t, dtheta, t->cell, h);
+  CK(cudaMemcpyAsync(d, h, sizeof(double) * 2 * t->c, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaEventRecord(ctx->ring_ev[slot], ctx->stream));
+  return reinterpret_cast<const double2*>(d);
+}
+
+void upload_kernels(gl_kernels* k, int device) {
+  if (k->device == device && k->d_ang_w) return;
+  DeviceGuard g(device);
+  if (k->d_spatial) cudaFree(k->d_spatial);
+  if (k->d_ang_off) cudaFree(k->d_ang_off);
+  if (k->d_ang_w) cudaFree(k->d_ang_w);
+  k->d_spatial = nullptr;
+  k->d_ang_off = nullptr;
+  k->d_ang_w = nullptr;
+  if (!k->spatial.empty()) {
+    CK(cudaMalloc(&k->d_spatial, k->spatial.size() * sizeof(double)));
+    CK(cudaMemcpy(k->d_spatial, k->spatial.data(),
+                  k->spatial.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  CK(cudaMalloc(&k->d_ang_off, k->ang_off.size() * sizeof(int)));
+  CK(cudaMemcpy(k->d_ang_off, k->ang_off.data(), k->ang_off.size() * sizeof(int),
+                cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&k->d_ang_w, k->ang_w.size() * sizeof(double)));
+  CK(cudaMemcpy(k->d_ang_w, k->ang_w.data(), k->ang_w.size() * sizeof(double),
+                cudaMemcpyHostToDevice));
+  k->device = device;
+}
+
+// Apply a pending 1/max rescale to the current buffer in place (consumers
+// other than the step read the tensor as stored).
+void materialize(gl_context* ctx, gl_tensor* t) {
+  glb::launch_apply_scale(ctx, t->d_buf[t->cur], elems_of(t),
+                          &t->d_block->buf[t->cur]);
+}
+
+gl_status read_status(gl_context* ctx, gl_tensor* t) {
+  CK(cudaMemcpyAsync(&ctx->h_block->step, &t->d_block->step,
+                     sizeof(glb::StepState), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return static_cast<gl_status>(ctx->h_block->step.status);
+}
+
+}  // namespace
+
+// Per-tensor TMA map cache (stored out of line to keep gl_tensor POD-ish).
+namespace {
+struct TensorExtra {
+  std::vector<TmapCache> maps;
+};
+std::mutex g_extra_mu;
+std::vector<std::pair<const gl_tensor*, std::unique_ptr<TensorExtra>>> g_extra;
+
+TensorExtra* extra_of(const gl_tensor* t) {
+  std::lock_guard<std::mutex> lk(g_extra_mu);
+  for (auto& e : g_extra)
+    if (e.first == t) return e.second.get();
+  g_extra.emplace_back(t, std::make_unique<TensorExtra>());
+  return g_extra.back().second.get();
+}
+
+void drop_extra(const gl_tensor* t) {
+  std::lock_guard<std::mutex> lk(g_extra_mu);
+  g_extra.erase(std::remove_if(g_extra.begin(), g_extra.end(),
+                               [t](auto& e) { return e.first == t; }),
+                g_extra.end());
+}
+
+const CUtensorMap* tensor_tmap(gl_tensor* t, int buf, int bw, int bh) {
+  TensorExtra* x = extra_of(t);
+  for (auto& m : x->maps)
+    if (m.base == t->d_buf[buf] && m.bw == bw && m.bh == bh) return &m.map;
+  TmapCache c;
+  c.base = t->d_buf[buf];
+  c.bw = bw;
+  c.bh = bh;
+  if (!make_tmap(&c.map, c.base, t->w, t->h, t->c, bw, bh)) return nullptr;
+  x->maps.push_back(c);
+  return &x->maps.back().map;
+}
+}  // namespace
+
+extern "C" {
+
+const char* gl_last_error(void) { return g_err.c_str(); }
+
+const char* gl_version(void) { return "gridloc_b200 0.1 sm_100a fp64"; }
+
+// ---------------------------------------------------------------- context
+gl_status gl_context_create(int device, gl_context** out) {
+  return guard([&] {
+    need(out != nullptr, "out is null");
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    need(device >= 0 && device < n, "no such CUDA device");
+    DeviceGuard g(device);
+    auto ctx = std::make_unique<gl_context>();
+    ctx->device = device;
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&ctx->ev_begin));
+    CK(cudaEventCreate(&ctx->ev_end));
+    for (auto& e : ctx->ring_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaMallocHost(&ctx->h_block, sizeof(glb::DeviceBlock)));
+    *out = ctx.release();
+  });
+}
+
+gl_status gl_context_destroy(gl_context* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    DeviceGuard g(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->d_s) cudaFree(ctx->d_s);
+    if (ctx->d_d) cudaFree(ctx->d_d);
+    if (ctx->d_motion) cudaFree(ctx->d_motion);
+    if (ctx->h_motion) cudaFreeHost(ctx->h_motion);
+    if (ctx->h_block) cudaFreeHost(ctx->h_block);
+    if (ctx->d_misc) cudaFree(ctx->d_misc);
+    if (ctx->h_misc) cudaFreeHost(ctx->h_misc);
+    for (auto& e : ctx->ring_ev) cudaEventDestroy(e);
+    cudaEventDestroy(ctx->ev_begin);
+    cudaEventDestroy(ctx->ev_end);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+gl_status gl_context_synchronize(gl_context* ctx) {
+  return guard([&] {
+    need(ctx, "null context");
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+gl_status gl_context_last_step_ms(gl_context* ctx, double* ms) {
+  return guard([&] {
+    need(ctx && ms, "null argument");
+    CK(cudaEventSynchronize(ctx->ev_end));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, ctx->ev_begin, ctx->ev_end));
+    *ms = f;
+  });
+}
+
+gl_status gl_context_set_path(gl_context* ctx, int path) {
+  return guard([&] {
+    need(ctx, "null context");
+    need(path >= GL_PATH_AUTO && path <= GL_PATH_GENERIC, "bad path");
+    ctx->path = path;
+  });
+}
+
+gl_status gl_context_launch_count(gl_context* ctx, uint64_t* n) {
+  return guard([&] {
+    need(ctx && n, "null argument");
+    *n = ctx->launches;
+  });
+}
+
+// ------------------------------------------------------------------- maps
+gl_status gl_load_map(const uint8_t* bytes, size_t n, int threshold,
+                      int* width, int* height, uint8_t* occ) {
+  return guard([&] {
+    need(bytes && width && height, "null argument");
+    glb::MapParse m = glb::parse_pgm_map(bytes, n, threshold);
+    *width = m.w;
+    *height = m.h;
+    if (occ) std::memcpy(occ, m.occ.data(), m.occ.size());
+  });
+}
+
+gl_status gl_map_create(gl_context* ctx, int width, int height,
+                        double resolution, double origin_x, double origin_y,
+                        const uint8_t* occ, gl_map** out) {
+  return guard([&] {
+    need(ctx && occ && out, "null argument");
+    if (width < 1 || height < 1) fail(GL_E_MAP_PARSE, "map with zero dimension");
+    need(resolution > 0.0, "map resolution must be > 0");
+    DeviceGuard g(ctx->device);
+    auto m = std::make_unique<gl_map>();
+    m->w = width;
+    m->h = height;
+    m->res = resolution;
+    m->ox = origin_x;
+    m->oy = origin_y;
+    m->occ.assign(occ, occ + static_cast<size_t>(width) * height);
+    for (auto& c : m->occ) c = c ? 1 : 0;
+    glb::force_ring(m->occ.data(), width, height);
+    m->free_count = static_cast<int>(std::count(m->occ.begin(), m->occ.end(), 0));
+    m->device = ctx->device;
+    CK(cudaMalloc(&m->d_occ, m->occ.size()));
+    CK(cudaMemcpy(m->d_occ, m->occ.data(), m->occ.size(), cudaMemcpyHostToDevice));
+    *out = m.release();
+  });
+}
+
+gl_status gl_map_destroy(gl_map* map) {
+  return guard([&] {
+    if (!map) return;
+    DeviceGuard g(map->device);
+    cudaFree(map->d_occ);
+    delete map;
+  });
+}
+
+gl_status gl_map_info(const gl_map* m, int* w, int* h, double* res, double* ox,
+                      double* oy, int* free_count) {
+  return guard([&] {
+    need(m, "null map");
+    if (w) *w = m->w;
+    if (h) *h = m->h;
+    if (res) *res = m->res;
+    if (ox) *ox = m->ox;
+    if (oy) *oy = m->oy;
+    if (free_count) *free_count = m->free_count;
+  });
+}
+
+gl_status gl_map_cells(const gl_map* m, uint8_t* out) {
+  return guard([&] {
+    need(m && out, "null argument");
+    std::memcpy(out, m->occ.data(), m->occ.size());
+  });
+}
+
+gl_status gl_field_create(gl_context* ctx, const gl_map* map, gl_field** out) {
+  return guard([&] {
+    need(ctx && map && out, "null argument");
+    DeviceGuard g(ctx->device);
+    auto f = std::make_unique<gl_field>();
+    f->w = map->w;
+    f->h = map->h;
+    f->values = glb::distance_field_host(map->occ.data(), map->w, map->h, map->res);
+    CK(cudaMalloc(&f->d_values, f->values.size() * sizeof(double)));
+    CK(cudaMemcpy(f->d_values, f->values.data(), f->values.size() * sizeof(double),
+                  cudaMemcpyHostToDevice));
+    *out = f.release();
+  });
+}
+
+gl_status gl_field_destroy(gl_field* f) {
+  return guard([&] {
+    if (!f) return;
+    cudaFree(f->d_values);
+    delete f;
+  });
+}
+
+gl_status gl_field_values(const gl_field* f, double* out) {
+  return guard([&] {
+    need(f && out, "null argument");
+    std::memcpy(out, f->values.data(), f->values.size() * sizeof(double));
+  });
+}
+
+// ---------------------------------------------------------------- kernels
+gl_status gl_build_kernels(double sigma_x, double sigma_y, double sigma_theta,
+                           int channels, double cell_size, double delta_theta,
+                           gl_kernels** out) {
+  return guard([&] {
+    need(out != nullptr, "out is null");
+    glb::HostKernels hk = glb::build_kernels_host(sigma_x, sigma_y, sigma_theta,
+                                                  channels, cell_size, delta_theta);
+    auto k = std::make_unique<gl_kernels>();
+    k->info.channels = hk.channels;
+    k->info.radius = hk.radius;
+    k->info.separable = hk.separable;
+    k->info.degenerate_spatial = hk.degenerate_spatial;
+    k->info.degenerate_angular = hk.degenerate_angular;
+    k->info.n_angular = static_cast<int>(hk.ang_w.size());
+    k->sep = std::move(hk.sep);
+    k->spatial = std::move(hk.spatial);
+    k->ang_off = std::move(hk.ang_off);
+    k->ang_w = std::move(hk.ang_w);
+    *out = k.release();
+  });
+}
+
+gl_status gl_kernels_create(gl_context*, const gl_kernel_info* info,
+                            const double* sep, const double* spatial,
+                            const int* ang_off, const double* ang_w,
+                            gl_kernels** out) {
+  return guard([&] {
+    need(info && out && ang_off && ang_w, "null argument");
+    need(info->radius >= 0 && info->n_angular >= 1 && info->channels >= 1,
+         "bad kernel info");
+    const int kw = 2 * info->radius + 1;
+    need(!info->separable || (sep && kw <= glb::kMaxSepTaps),
+         "separable kernels need 2r+1 <= 63 taps");
+    need(info->separable || spatial, "dense kernels need spatial weights");
+    auto k = std::make_unique<gl_kernels>();
+    k->info = *info;
+    if (info->separable) k->sep.assign(sep, sep + kw);
+    if (spatial) {
+      k->spatial.assign(spatial, spatial + static_cast<size_t>(info->channels) * kw * kw);
+    } else {
+      k->spatial.resize(static_cast<size_t>(info->channels) * kw * kw);
+      for (int c = 0; c < info->channels; ++c)
+        for (int a = 0; a < kw; ++a)
+          for (int b = 0; b < kw; ++b)
+            k->spatial[static_cast<size_t>(c) * kw * kw + a * kw + b] = k->sep[a] * k->sep[b];
+    }
+    k->ang_off.assign(ang_off, ang_off + info->n_angular);
+    k->ang_w.assign(ang_w, ang_w + info->n_angular);
+    *out = k.release();
+  });
+}
+
+gl_status gl_kernels_destroy(gl_kernels* k) {
+  return guard([&] {
+    if (!k) return;
+    if (k->device >= 0) {
+      DeviceGuard g(k->device);
+      cudaFree(k->d_spatial);
+      cudaFree(k->d_ang_off);
+      cudaFree(k->d_ang_w);
+    }
+    delete k;
+  });
+}
+
+gl_status gl_kernels_info(const gl_kernels* k, gl_kernel_info* info) {
+  return guard([&] {
+    need(k && info, "null argument");
+    *info = k->info;
+  });
+}
+
+gl_status gl_kernels_get(const gl_kernels* k, double* sep, double* spatial,
+                         int* ang_off, double* ang_w) {
+  return guard([&] {
+    need(k, "null kernels");
+    if (sep) std::copy(k->sep.begin(), k->sep.end(), sep);
+    if (spatial) std::copy(k->spatial.begin(), k->spatial.end(), spatial);
+    if (ang_off) std::copy(k->ang_off.begin(), k->ang_off.end(), ang_off);
+    if (ang_w) std::copy(k->ang_w.begin(), k->ang_w.end(), ang_w);
+  });
+}
+
+gl_status gl_make_activation(gl_context* ctx, const gl_map* map,
+                             const gl_kernels* kernels, int channels,
+                             gl_activation** out) {
+  return guard([&] {
+    need(ctx && map && kernels && out, "null argument");
+    need(channels >= 1, "channels must be >= 1");
+    need(kernels->info.separable || kernels->info.channels >= channels,
+         "kernel set has fewer channels than the tensor");
+    DeviceGuard g(ctx->device);
+    auto* kk = const_cast<gl_kernels*>(kernels);
+    upload_kernels(kk, ctx->device);
+    auto a = std::make_unique<gl_activation>();
+    a->w = map->w;
+    a->h = map->h;
+    a->channels = channels;
+    // isotropic (separable) and impulse kernels make every channel's
+    // activation identical (SURVEY.md probe P4): store one plane.
+    a->k_invariant = kernels->info.separable || kernels->info.radius == 0;
+    const size_t plane = static_cast<size_t>(map->w) * map->h;
+    const size_t np = a->k_invariant ? 1 : channels;
+    CK(cudaMalloc(&a->d_values, plane * np * sizeof(double)));
+    CK(cudaMalloc(&a->d_inverse, plane * np * sizeof(double)));
+    const size_t scratch = plane * (2 + 2 * np);
+    double* d_scratch = static_cast<double*>(ensure_misc(ctx, scratch * sizeof(double)));
+    glb::launch_make_activation(ctx, map->d_occ, map->w, map->h, channels, kk,
+                                a->d_values, a->d_inverse, a->k_invariant,
+                                d_scratch);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    *out = a.release();
+  });
+}
+
+gl_status gl_activation_destroy(gl_activation* a) {
+  return guard([&] {
+    if (!a) return;
+    cudaFree(a->d_values);
+    cudaFree(a->d_inverse);
+    delete a;
+  });
+}
+
+gl_status gl_activation_get(gl_context* ctx, const gl_activation* a,
+                            double* values, double* inverse) {
+  return guard([&] {
+    need(ctx && a, "null argument");
+    DeviceGuard g(ctx->device);
+    const size_t plane = static_cast<size_t>(a->w) * a->h;
+    for (int k = 0; k < a->channels; ++k) {
+      const size_t off = a->k_invariant ? 0 : plane * k;
+      if (values)
+        CK(cudaMemcpyAsync(values + plane * k, a->d_values + off,
+                           plane * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      if (inverse)
+        CK(cudaMemcpyAsync(inverse + plane * k, a->d_inverse + off,
+                           plane * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// ---------------------------------------------------------------- tensors
+static gl_tensor* new_tensor(gl_context* ctx, int w, int h, int c, double cell,
+                             double ox, double oy) {
+  need(w >= 1 && h >= 1 && c >= 1, "belief tensor dimensions must be positive");
+  auto t = std::make_unique<gl_tensor>();
+  t->w = w;
+  t->h = h;
+  t->c = c;
+  t->cell = cell;
+  t->ox = ox;
+  t->oy = oy;
+  t->device = ctx->device;
+  const size_t n = static_cast<size_t>(w) * h * c;
+  CK(cudaMalloc(&t->d_buf[0], n * sizeof(double)));
+  CK(cudaMalloc(&t->d_buf[1], n * sizeof(double)));
+  CK(cudaMalloc(&t->d_block, sizeof(glb::DeviceBlock)));
+  glb::DeviceBlock init{};
+  init.buf[0].scale = init.buf[1].scale = 1.0;
+  CK(cudaMemcpy(t->d_block, &init, sizeof(init), cudaMemcpyHostToDevice));
+  return t.release();
+}
+
+gl_status gl_tensor_create(gl_context* ctx, int width, int height,
+                           int channels, double cell_size, double origin_x,
+                           double origin_y, gl_tensor** out) {
+  return guard([&] {
+    need(ctx && out, "null argument");
+    DeviceGuard g(ctx->device);
+    gl_tensor* t = new_tensor(ctx, width, height, channels, cell_size, origin_x, origin_y);
+    glb::launch_fill(ctx, t->d_buf[0], elems_of(t), 0.0);
+    CK(cudaStreamSynchronize(ctx->stream));
+    *out = t;
+  });
+}
+
+gl_status gl_init_uniform(gl_context* ctx, const gl_map* map, int channels,
+                          gl_tensor** out) {
+  return guard([&] {
+    need(ctx && map && out, "null argument");
+    need(channels >= 4 && channels % 2 == 0, "channel count must be even and >= 4");
+    need(map->free_count > 0, "map has no free cells to initialize from");
+    DeviceGuard g(ctx->device);
+    gl_tensor* t = new_tensor(ctx, map->w, map->h, channels, map->res, map->ox, map->oy);
+    glb::launch_init_uniform(ctx, t->d_buf[0], map->d_occ, map->w, map->h, channels);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    *out = t;
+  });
+}
+
+gl_status gl_tensor_destroy(gl_tensor* t) {
+  return guard([&] {
+    if (!t) return;
+    DeviceGuard g(t->device);
+    cudaFree(t->d_buf[0]);
+    cudaFree(t->d_buf[1]);
+    cudaFree(t->d_block);
+    drop_extra(t);
+    delete t;
+  });
+}
+
+gl_status gl_tensor_info(const gl_tensor* t, int* w, int* h, int* c,
+                         double* cell, double* ox, double* oy) {
+  return guard([&] {
+    need(t, "null tensor");
+    if (w) *w = t->w;
+    if (h) *h = t->h;
+    if (c) *c = t->c;
+    if (cell) *cell = t->cell;
+    if (ox) *ox = t->ox;
+    if (oy) *oy = t->oy;
+  });
+}
+
+gl_status gl_tensor_theta(const gl_tensor* t, double* theta_t) {
+  return guard([&] {
+    need(t && theta_t, "null argument");
+    *theta_t = t->theta_t;
+  });
+}
+
+gl_status gl_tensor_set_theta(gl_tensor* t, double theta_t) {
+  return guard([&] {
+    need(t, "null tensor");
+    t->theta_t = theta_t;
+  });
+}
+
+gl_status gl_tensor_upload(gl_context* ctx, gl_tensor* t, const double* host) {
+  return guard([&] {
+    need(ctx && t && host, "null argument");
+    DeviceGuard g(ctx->device);
+    CK(cudaMemcpyAsync(t->d_buf[t->cur], host, elems_of(t) * sizeof(double),
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(&t->d_block->buf[t->cur], 0, sizeof(glb::BufState), ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+gl_status gl_tensor_download(gl_context* ctx, gl_tensor* t, double* host) {
+  return guard([&] {
+    need(ctx && t && host, "null argument");
+    DeviceGuard g(ctx->device);
+    materialize(ctx, t);
+    CK(cudaMemcpyAsync(host, t->d_buf[t->cur], elems_of(t) * sizeof(double),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+gl_status gl_tensor_hash(gl_context* ctx, gl_tensor* t, uint64_t* hash) {
+  return guard([&] {
+    need(ctx && t && hash, "null argument");
+    DeviceGuard g(ctx->device);
+    materialize(ctx, t);
+    auto* d = static_cast<unsigned long long*>(ensure_misc(ctx, 64));
+    glb::launch_hash(ctx, t->d_buf[t->cur], elems_of(t), d);
+    unsigned long long hv = 0;
+    CK(cudaMemcpyAsync(&hv, d, sizeof(hv), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    *hash = hv;
+  });
+}
+
+gl_status gl_tensor_device_ptr(gl_context* ctx, gl_tensor* t, double** dptr) {
+  return guard([&] {
+    need(ctx && t && dptr, "null argument");
+    DeviceGuard g(ctx->device);
+    materialize(ctx, t);
+    CK(cudaStreamSynchronize(ctx->stream));
+    *dptr = t->d_buf[t->cur];
+  });
+}
+
+// ----------------------------------------------------------------- step
+static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
+                         double w, const gl_map* map, const gl_kernels* kernels,
+                         const gl_activation* act) {
+  need(ctx && t && map && kernels && act, "null argument");
+  need(map->w == t->w && map->h == t->h, "map and tensor sizes differ");
+  need(act->w == t->w && act->h == t->h && act->channels == t->c,
+       "activation does not match the tensor");
+  need(kernels->info.separable || kernels->info.channels >= t->c,
+       "kernel set has fewer channels than the tensor");
+  DeviceGuard g(ctx->device);
+  auto* kk = const_cast<gl_kernels*>(kernels);
+  upload_kernels(kk, ctx->device);
+
+  glb::StepArgs a{};
+  const int src = t->cur, dst = 1 - t->cur;
+  a.src = t->d_buf[src];
+  a.dst = t->d_buf[dst];
+  a.src_state = &t->d_block->buf[src];
+  a.dst_state = &t->d_block->buf[dst];
+  a.step_state = &t->d_block->step;
+  a.occ = map->d_occ;
+  a.inv = act->d_inverse;
+  a.inv_per_channel = act->k_invariant ? 0 : 1;
+  a.w = t->w;
+  a.h = t->h;
+  a.c = t->c;
+
+  CK(cudaEventRecord(ctx->ev_begin, ctx->stream));
+  a.motion = upload_motion(ctx, t, u, v);
+
+  const int r = kernels->info.radius;
+  glb::AngTaps ang{};
+  bool fused = ctx->path != GL_PATH_GENERIC &&
+               (kernels->info.separable || r == 0) &&
+               kernels->info.n_angular <= 2 * glb::kFusedMaxHalf + 1;
+  if (fused) {
+    ang.n = kernels->info.n_angular;
+    for (int q = 0; q < ang.n; ++q) {
+      ang.off[q] = kernels->ang_off[q];
+      ang.w[q] = kernels->ang_w[q];
+    }
+    fused = glb::fused_supported(r, ang, t->c);
+  }
+  const CUtensorMap* tm = nullptr;
+  if (fused) {
+    int bw = 0, bh = 0;
+    glb::fused_box(r, ang.n / 2, &bw, &bh);
+    tm = tensor_tmap(t, src, bw, bh);
+    fused = tm != nullptr;
+  }
+  if (ctx->path == GL_PATH_FUSED && !fused) {
+    fail(GL_E_INVALID, "fused path requested but unsupported for this kernel set/grid");
+  }
+  if (fused) {
+    glb::launch_fused_step(ctx, a, tm, kernels->sep.data(), r, ang);
+  } else {
+    const size_t n = elems_of(t);
+    ensure_scratch(ctx, n);
+    glb::launch_shift_mask(ctx, a, ctx->d_s, 1);
+    const double* D = ctx->d_s;
+    if (kernels->info.separable) {
+      glb::SepTaps taps{};
+      for (int q = 0; q < 2 * r + 1; ++q) taps.t[q] = kernels->sep[q];
+      // rows into d_d, columns back into d_s (S is free after phase 1)
+      glb::launch_conv_separable(ctx, ctx->d_s, ctx->d_d, ctx->d_s, t->w, t->h,
+                                 t->c, taps, r);
+    } else if (r > 0) {
+      glb::launch_conv_dense(ctx, ctx->d_s, ctx->d_d, t->w, t->h, t->c,
+                             kk->d_spatial, r, kernels->info.channels);
+      D = ctx->d_d;
+    }
+    glb::launch_angular(ctx, a, D, kk->d_ang_off, kk->d_ang_w,
+                        kernels->info.n_angular);
+    glb::launch_step_finalize(ctx, a);
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev_end, ctx->stream));
+  t->cur = dst;
+  t->theta_t = t->theta_t + w;  // belief_tensor.cpp:478
+}
+
+gl_status gl_step(gl_context* ctx, gl_tensor* t, double u, double v, double w,
+                  const gl_map* map, const gl_kernels* kernels,
+                  const gl_activation* act) {
+  gl_status st = guard([&] { enqueue_step(ctx, t, u, v, w, map, kernels, act); });
+  if (st != GL_OK) return st;
+  st = guard([&] {
+    if (read_status(ctx, t) == GL_E_EXTINGUISHED) {
+      fail(GL_E_EXTINGUISHED, "belief tensor extinguished: no positive mass after step");
+    }
+  });
+  return st;
+}
+
+gl_status gl_step_async(gl_context* ctx, gl_tensor* t, double u, double v,
+                        double w, const gl_map* map, const gl_kernels* kernels,
+                        const gl_activation* act) {
+  return guard([&] { enqueue_step(ctx, t, u, v, w, map, kernels, act); });
+}
+
+gl_status gl_tensor_status(gl_context* ctx, gl_tensor* t) {
+  return guard([&] {
+    need(ctx && t, "null argument");
+    DeviceGuard g(ctx->device);
+    if (read_status(ctx, t) == GL_E_EXTINGUISHED) {
+      fail(GL_E_EXTINGUISHED, "belief tensor extinguished: no positive mass after step");
+    }
+  });
+}
+
+gl_status gl_apply_motion(gl_context* ctx, gl_tensor* t, double u, double v,
+                          double w) {
+  return guard([&] {
+    need(ctx && t, "null argument");
+    DeviceGuard g(ctx->device);
+    glb::StepArgs a{};
+    const int src = t->cur, dst = 1 - t->cur;
+    a.src = t->d_buf[src];
+    a.src_state = &t->d_block->buf[src];
+    a.w = t->w;
+    a.h = t->h;
+    a.c = t->c;
+    a.motion = upload_motion(ctx, t, u, v);
+    glb::launch_shift_mask(ctx, a, t->d_buf[dst], 2);
+    CK(cudaMemsetAsync(&t->d_block->buf[dst], 0, sizeof(glb::BufState), ctx->stream));
+    CK(cudaGetLastError());
+    t->cur = dst;
+    t->theta_t = t->theta_t + w;
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// ------------------------------------------------------------ read-outs
+static double wrap_angle(double a) {  // geometry.hpp:8-13
+  a = std::fmod(a, 2.0 * M_PI);
+  if (a < -M_PI) a += 2.0 * M_PI;
+  if (a >= M_PI) a -= 2.0 * M_PI;
+  return a;
+}
+
+gl_status gl_belief_map(gl_context* ctx, gl_tensor* t, double* host_out) {
+  return guard([&] {
+    need(ctx && t && host_out, "null argument");
+    DeviceGuard g(ctx->device);
+    materialize(ctx, t);
+    double* d = static_cast<double*>(ensure_misc(ctx, plane_of(t) * sizeof(double)));
+    glb::launch_belief_map(ctx, t->d_buf[t->cur], t->w, t->h, t->c, d);
+    CK(cudaMemcpyAsync(host_out, d, plane_of(t) * sizeof(double),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+gl_status gl_argmax(gl_context* ctx, gl_tensor* t, gl_pose_estimate* out) {
+  return guard([&] {
+    need(ctx && t && out, "null argument");
+    DeviceGuard g(ctx->device);
+    materialize(ctx, t);
+    const size_t n = elems_of(t);
+    const size_t sb = glb::argmax_scratch_bytes(n);
+    char* d = static_cast<char*>(ensure_misc(ctx, sb + 256));
+    glb::launch_argmax(ctx, t->d_buf[t->cur], n, d, sb, d + sb);
+    struct {
+      double v;
+      long long idx;
+      double sum;
+    } res{};
+    CK(cudaMemcpyAsync(&res, d + sb, sizeof(res), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (!(res.v > 0.0)) fail(GL_E_EXTINGUISHED, "argmax on an all-zero belief tensor");
+    const size_t plane = plane_of(t);
+    const size_t p = static_cast<size_t>(res.idx) % plane;
+    out->k = static_cast<int>(static_cast<size_t>(res.idx) / plane);
+    out->i = static_cast<int>(p % t->w);
+    out->j = static_cast<int>(p / t->w);
+    out->x = t->ox + (out->i + 0.5) * t->cell;
+    out->y = t->oy + (out->j + 0.5) * t->cell;
+    out->theta = wrap_angle(out->k * (2.0 * M_PI / t->c) + t->theta_t);
+    out->confidence = res.sum > 0.0 ? res.v / res.sum : 0.0;
+  });
+}
+
+static void run_dither(gl_context* ctx, const double* d_bm, int w, int h,
+                       int budget, int32_t* cells, int cap, int* n,
+                       double* mass) {
+  need(budget >= 1, "sample budget must be >= 1");
+  need(cap >= 0 && n && mass, "bad output arguments");
+  const size_t plane = static_cast<size_t>(w) * h;
+  // device capacity: every cell could emit at most once
+  const size_t dcap = std::min<size_t>(plane, static_cast<size_t>(std::max(cap, 1)));
+  char* base = static_cast<char*>(ensure_misc(ctx, plane * sizeof(double) + 64 + dcap * 8));
+  // layout: [bm plane (if copied)] [n, mass] [cells]
+  int* d_n = reinterpret_cast<int*>(base + plane * sizeof(double));
+  double* d_mass = reinterpret_cast<double*>(base + plane * sizeof(double) + 8);
+  int* d_cells = reinterpret_cast<int*>(base + plane * sizeof(double) + 64);
+  glb::launch_dither(ctx, d_bm, w, h, budget, d_cells, static_cast<int>(dcap), d_n, d_mass);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(n, d_n, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(mass, d_mass, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const int got = std::min(*n, cap);
+  if (got > 0 && cells) {
+    CK(cudaMemcpyAsync(cells, d_cells, sizeof(int32_t) * 2 * got,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+}
+
+gl_status gl_dither(gl_context* ctx, const double* belief_map, int width,
+                    int height, int budget, int32_t* cells, int cap, int* n,
+                    double* source_mass) {
+  return guard([&] {
+    need(ctx && belief_map, "null argument");
+    need(width >= 1 && height >= 1, "bad belief map size");
+    DeviceGuard g(ctx->device);
+    const size_t plane = static_cast<size_t>(width) * height;
+    double* d = static_cast<double*>(
+        ensure_misc(ctx, plane * sizeof(double) + 64 + std::min<size_t>(plane, std::max(cap, 1)) * 8));
+    CK(cudaMemcpyAsync(d, belief_map, plane * sizeof(double),
+                       cudaMemcpyHostToDevice, ctx->stream));
+    run_dither(ctx, d, width, height, budget, cells, cap, n, source_mass);
+  });
+}
+
+gl_status gl_dither_tensor(gl_context* ctx, gl_tensor* t, int budget,
+                           int32_t* cells, int cap, int* n,
+                           double* source_mass) {
+  return guard([&] {
+    need(ctx && t, "null argument");
+    DeviceGuard g(ctx->device);
+    materialize(ctx, t);
+    const size_t plane = plane_of(t);
+    double* d = static_cast<double*>(
+        ensure_misc(ctx, plane * sizeof(double) + 64 + std::min<size_t>(plane, std::max(cap, 1)) * 8));
+    glb::launch_belief_map(ctx, t->d_buf[t->cur], t->w, t->h, t->c, d);
+    run_dither(ctx, d, t->w, t->h, budget, cells, cap, n, source_mass);
+  });
+}
+
+// ----------------------------------------------------------- observation
+namespace {
+
+struct ObsTables {
+  std::vector<double> score;  // per cell beam log-score
+  double oob = 0.0;
+  double sigma_hit = -1.0, floor_w = -1.0;
+  double* d_score = nullptr;
+};
+
+std::mutex g_obs_mu;
+std::vector<std::pair<const gl_field*, std::unique_ptr<ObsTables>>> g_obs;
+
+// Per-cell likelihood-field beam score with the reference's libm:
+// log((1 - f) * exp(-d*d*inv2s2) + f) (observation.cpp:101-106).
+ObsTables* obs_tables(gl_context* ctx, const gl_field* f, gl_likelihood p) {
+  std::lock_guard<std::mutex> lk(g_obs_mu);
+  ObsTables* tb = nullptr;
+  for (auto& e : g_obs)
+    if (e.first == f) tb = e.second.get();
+  if (!tb) {
+    g_obs.emplace_back(f, std::make_unique<ObsTables>());
+    tb = g_obs.back().second.get();
+  }
+  if (tb->sigma_hit == p.sigma_hit && tb->floor_w == p.weight_floor && tb->d_score)
+    return tb;
+  const double fl = p.weight_floor;
+  const double inv2s2 = 1.0 / (2.0 * p.sigma_hit * p.sigma_hit);
+  tb->score.resize(f->values.size());
+  for (size_t q = 0; q < f->values.size(); ++q) {
+    const double d = f->values[q];
+    const double gauss = std::exp(-d * d * inv2s2);
+    tb->score[q] = std::log((1.0 - fl) * gauss + fl);
+  }
+  tb->oob = std::log((1.0 - fl) * 0.0 + fl);
+  if (tb->d_score) cudaFree(tb->d_score);
+  tb->d_score = nullptr;
+  CK(cudaMalloc(&tb->d_score, tb->score.size() * sizeof(double)));
+  CK(cudaMemcpyAsync(tb->d_score, tb->score.data(), tb->score.size() * sizeof(double),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  tb->sigma_hit = p.sigma_hit;
+  tb->floor_w = p.weight_floor;
+  return tb;
+}
+
+}  // namespace
+
+gl_status gl_scan_likelihood(gl_context* ctx, const gl_map* map,
+                             const gl_field* field, double x, double y,
+                             double theta, const double* angles,
+                             const double* ranges, int n_beams,
+                             double max_range, gl_likelihood params,
+                             double* out) {
+  // Single-pose convenience: one (sample, channel) evaluated by the same
+  // device kernel as observation_update, with a 1-channel pose table.
+  return guard([&] {
+    need(ctx && map && field && out, "null argument");
+    need(n_beams >= 1 && angles && ranges, "scan must have matching, nonempty beams");
+    DeviceGuard g(ctx->device);
+    ObsTables* tb = obs_tables(ctx, field, params);
+    const int stride = std::max(1, params.beam_stride);
+    std::vector<double> dirs, reach;
+    const double half = 0.5 * map->res;
+    for (int b = 0; b < n_beams; b += stride) {
+      if (ranges[b] >= max_range - 1e-9) continue;
+      const double a = theta + angles[b];
+      dirs.push_back(std::cos(a));
+      dirs.push_back(std::sin(a));
+      reach.push_back(ranges[b] + half);
+    }
+    // pose in world coords: pass as a "sample" at fractional cell via origin
+    // shift: tox + (0 + 0.5)*cell == x  <=>  tox = x - 0.5*cell with cell = 1
+    const int ns = static_cast<int>(reach.size());
+    size_t bytes = 64 + (ns + 1) * 24 + 64;
+    char* d = static_cast<char*>(ensure_misc(ctx, bytes));
+    int* d_s = reinterpret_cast<int*>(d);
+    double* d_L = reinterpret_cast<double*>(d + 16);
+    double* d_reach = reinterpret_cast<double*>(d + 64);
+    double2* d_dir = reinterpret_cast<double2*>(d + 64 + 8 * (ns + 1) + 8);
+    d_dir = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(d_dir) + 15) & ~uintptr_t(15));
+    const int zero2[2] = {0, 0};
+    CK(cudaMemcpyAsync(d_s, zero2, sizeof(zero2), cudaMemcpyHostToDevice, ctx->stream));
+    if (ns > 0) {
+      CK(cudaMemcpyAsync(d_reach, reach.data(), ns * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(d_dir, dirs.data(), ns * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    // x = tox + (0 + 0.5) * 0.0 ... use cell = 0 so the pose is exactly (x, y)
+    glb::launch_likelihoods(ctx, map->d_occ, tb->d_score, tb->oob, map->w, map->h,
+                            map->res, map->ox, map->oy, 0.0, x, y, d_s, 1, 1,
+                            d_dir, ns, d_reach, params.weight_floor, d_L);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, d_L, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+gl_status gl_observation_update(gl_context* ctx, gl_tensor* t,
+                                const int32_t* cells, int n,
+                                const double* angles, const double* ranges,
+                                int n_beams, double max_range,
+                                const gl_map* map, const gl_field* field,
+                                gl_likelihood params) {
+  return guard([&] {
+    need(ctx && t && map && field, "null argument");
+    if (n == 0) return;  // observation.cpp:117
+    need(cells != nullptr && n > 0, "bad sample set");
+    need(n_beams >= 1 && angles && ranges, "scan must have matching, nonempty beams");
+    DeviceGuard g(ctx->device);
+    ObsTables* tb = obs_tables(ctx, field, params);
+    const int C = t->c;
+    // scored beams and per-(channel, beam) directions with host libm
+    const int stride = std::max(1, params.beam_stride);
+    std::vector<int> scored;
+    for (int b = 0; b < n_beams; b += stride)
+      if (!(ranges[b] >= max_range - 1e-9)) scored.push_back(b);
+    const int ns = static_cast<int>(scored.size());
+    const double half = 0.5 * map->res;
+    const double dtheta = 2.0 * M_PI / C;
+    std::vector<double> reach(std::max(ns, 1));
+    for (int q = 0; q < ns; ++q) reach[q] = ranges[scored[q]] + half;
+    std::vector<double> dirs(static_cast<size_t>(C) * std::max(ns, 1) * 2);
+    for (int k = 0; k < C; ++k) {
+      const double ak = k * dtheta + t->theta_t;  // channel_angle(k)
+      for (int q = 0; q < ns; ++q) {
+        const double a = ak + angles[scored[q]];
+        dirs[(static_cast<size_t>(k) * ns + q) * 2] = std::cos(a);
+        dirs[(static_cast<size_t>(k) * ns + q) * 2 + 1] = std::sin(a);
+      }
+    }
+    const size_t nL = static_cast<size_t>(n) * C;
+    size_t off_s = 0;
+    size_t off_L = (off_s + sizeof(int) * 2 * n + 255) & ~size_t(255);
+    size_t off_mean = (off_L + sizeof(double) * nL + 255) & ~size_t(255);
+    size_t off_reach = off_mean + 256;
+    size_t off_dir = (off_reach + sizeof(double) * reach.size() + 255) & ~size_t(255);
+    size_t total = off_dir + sizeof(double) * dirs.size() + 256;
+    char* d = static_cast<char*>(ensure_misc(ctx, total));
+    int* d_s = reinterpret_cast<int*>(d + off_s);
+    double* d_L = reinterpret_cast<double*>(d + off_L);
+    double* d_mean = reinterpret_cast<double*>(d + off_mean);
+    double* d_reach = reinterpret_cast<double*>(d + off_reach);
+    double2* d_dir = reinterpret_cast<double2*>(d + off_dir);
+    CK(cudaMemcpyAsync(d_s, cells, sizeof(int) * 2 * n, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(d_reach, reach.data(), sizeof(double) * reach.size(), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(d_dir, dirs.data(), sizeof(double) * dirs.size(), cudaMemcpyHostToDevice, ctx->stream));
+    materialize(ctx, t);
+    glb::launch_likelihoods(ctx, map->d_occ, tb->d_score, tb->oob, map->w, map->h,
+                            map->res, map->ox, map->oy, t->cell, t->ox, t->oy, d_s,
+                            n, C, d_dir, ns, d_reach, params.weight_floor, d_L);
+    glb::launch_observe_apply(ctx, t->d_buf[t->cur], t->w, t->h, C, d_s, n, d_L, d_mean);
+    glb::launch_plane_max(ctx, t->d_buf[t->cur], elems_of(t), &t->d_block->step.gmax_bits);
+    glb::launch_observe_finalize(ctx, &t->d_block->step, &t->d_block->buf[t->cur]);
+    CK(cudaGetLastError());
+    if (read_status(ctx, t) == GL_E_EXTINGUISHED) {
+      fail(GL_E_EXTINGUISHED, "observation update zeroed the tensor");
+    }
+  });
+}
+
+}  // extern "C"

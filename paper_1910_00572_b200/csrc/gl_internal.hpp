@@ -1,0 +1,197 @@
+// Internal types shared by the host runtime (capi.cpp, host_math.cpp) and
+// the CUDA kernels (k_*.cu). Not part of the public C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "gridloc_b200.h"
+
+namespace glb {
+
+constexpr int kMaxSepTaps = 63;      // separable taps held in kernel params
+constexpr int kFusedMaxHalf = 3;     // fused path: angular offsets in [-3, 3]
+constexpr int kFusedMaxRadius = 2;   // fused path: separable radius <= 2 (or 0)
+
+// Per-buffer "pending rescale" (belief_tensor.cpp:486-493). The step that
+// produced a buffer records whether its global max fell below 1e-6; the
+// multiply by 1/max is folded into the next reader's load (bit-identical:
+// the reader computes value*scale exactly where the reference stored it).
+struct BufState {
+  double scale;  // valid when scaled != 0
+  int scaled;
+  int pad;
+};
+
+// Step reduction scratch on the device. gmax_bits holds the running global
+// maximum as uint64 bits (valid ordering for non-negative doubles); the last
+// CTA to finish turns it into the status + the next buffer's BufState.
+struct StepState {
+  unsigned long long gmax_bits;
+  unsigned int blocks_done;
+  int status;  // GL_OK or GL_E_EXTINGUISHED for the latest step
+};
+
+struct DeviceBlock {  // one allocation per tensor
+  BufState buf[2];
+  StepState step;
+};
+
+// Angular taps (belief_tensor.hpp:82): (offset, weight) in list order.
+struct AngTaps {
+  int n;
+  int off[2 * kFusedMaxHalf + 1];
+  double w[2 * kFusedMaxHalf + 1];
+};
+
+}  // namespace glb
+
+struct gl_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+  int path = GL_PATH_AUTO;
+  uint64_t launches = 0;
+  // generic-path scratch (S and D tensors), grown on demand
+  double* d_s = nullptr;
+  double* d_d = nullptr;
+  size_t scratch_elems = 0;
+  // motion-vector upload ring (pinned host -> device), one slot per step
+  static constexpr int kRing = 32;
+  double* h_motion = nullptr;  // pinned, kRing * cap * 2
+  double* d_motion = nullptr;  // device, kRing * cap * 2
+  cudaEvent_t ring_ev[kRing] = {};
+  int ring_cap = 0;
+  int ring_next = 0;
+  // pinned scalars for status read-back
+  glb::DeviceBlock* h_block = nullptr;
+  // misc device scratch for reductions / dither
+  void* d_misc = nullptr;
+  size_t misc_bytes = 0;
+  void* h_misc = nullptr;  // pinned mirror of d_misc
+  size_t h_misc_bytes = 0;
+};
+
+struct gl_map {
+  int w = 0, h = 0;
+  double res = 0.1, ox = 0.0, oy = 0.0;
+  int free_count = 0;
+  std::vector<uint8_t> occ;  // host copy, 1 = occupied
+  uint8_t* d_occ = nullptr;
+  int device = 0;
+};
+
+struct gl_field {
+  int w = 0, h = 0;
+  std::vector<double> values;  // meters
+  double* d_values = nullptr;
+};
+
+struct gl_kernels {
+  gl_kernel_info info{};
+  std::vector<double> sep;
+  std::vector<double> spatial;  // channels*(2r+1)^2
+  std::vector<int> ang_off;
+  std::vector<double> ang_w;
+  // device copies (lazily uploaded per device)
+  int device = -1;
+  double* d_spatial = nullptr;
+  int* d_ang_off = nullptr;
+  double* d_ang_w = nullptr;
+};
+
+struct gl_activation {
+  int w = 0, h = 0, channels = 0;
+  bool k_invariant = false;  // one W*H plane serves every channel
+  double* d_values = nullptr;
+  double* d_inverse = nullptr;
+};
+
+struct gl_tensor {
+  int w = 0, h = 0, c = 0;
+  double cell = 0.1, ox = 0.0, oy = 0.0;
+  double theta_t = 0.0;
+  double* d_buf[2] = {nullptr, nullptr};
+  int cur = 0;
+  glb::DeviceBlock* d_block = nullptr;
+  int device = 0;
+  CUtensorMap tmap[2];  // 3-D TMA descriptors over d_buf[0/1]
+  bool tmap_ok = false;
+};
+
+// ---------------------------------------------------------------- launchers
+// (defined in the .cu files; all enqueue on ctx->stream)
+namespace glb {
+
+struct SepTaps {
+  double t[kMaxSepTaps];
+};
+
+struct StepArgs {
+  const double* src;       // input buffer (C planes)
+  double* dst;             // output buffer
+  const BufState* src_state;
+  BufState* dst_state;
+  StepState* step_state;
+  const double2* motion;   // per channel (dx, dy) in cells
+  const uint8_t* occ;
+  const double* inv;       // activation inverse
+  int inv_per_channel;     // 0: one plane for all k
+  int w, h, c;
+};
+
+// k_generic.cu
+void launch_shift_mask(gl_context* ctx, const StepArgs& a, double* S, int mode);
+void launch_conv_separable(gl_context* ctx, const double* S, double* tmp,
+                           double* D, int w, int h, int c, const SepTaps& taps,
+                           int r);
+void launch_conv_dense(gl_context* ctx, const double* S, double* D, int w,
+                       int h, int c, const double* d_spatial, int r,
+                       int kernel_channels);
+void launch_angular(gl_context* ctx, const StepArgs& a, const double* D,
+                    const int* d_off, const double* d_w, int n_ang);
+void launch_step_finalize(gl_context* ctx, const StepArgs& a);
+void launch_apply_scale(gl_context* ctx, double* buf, size_t n,
+                        BufState* state);
+void launch_fill(gl_context* ctx, double* buf, size_t n, double v);
+void launch_init_uniform(gl_context* ctx, double* buf, const uint8_t* occ,
+                         int w, int h, int c);
+void launch_make_activation(gl_context* ctx, const uint8_t* occ, int w, int h,
+                            int c, const gl_kernels* k, double* values,
+                            double* inverse, bool k_invariant, double* scratch);
+void launch_belief_map(gl_context* ctx, const double* buf, int w, int h,
+                       int c, double* out);
+size_t argmax_scratch_bytes(size_t n);
+void launch_argmax(gl_context* ctx, const double* buf, size_t n,
+                   void* d_scratch, size_t scratch_bytes, void* d_out);
+void launch_hash(gl_context* ctx, const double* buf, size_t n,
+                 unsigned long long* d_out);
+void launch_plane_max(gl_context* ctx, const double* buf, size_t n,
+                      unsigned long long* d_gmax);
+
+// k_fused.cu
+bool fused_supported(int r, const AngTaps& ang, int c);
+void fused_box(int r, int H, int* bw, int* bh);
+void launch_fused_step(gl_context* ctx, const StepArgs& a,
+                       const CUtensorMap* tmap, const double* sep, int r,
+                       const AngTaps& ang);
+
+// k_observe.cu
+void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
+                   int* d_cells, int cap, int* d_n, double* d_mass);
+void launch_likelihoods(gl_context* ctx, const uint8_t* occ, const double* score,
+                        double oob_score, int w, int h, double res, double ox,
+                        double oy, double cell, double tox, double toy,
+                        const int* d_samples, int n, int c,
+                        const double2* d_dir, int n_scored,
+                        const double* d_reach, double floor_w, double* d_L);
+void launch_observe_apply(gl_context* ctx, double* buf, int w, int h, int c,
+                          const int* d_samples, int n, const double* d_L,
+                          double* d_mean);
+void launch_observe_finalize(gl_context* ctx, StepState* st, BufState* buf);
+
+}  // namespace glb

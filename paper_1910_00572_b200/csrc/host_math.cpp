@@ -1,0 +1,289 @@
+// Host-side setup math of the filter: everything that calls libm
+// transcendentals (exp, cos, sin) runs here, on the host, exactly where the
+// reference evaluates it, so taps, motion vectors and likelihood tables are
+// bit-identical to the reference on the same host. Compiled with
+// -ffp-contract=off (no FMA contraction), like the reference build.
+#include <algorithm>
+#include <cctype>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <stdexcept>
+
+#include "gl_internal.hpp"
+#include "host_math.hpp"
+
+namespace glb {
+
+// --------------------------------------------------------------- kernels
+// Restates build_kernels (belief_tensor.cpp:243-338):
+//   spatial: sigma below 0.1 cell -> impulse (r = 0); isotropic -> separable
+//   normalised 1-D Gaussian with r = max(1, ceil(3 sigma)); otherwise one
+//   rotated anisotropic (2r+1)^2 Gaussian per channel at phi = k*dtheta.
+//   angular: sa = sigma_theta/dtheta; impulse below 0.1; h = max(1,ceil(3sa))
+//   taps -h..h, folded mod C when 2h+1 >= C.
+HostKernels build_kernels_host(double sigma_x, double sigma_y,
+                               double sigma_theta, int channels, double cell,
+                               double dtheta) {
+  if (!(sigma_x > 0.0 && sigma_y > 0.0 && sigma_theta > 0.0)) {
+    throw std::invalid_argument("motion noise sigmas must be > 0");
+  }
+  if (channels < 1) throw std::invalid_argument("channels must be >= 1");
+  HostKernels ks;
+  ks.channels = channels;
+  const double sx = sigma_x / cell;
+  const double sy = sigma_y / cell;
+  const double smax = std::max(sx, sy);
+  auto gauss1 = [](int d, double s) { return std::exp(-0.5 * d * d / (s * s)); };
+
+  if (smax < 0.1) {
+    ks.radius = 0;
+    ks.degenerate_spatial = true;
+    ks.spatial.assign(static_cast<size_t>(channels), 1.0);
+  } else if (sx == sy) {
+    const int r = std::max(1, static_cast<int>(std::ceil(3.0 * smax)));
+    ks.radius = r;
+    ks.separable = true;
+    ks.sep.resize(2 * r + 1);
+    double total = 0.0;
+    for (int t = 0; t < 2 * r + 1; ++t) {
+      ks.sep[t] = gauss1(t - r, sx);
+      total += ks.sep[t];
+    }
+    for (double& t : ks.sep) t /= total;
+    const int kw = 2 * r + 1;
+    ks.spatial.resize(static_cast<size_t>(channels) * kw * kw);
+    for (int k = 0; k < channels; ++k) {
+      double* dst = ks.spatial.data() + static_cast<size_t>(k) * kw * kw;
+      for (int a = 0; a < kw; ++a)
+        for (int b = 0; b < kw; ++b) dst[a * kw + b] = ks.sep[a] * ks.sep[b];
+    }
+  } else {
+    const int r = std::max(1, static_cast<int>(std::ceil(3.0 * smax)));
+    ks.radius = r;
+    const int kw = 2 * r + 1;
+    ks.spatial.resize(static_cast<size_t>(channels) * kw * kw);
+    for (int k = 0; k < channels; ++k) {
+      const double phi = k * dtheta;
+      const double c = std::cos(phi);
+      const double s = std::sin(phi);
+      double* dst = ks.spatial.data() + static_cast<size_t>(k) * kw * kw;
+      double total = 0.0;
+      for (int dy = -r; dy <= r; ++dy) {
+        for (int dx = -r; dx <= r; ++dx) {
+          const double bu = dx * c + dy * s;
+          const double bv = -dx * s + dy * c;
+          const double e =
+              std::exp(-0.5 * (bu * bu / (sx * sx) + bv * bv / (sy * sy)));
+          dst[(dy + r) * kw + (dx + r)] = e;
+          total += e;
+        }
+      }
+      for (int t = 0; t < kw * kw; ++t) dst[t] /= total;
+    }
+  }
+
+  const double sa = sigma_theta / dtheta;
+  if (sa < 0.1) {
+    ks.degenerate_angular = true;
+    ks.ang_off = {0};
+    ks.ang_w = {1.0};
+  } else {
+    const int hh = std::max(1, static_cast<int>(std::ceil(3.0 * sa)));
+    if (2 * hh + 1 >= channels) {
+      std::vector<double> bins(static_cast<size_t>(channels), 0.0);
+      double total = 0.0;
+      for (int dk = -hh; dk <= hh; ++dk) {
+        const double e = gauss1(dk, sa);
+        bins[((dk % channels) + channels) % channels] += e;
+        total += e;
+      }
+      for (int off = 0; off < channels; ++off) {
+        ks.ang_off.push_back(off);
+        ks.ang_w.push_back(bins[off] / total);
+      }
+    } else {
+      double total = 0.0;
+      for (int dk = -hh; dk <= hh; ++dk) total += gauss1(dk, sa);
+      for (int dk = -hh; dk <= hh; ++dk) {
+        ks.ang_off.push_back(dk);
+        ks.ang_w.push_back(gauss1(dk, sa) / total);
+      }
+    }
+  }
+  return ks;
+}
+
+// motion_vector (belief_tensor.cpp:55-62) for every channel of a step:
+// (dx, dy) in cells, with theta_t before the step's rotation is applied.
+void motion_table(double u, double v, int c_begin, int count, double theta_t,
+                  double dtheta, double cell, double* out_xy) {
+  for (int q = 0; q < count; ++q) {
+    const int k = c_begin + q;
+    const double angle = k * dtheta + theta_t;
+    const double c = std::cos(angle);
+    const double s = std::sin(angle);
+    out_xy[2 * q] = (c * u - s * v) / cell;
+    out_xy[2 * q + 1] = (s * u + c * v) / cell;
+  }
+}
+
+// ------------------------------------------------------------------ maps
+namespace {
+
+struct Cursor {
+  const uint8_t* b;
+  size_t n;
+  size_t pos;
+  // whitespace and '#' comments between header tokens
+  void skip() {
+    while (pos < n) {
+      if (b[pos] == '#') {
+        while (pos < n && b[pos] != '\n') ++pos;
+      } else if (std::isspace(b[pos])) {
+        ++pos;
+      } else {
+        break;
+      }
+    }
+  }
+  bool integer(long* out) {
+    skip();
+    if (pos >= n || !std::isdigit(b[pos])) return false;
+    long v = 0;
+    while (pos < n && std::isdigit(b[pos])) {
+      v = v * 10 + (b[pos] - '0');
+      if (v > std::numeric_limits<int>::max()) return false;
+      ++pos;
+    }
+    *out = v;
+    return true;
+  }
+};
+
+}  // namespace
+
+// load_map (occupancy_map.cpp:148-165) with decode_pgm (:84-145) and the
+// OccupancyMap boundary ring (:32-40).
+MapParse parse_pgm_map(const uint8_t* bytes, size_t n, int threshold) {
+  if (threshold <= 0 || threshold >= 255) {
+    throw std::invalid_argument("threshold must be in (0, 255)");
+  }
+  MapParse m;
+  auto fail = [](const char* why) { return MapParseFailure(why); };
+  if (n >= 8 && bytes[0] == 0x89 && bytes[1] == 'P' && bytes[2] == 'N' &&
+      bytes[3] == 'G') {
+    throw fail("PNG maps are not supported by gridloc_b200 (convert to PGM)");
+  }
+  if (n < 2 || bytes[0] != 'P' || (bytes[1] != '2' && bytes[1] != '5')) {
+    throw fail("not a P2/P5 PGM (bad magic)");
+  }
+  Cursor cur{bytes, n, 2};
+  long w = 0, h = 0, maxval = 0;
+  if (!cur.integer(&w) || !cur.integer(&h) || !cur.integer(&maxval)) {
+    throw fail("expected integer in PGM header");
+  }
+  if (w == 0 || h == 0) throw fail("PGM with zero dimension");
+  if (maxval <= 0 || maxval > 255) throw fail("PGM maxval unsupported; need 1..255");
+  const size_t cells = static_cast<size_t>(w) * static_cast<size_t>(h);
+  std::vector<uint8_t> gray(cells);
+  if (bytes[1] == '5') {
+    if (cur.pos >= n || !std::isspace(bytes[cur.pos])) {
+      throw fail("missing separator before P5 raster");
+    }
+    ++cur.pos;
+    if (n - cur.pos < cells) throw fail("P5 raster truncated");
+    std::memcpy(gray.data(), bytes + cur.pos, cells);
+  } else {
+    for (size_t q = 0; q < cells; ++q) {
+      long v = 0;
+      if (!cur.integer(&v)) throw fail("P2 raster truncated");
+      if (v > maxval) throw fail("P2 sample exceeds maxval");
+      gray[q] = static_cast<uint8_t>(v);
+    }
+  }
+  m.w = static_cast<int>(w);
+  m.h = static_cast<int>(h);
+  m.occ.resize(cells);
+  for (size_t q = 0; q < cells; ++q) {
+    int g = gray[q];
+    if (maxval != 255) g = static_cast<uint8_t>(g * 255L / maxval);
+    m.occ[q] = g >= threshold ? 0 : 1;
+  }
+  force_ring(m.occ.data(), m.w, m.h);
+  return m;
+}
+
+void force_ring(uint8_t* occ, int w, int h) {
+  for (int i = 0; i < w; ++i) {
+    occ[i] = 1;
+    occ[static_cast<size_t>(h - 1) * w + i] = 1;
+  }
+  for (int j = 0; j < h; ++j) {
+    occ[static_cast<size_t>(j) * w] = 1;
+    occ[static_cast<size_t>(j) * w + w - 1] = 1;
+  }
+}
+
+// distance_field (occupancy_map.cpp:231-271): per-column two-sweep run
+// lengths squared, then the Felzenszwalb-Huttenlocher lower envelope per
+// row, sqrt * resolution. Setup-time, host side (input to the likelihood
+// table, like the reference's field).
+std::vector<double> distance_field_host(const uint8_t* occ, int w, int h,
+                                        double res) {
+  std::vector<double> sq(static_cast<size_t>(w) * h);
+  const int far = w + h;
+  for (int i = 0; i < w; ++i) {
+    int run = far;
+    for (int j = 0; j < h; ++j) {
+      const size_t p = static_cast<size_t>(j) * w + i;
+      run = occ[p] ? 0 : std::min(far, run + 1);
+      sq[p] = run;
+    }
+    run = far;
+    for (int j = h - 1; j >= 0; --j) {
+      const size_t p = static_cast<size_t>(j) * w + i;
+      run = occ[p] ? 0 : std::min(far, run + 1);
+      const double c = std::min(sq[p], static_cast<double>(run));
+      sq[p] = c * c;
+    }
+  }
+  std::vector<double> f(w), d(w), z(w + 1);
+  std::vector<int> v(w);
+  const double inf = std::numeric_limits<double>::infinity();
+  for (int j = 0; j < h; ++j) {
+    double* row = sq.data() + static_cast<size_t>(j) * w;
+    std::copy(row, row + w, f.begin());
+    int k = 0;
+    v[0] = 0;
+    z[0] = -inf;
+    z[1] = inf;
+    for (int q = 1; q < w; ++q) {
+      double s;
+      for (;;) {
+        const int p = v[k];
+        s = ((f[q] + q * q) - (f[p] + p * p)) / (2.0 * q - 2.0 * p);
+        if (s <= z[k]) {
+          --k;
+        } else {
+          break;
+        }
+      }
+      ++k;
+      v[k] = q;
+      z[k] = s;
+      z[k + 1] = inf;
+    }
+    k = 0;
+    for (int q = 0; q < w; ++q) {
+      while (z[k + 1] < q) ++k;
+      const int p = v[k];
+      d[q] = (q - p) * (q - p) + f[p];
+    }
+    std::copy(d.begin(), d.end(), row);
+  }
+  for (double& x : sq) x = std::sqrt(x) * res;
+  return sq;
+}
+
+}  // namespace glb
