@@ -786,7 +786,10 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
     fail(GL_E_INVALID, "fused path requested but unsupported for this kernel set/grid");
   }
   if (fused) {
-    glb::launch_fused_step(ctx, a, tm, kernels->sep.data(), r, ang);
+    // r == 0 (impulse) kernels have no separable taps; the fused variant
+    // then skips the spatial passes entirely
+    const double one = 1.0;
+    glb::launch_fused_step(ctx, a, tm, r > 0 ? kernels->sep.data() : &one, r, ang);
   } else {
     const size_t n = elems_of(t);
     ensure_scratch(ctx, n);

@@ -97,7 +97,9 @@ template <int R, int ROWS>
 struct Geo {
   static constexpr int SW = TW + 2 * R;          // S tile width
   static constexpr int SH = ROWS + 2 * R;        // S tile height
-  static constexpr int BW = (TW + 2 * R + 1 + 1) & ~1;  // TMA box width (16B)
+  // TMA box width: TW+2R+1 source columns plus one for the even-aligned
+  // origin (TMA needs 16-B aligned inner coordinates), rounded to 16 B
+  static constexpr int BW = (TW + 2 * R + 1 + 1) & ~1;
   static constexpr int BH = ROWS + 2 * R + 1;    // TMA box height
   static constexpr int B_ELEMS = BW * BH;
   static constexpr uint32_t B_BYTES = B_ELEMS * 8;   // TMA transaction bytes
@@ -193,12 +195,16 @@ __global__ void __launch_bounds__(TW, 7)
                  const FusedParams p) {
   using G = Geo<R, ROWS>;
   constexpr int NG = 2 * H + 1;  // ring depth == angular taps
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* Bs = reinterpret_cast<double*>(smem_raw);              // NS boxes
+  extern __shared__ unsigned char smem_raw[];
+  // TMA destinations must be 128-B aligned: align the dynamic base by hand
+  unsigned char* smem_base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  double* Bs = reinterpret_cast<double*>(smem_base);             // NS boxes
   double* Ss = Bs + NS * G::STAGE;                             // 2 S tiles
   uint8_t* occ_sh = reinterpret_cast<uint8_t*>(Ss + (R > 0 ? 2 * G::S_ELEMS : 0));
   uint64_t* mbar = reinterpret_cast<uint64_t*>(
       (reinterpret_cast<uintptr_t>(occ_sh + G::S_ELEMS) + 15) & ~uintptr_t(15));
+  double* wmax = reinterpret_cast<double*>(mbar + NS);  // TW/32 warp maxima
 
   const int tid = threadIdx.x;
   const int x0 = blockIdx.x * TW;
@@ -212,7 +218,9 @@ __global__ void __launch_bounds__(TW, 7)
     const int kc = ((m % C) + C) % C;
     const ChanShift cs = chan_shift(p.motion[kc]);
     mbar_arrive_expect(&mbar[stage], G::B_BYTES);
-    tma_load_3d(Bs + stage * G::STAGE, &tmap, x0 - cs.sx - 1 - R,
+    // the innermost TMA coordinate must be 16-B aligned (an even double
+    // index): round the box origin down; the consumer skips the odd column
+    tma_load_3d(Bs + stage * G::STAGE, &tmap, (x0 - cs.sx - 1 - R) & ~1,
                 y0 - cs.sy - 1 - R, kc, &mbar[stage]);
   };
 
@@ -256,7 +264,7 @@ __global__ void __launch_bounds__(TW, 7)
       const int kc = ((m % C) + C) % C;
       const ChanShift cs = chan_shift(p.motion[kc]);
       mbar_wait(&mbar[stage], static_cast<uint32_t>((it / NS) & 1));
-      const double* Bb = Bs + stage * G::STAGE;
+      const double* Bb = Bs + stage * G::STAGE + ((x0 - cs.sx - 1 - R) & 1);
 
       if constexpr (R == 0) {
         // rotation-only kernels: no spatial diffusion, S == D
@@ -333,7 +341,6 @@ __global__ void __launch_bounds__(TW, 7)
   // global max -> last CTA finalises status and the pending rescale
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) vmax = dmax_ref(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
-  __shared__ double wmax[TW / 32];
   if ((tid & 31) == 0) wmax[tid >> 5] = vmax;
   __syncthreads();
   if (tid == 0) {
@@ -367,7 +374,7 @@ constexpr size_t smem_bytes() {
   using G = Geo<R, ROWS>;
   size_t b = NS * G::STAGE * 8 + (R > 0 ? 2 * G::S_ELEMS * 8 : 0) + G::S_ELEMS;
   b = (b + 15) & ~size_t(15);
-  return b + NS * 8;
+  return 128 + b + NS * 8 + (TW / 32) * 8;  // + alignment slack
 }
 
 template <int R, int H, int ROWS, int NS>
