@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""bench.py — belief updates/sec of the FP64 Algorithm-1 step on B200.
+
+Metric (BASELINE.json): belief updates per second (Hz) — step() calls per
+second — at 1024x1024x72 (configs[1], the single-GPU headline), with the HBM
+GB/s of the fused step kernel against the measured peak.
+
+One "step" is gridloc::step (belief_tensor.cpp:396-498) on the resident FP64
+tensor, driven by the reference's own benchmark stream (cmd_bench,
+gridloc_main.cpp:207-233: u = (res, 0, 0), main kernels, every step).
+
+  value  : steps/s with the tensor resident in HBM (async gl_step_async,
+           device time between CUDA events on the library stream, max over
+           ranks); the tensor (604 MB) exceeds L2 (126 MB), so every step
+           streams it from HBM.
+  e2e    : the same metric through the synchronous C-ABI call a user makes
+           (gl_step: host motion table -> device in the launch, status
+           read back to the host every step), wall clock.
+  roofline: algorithmic bytes per launch (2*8*W*H*C + W*H + 8*W*H) / the
+           fused kernel's average CUDA-event duration over the timed region.
+  cpu_baseline: the reference itself (oracle/_ref, compiled from the
+           reference sources) on this host's cores, bounded sample.
+
+--impl reference runs the reference's CPU implementation of the same path
+(oracle/_ref; rank 0 only under torchrun) and prints the same line.
+N > 1: independent replicas per rank (weak scaling), no data-path collective.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c2": dict(W=1024, H=1024, C=72, workload="1024x1024x72 floor-plan, odometry+map correction, 1 B200 "
+                                              "(BASELINE configs[1]); cmd_bench translation stream u=(res,0,0)"),
+    "c1": dict(W=256, H=256, C=36, workload="256x256x36 floor-plan, odometry+map only (BASELINE configs[0])"),
+    "c5": dict(W=512, H=512, C=72, workload="512x512x72 floor-plan (BASELINE configs[4], one robot)"),
+    "c4s": dict(W=2048, H=2048, C=360, workload="2048x2048x360 floor-plan (config-4 angular width, 1/4 area)"),
+}
+METRIC = "belief updates/sec (Hz) at 1024^2x72"
+HBM_FALLBACK = 6650.0
+
+
+def algo_bytes(W, H, C):
+    """read + write the FP64 belief, the uint8 occupancy and
+    the k-invariant FP64 activation inverse plane (isotropic kernels)."""
+    return 2 * 8 * W * H * C + W * H + 8 * W * H
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+def ncu_traffic(cfg_key):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the fused
+    kernel from the committed ncu --set full capture (profiles/)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(cfg_key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x20: "sync_boost", 0x40: "sw_thermal_slowdown", 0x80: "hw_thermal_slowdown",
+               0x100: "hw_power_brake_slowdown", 0x200: "display_clock"}
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                bits = int(parts[2], 16)
+            except ValueError:
+                continue
+            for b, name in self.REASONS.items():
+                if bits & b:
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(impl):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if impl == "ours":
+            import torch
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    return world, rank, local
+
+
+def dist_max(x, world, impl):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))) if impl == "ours" else torch.device("cpu")
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def dist_barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def make_map_bytes(W, H):
+    from paper_1910_00572_b200.floorplan import make_floorplan, write_pgm
+    return write_pgm(make_floorplan(W, H, seed=0))
+
+
+# ---------------------------------------------------------------- CPU legs
+def reference_engine(pgm, C, threads=0):
+    import oracle
+    if not oracle.ref_available():
+        return None, None
+    ref = oracle.Ref()
+    rm = oracle.RefMap(ref, pgm=pgm)
+    eng = oracle.RefEngine(ref, rm, C, threads=threads, rot_slot=False)
+    return eng, rm
+
+
+def cpu_baseline(pgm, cfg, budget_s=12.0, max_steps=200):
+    """The reference's step() (oracle/_ref) on all host cores, bounded sample."""
+    eng, _ = reference_engine(pgm, cfg["C"])
+    if eng is None:
+        return None
+    eng.step(0.1, 0.0, 0.0)  # first step allocates scratch (excluded, like §6)
+    n = 0
+    t0 = time.perf_counter()
+    while n < max_steps and time.perf_counter() - t0 < budget_s:
+        rc = eng.step(0.1, 0.0, 0.0)
+        if rc:
+            break
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "Hz", "cores": eng.threads, "kind": "reference",
+            "sample": f"{n} reference step() calls on {cfg['W']}x{cfg['H']}x{cfg['C']} after 1 warm-up step, "
+                      f"ThreadPool({eng.threads}), {dt:.1f} s"}
+
+
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return 0
+    pgm = make_map_bytes(cfg["W"], cfg["H"])
+    eng, _ = reference_engine(pgm, cfg["C"])
+    if eng is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (reference sources absent)"}))
+        return 0
+    for _ in range(max(1, args.warmup)):
+        eng.step(0.1, 0.0, 0.0)
+    budget = args.ref_budget_s
+    n = 0
+    t0 = time.perf_counter()
+    while n < args.steps and time.perf_counter() - t0 < budget:
+        eng.step(0.1, 0.0, 0.0)
+        n += 1
+    dt = time.perf_counter() - t0
+    hz = n / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": hz, "unit": "Hz", "n_gpus": world, "steps": n,
+        "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(n, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "W": cfg["W"], "H": cfg["H"], "channels": cfg["C"],
+                   "parallelism": f"ThreadPool({eng.threads}) host threads"},
+        "cpu_baseline": {"value": hz, "unit": "Hz", "cores": eng.threads, "kind": "reference",
+                         "sample": f"{n} reference step() calls after {args.warmup} warm-up, {dt:.1f} s "
+                                   f"(capped at {budget:.0f} s)"},
+        "e2e": {"value": hz, "unit": "Hz", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------- ours
+def run_ours(args, cfg, world, rank, local):
+    import paper_1910_00572_b200 as g
+    W, H, C = cfg["W"], cfg["H"], cfg["C"]
+    ctx = g.Context(local)
+    pgm = make_map_bytes(W, H)
+    m = g.load_map(pgm, 250, 0.1, ctx=ctx)
+    ks = g.build_kernels(g.MotionNoise(), C, m.resolution(), 2.0 * math.pi / C)
+    act = g.make_activation(m, ks, C, ctx)
+    t = g.init_uniform(m, C, ctx)
+    u = g.OdometryDelta(m.resolution(), 0.0, 0.0)  # gridloc_main.cpp:221
+
+    for _ in range(args.warmup):
+        g.step_async(t, u, m, ks, act, ctx)
+    ctx.synchronize()
+    g.tensor_status(t)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    dist_barrier(world)
+    ctx.synchronize()
+    n0 = ctx.launch_count()
+    ctx.time_steps(True)
+    ctx.mark(0)
+    for _ in range(args.steps):
+        g.step_async(t, u, m, ks, act, ctx)
+    ctx.mark(1)
+    ms = ctx.marks_ms(0, 1)
+    ctx.synchronize()
+    launches = ctx.launch_count() - n0
+    kern_ms, kern_n = ctx.step_times()
+    ctx.time_steps(False)
+    clk = clocks.stop()
+    g.tensor_status(t)  # raises BeliefExtinguishedError like the reference
+    ms_max = dist_max(ms, world, "ours")
+    value = world * args.steps / (ms_max / 1e3)
+
+    # e2e: synchronous C-ABI step per call (host motion table in, status out)
+    n_e2e = max(1, min(args.steps, args.e2e_steps))
+    dist_barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        g.step(t, u, m, ks, act, ctx)
+    e2e_s = time.perf_counter() - t0
+    e2e_s = dist_max(e2e_s, world, "ours")
+    e2e = world * n_e2e / e2e_s
+
+    bytes_launch = algo_bytes(W, H, C)
+    avg_kern_s = (kern_ms / max(kern_n, 1)) / 1e3
+    achieved = bytes_launch / avg_kern_s / 1e9
+    peak, peak_src = measured_peak()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(pgm, cfg, budget_s=args.cpu_budget_s)
+    if rank != 0:
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": "Hz", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "W": W, "H": H, "channels": C,
+                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (one per GPU)",
+                   "l2": "belief tensor (604 MB at 1024^2x72) exceeds the 126 MB L2: every step streams it from HBM",
+                   "noise": [0.03, 0.03, 0.012], "kernel_path": "fused sm_100a TMA step"},
+        "e2e": {"value": e2e, "unit": "Hz", "h2d_bytes_per_step": 16 * C, "d2h_bytes_per_step": 16,
+                "how": f"{n_e2e} synchronous gl_step calls (motion table H2D in the launch, status D2H), wall clock"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(args.config), "peak_source": peak_src,
+                     "bytes_per_launch": bytes_launch, "avg_kernel_ms": avg_kern_s * 1e3, "launches_timed": kern_n},
+        "cpu_baseline": cpu,
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--e2e-steps", type=int, default=500)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--ref-budget-s", type=float, default=90.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    world, rank, local = dist_setup(args.impl)
+    try:
+        if args.impl == "reference":
+            return run_reference(args, cfg, world, rank)
+        return run_ours(args, cfg, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -65,6 +65,18 @@ enum { GL_PATH_AUTO = 0, GL_PATH_FUSED = 1, GL_PATH_GENERIC = 2 };
 gl_status gl_context_set_path(gl_context* ctx, int path);
 /* Number of kernels this context launched since creation. */
 gl_status gl_context_launch_count(gl_context* ctx, uint64_t* n);
+/* The context's cudaStream_t, as an opaque pointer (for NCCL / events). */
+gl_status gl_context_stream(gl_context* ctx, void** stream);
+/* Per-launch device timing of the step kernels: when enabled, every step
+ * kernel is bracketed by CUDA events on the context stream; *_times
+ * synchronises and returns the summed duration and count since the last
+ * call (then resets). */
+gl_status gl_context_time_steps(gl_context* ctx, int enable);
+gl_status gl_context_step_times(gl_context* ctx, double* total_ms, int* count);
+/* Region timing on the context stream: record marker i (0..15), then read
+ * the device time between two markers (synchronises). */
+gl_status gl_context_mark(gl_context* ctx, int i);
+gl_status gl_context_marks_ms(gl_context* ctx, int i, int j, double* ms);
 
 /* ---- maps ------------------------------------------------------------- */
 /* load_map (occupancy_map.hpp:106-108, occupancy_map.cpp:148-165): PGM P2/P5

@@ -65,6 +65,11 @@ SIGNATURES = {
     "gl_context_last_step_ms": [_vp, _dp],
     "gl_context_set_path": [_vp, C.c_int],
     "gl_context_launch_count": [_vp, C.POINTER(C.c_uint64)],
+    "gl_context_stream": [_vp, _pvp],
+    "gl_context_time_steps": [_vp, C.c_int],
+    "gl_context_step_times": [_vp, _dp, _ip],
+    "gl_context_mark": [_vp, C.c_int],
+    "gl_context_marks_ms": [_vp, C.c_int, C.c_int, _dp],
     "gl_load_map": [_u8p, C.c_size_t, C.c_int, _ip, _ip, _u8p],
     "gl_map_create": [_vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, _u8p, _pvp],
     "gl_map_destroy": [_vp],

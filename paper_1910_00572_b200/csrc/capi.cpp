@@ -316,6 +316,7 @@ gl_status gl_context_destroy(gl_context* ctx) {
     if (ctx->d_misc) cudaFree(ctx->d_misc);
     if (ctx->h_misc) cudaFreeHost(ctx->h_misc);
     for (auto& e : ctx->ring_ev) cudaEventDestroy(e);
+    for (auto& e : ctx->tev) cudaEventDestroy(e);
     cudaEventDestroy(ctx->ev_begin);
     cudaEventDestroy(ctx->ev_end);
     cudaStreamDestroy(ctx->stream);
@@ -333,10 +334,68 @@ gl_status gl_context_synchronize(gl_context* ctx) {
 gl_status gl_context_last_step_ms(gl_context* ctx, double* ms) {
   return guard([&] {
     need(ctx && ms, "null argument");
-    CK(cudaEventSynchronize(ctx->ev_end));
+    need(ctx->ev_end_last != nullptr, "no step has run on this context");
+    CK(cudaEventSynchronize(ctx->ev_end_last));
     float f = 0.f;
-    CK(cudaEventElapsedTime(&f, ctx->ev_begin, ctx->ev_end));
+    CK(cudaEventElapsedTime(&f, ctx->ev_begin_last, ctx->ev_end_last));
     *ms = f;
+  });
+}
+
+gl_status gl_context_mark(gl_context* ctx, int i) {
+  return guard([&] {
+    need(ctx && i >= 0 && i < 16, "bad marker");
+    DeviceGuard g(ctx->device);
+    if (!ctx->marks[i]) CK(cudaEventCreate(&ctx->marks[i]));
+    CK(cudaEventRecord(ctx->marks[i], ctx->stream));
+  });
+}
+
+gl_status gl_context_marks_ms(gl_context* ctx, int i, int j, double* ms) {
+  return guard([&] {
+    need(ctx && ms && i >= 0 && i < 16 && j >= 0 && j < 16, "bad marker");
+    need(ctx->marks[i] && ctx->marks[j], "marker not recorded");
+    CK(cudaEventSynchronize(ctx->marks[j]));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, ctx->marks[i], ctx->marks[j]));
+    *ms = f;
+  });
+}
+
+gl_status gl_context_stream(gl_context* ctx, void** stream) {
+  return guard([&] {
+    need(ctx && stream, "null argument");
+    *stream = reinterpret_cast<void*>(ctx->stream);
+  });
+}
+
+gl_status gl_context_time_steps(gl_context* ctx, int enable) {
+  return guard([&] {
+    need(ctx, "null context");
+    DeviceGuard g(ctx->device);
+    if (enable && ctx->tev.empty()) {
+      ctx->tev.resize(2 * gl_context::kTimers);
+      for (auto& e : ctx->tev) CK(cudaEventCreate(&e));
+    }
+    ctx->timing = enable != 0;
+    ctx->tcount = 0;
+  });
+}
+
+gl_status gl_context_step_times(gl_context* ctx, double* total_ms, int* count) {
+  return guard([&] {
+    need(ctx && total_ms && count, "null argument");
+    DeviceGuard g(ctx->device);
+    CK(cudaStreamSynchronize(ctx->stream));
+    double tot = 0.0;
+    for (int q = 0; q < ctx->tcount; ++q) {
+      float f = 0.f;
+      CK(cudaEventElapsedTime(&f, ctx->tev[2 * q], ctx->tev[2 * q + 1]));
+      tot += f;
+    }
+    *total_ms = tot;
+    *count = ctx->tcount;
+    ctx->tcount = 0;
   });
 }
 
@@ -759,9 +818,6 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
   a.h = t->h;
   a.c = t->c;
 
-  CK(cudaEventRecord(ctx->ev_begin, ctx->stream));
-  a.motion = upload_motion(ctx, t, u, v);
-
   const int r = kernels->info.radius;
   glb::AngTaps ang{};
   bool fused = ctx->path != GL_PATH_GENERIC &&
@@ -785,6 +841,19 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
   if (ctx->path == GL_PATH_FUSED && !fused) {
     fail(GL_E_INVALID, "fused path requested but unsupported for this kernel set/grid");
   }
+  // motion vectors (host libm): carried in the launch parameters on the
+  // fused path, otherwise uploaded through the pinned ring
+  thread_local std::vector<double> hm;
+  if (fused && t->c <= glb::kParamChannels) {
+    hm.resize(2 * static_cast<size_t>(t->c));
+    glb::motion_table(u, v, 0, t->c, t->theta_t, 2.0 * M_PI / t->c, t->cell, hm.data());
+    a.h_motion = hm.data();
+    a.motion = nullptr;
+  } else {
+    a.motion = upload_motion(ctx, t, u, v);
+  }
+  const int tslot = (ctx->timing && ctx->tcount < gl_context::kTimers) ? ctx->tcount++ : -1;
+  CK(cudaEventRecord(tslot >= 0 ? ctx->tev[2 * tslot] : ctx->ev_begin, ctx->stream));
   if (fused) {
     // r == 0 (impulse) kernels have no separable taps; the fused variant
     // then skips the spatial passes entirely
@@ -811,7 +880,14 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
     glb::launch_step_finalize(ctx, a);
   }
   CK(cudaGetLastError());
-  CK(cudaEventRecord(ctx->ev_end, ctx->stream));
+  CK(cudaEventRecord(tslot >= 0 ? ctx->tev[2 * tslot + 1] : ctx->ev_end, ctx->stream));
+  if (tslot >= 0) {
+    ctx->ev_begin_last = ctx->tev[2 * tslot];
+    ctx->ev_end_last = ctx->tev[2 * tslot + 1];
+  } else {
+    ctx->ev_begin_last = ctx->ev_begin;
+    ctx->ev_end_last = ctx->ev_end;
+  }
   t->cur = dst;
   t->theta_t = t->theta_t + w;  // belief_tensor.cpp:478
 }

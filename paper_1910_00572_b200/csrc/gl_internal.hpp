@@ -14,6 +14,7 @@
 namespace glb {
 
 constexpr int kMaxSepTaps = 63;      // separable taps held in kernel params
+constexpr int kParamChannels = 384;  // fused path: motion vectors ride in the launch params
 constexpr int kFusedMaxHalf = 3;     // fused path: angular offsets in [-3, 3]
 constexpr int kFusedMaxRadius = 2;   // fused path: separable radius <= 2 (or 0)
 
@@ -74,6 +75,13 @@ struct gl_context {
   size_t misc_bytes = 0;
   void* h_misc = nullptr;  // pinned mirror of d_misc
   size_t h_misc_bytes = 0;
+  // optional per-launch step timing (event pairs)
+  static constexpr int kTimers = 8192;
+  bool timing = false;
+  std::vector<cudaEvent_t> tev;  // 2 * kTimers
+  int tcount = 0;
+  cudaEvent_t ev_begin_last = nullptr, ev_end_last = nullptr;
+  cudaEvent_t marks[16] = {};
 };
 
 struct gl_map {
@@ -137,7 +145,8 @@ struct StepArgs {
   const BufState* src_state;
   BufState* dst_state;
   StepState* step_state;
-  const double2* motion;   // per channel (dx, dy) in cells
+  const double2* motion;   // per channel (dx, dy) in cells (device)
+  const double* h_motion;  // same table on the host (fused path: params)
   const uint8_t* occ;
   const double* inv;       // activation inverse
   int inv_per_channel;     // 0: one plane for all k

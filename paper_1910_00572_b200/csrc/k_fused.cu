@@ -81,7 +81,8 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map,
 
 struct FusedParams {
   double* dst;
-  const double2* motion;  // per channel (dx, dy), cells
+  const double2* motion;  // per channel (dx, dy), cells (when C > kParamChannels)
+  int param_motion;       // 1: motion vectors are in mv[] below
   const uint8_t* occ;
   const double* inv;
   int inv_per_k;
@@ -91,6 +92,7 @@ struct FusedParams {
   StepState* step_state;
   double sep[2 * kFusedMaxRadius + 1];
   double ang[2 * kFusedMaxHalf + 1];
+  double2 mv[kParamChannels];  // the step's motion table, carried by the launch
 };
 
 template <int R, int ROWS>
@@ -216,7 +218,7 @@ __global__ void __launch_bounds__(TW, 7)
   auto issue = [&](int it, int stage) {
     const int m = it - H;
     const int kc = ((m % C) + C) % C;
-    const ChanShift cs = chan_shift(p.motion[kc]);
+    const ChanShift cs = chan_shift(p.param_motion ? p.mv[kc] : p.motion[kc]);
     mbar_arrive_expect(&mbar[stage], G::B_BYTES);
     // the innermost TMA coordinate must be 16-B aligned (an even double
     // index): round the box origin down; the consumer skips the odd column
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(TW, 7)
       const int stage = it % NS;
       const int m = it - H;
       const int kc = ((m % C) + C) % C;
-      const ChanShift cs = chan_shift(p.motion[kc]);
+      const ChanShift cs = chan_shift(p.param_motion ? p.mv[kc] : p.motion[kc]);
       mbar_wait(&mbar[stage], static_cast<uint32_t>((it / NS) & 1));
       const double* Bb = Bs + stage * G::STAGE + ((x0 - cs.sx - 1 - R) & 1);
 
@@ -445,6 +447,10 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
   FusedParams fp{};
   fp.dst = a.dst;
   fp.motion = a.motion;
+  fp.param_motion = (a.c <= kParamChannels && a.h_motion != nullptr) ? 1 : 0;
+  if (fp.param_motion) {
+    for (int k = 0; k < a.c; ++k) fp.mv[k] = make_double2(a.h_motion[2 * k], a.h_motion[2 * k + 1]);
+  }
   fp.occ = a.occ;
   fp.inv = a.inv;
   fp.inv_per_k = a.inv_per_channel;

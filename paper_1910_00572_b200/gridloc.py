@@ -160,6 +160,31 @@ class Context:
         check(self.lib.gl_context_launch_count(self.h, C.byref(n)))
         return n.value
 
+    def stream(self) -> int:
+        s = C.c_void_p()
+        check(self.lib.gl_context_stream(self.h, C.byref(s)))
+        return s.value or 0
+
+    def mark(self, i: int):
+        """Record CUDA-event marker i on the context stream."""
+        check(self.lib.gl_context_mark(self.h, i))
+
+    def marks_ms(self, i: int, j: int) -> float:
+        ms = C.c_double()
+        check(self.lib.gl_context_marks_ms(self.h, i, j, C.byref(ms)))
+        return ms.value
+
+    def time_steps(self, enable: bool):
+        """Bracket every step kernel with CUDA events on the context stream."""
+        check(self.lib.gl_context_time_steps(self.h, int(enable)))
+
+    def step_times(self):
+        """(total ms, count) of the timed step kernels since the last call."""
+        tot = C.c_double()
+        n = C.c_int()
+        check(self.lib.gl_context_step_times(self.h, C.byref(tot), C.byref(n)))
+        return tot.value, n.value
+
     def __del__(self):
         try:
             if getattr(self, "h", None):
