@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgridloc_b200.so")
+LIB_PATH = os.environ.get("GRIDLOC_B200_LIB", os.path.join(HERE, "libgridloc_b200.so"))
 
 GL_OK = 0
 GL_E_EXTINGUISHED = 1

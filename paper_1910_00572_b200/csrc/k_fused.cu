@@ -1,21 +1,26 @@
 // Fused Algorithm-1 step for sm_100a: one launch reads the belief tensor
 // once and writes it once (belief_tensor.cpp:396-498 in a single pass).
 //
-// CTA = 64 threads (2 warps) owning a 64 x ROWS spatial tile and ALL
-// channels. Per channel m (m = -H .. C-1+H, circular):
+// Work unit = one WARP owning an OW x ROWS output tile (OW = 32 - 2R
+// columns) for ALL channels; a CTA holds NWARP independent warps. Lane l
+// computes the shifted/masked value S at column x0 - R + l, so the R
+// outermost lanes carry the horizontal halo and no shared-memory exchange or
+// block barrier is needed inside the channel loop. Per channel m
+// (m = -H .. C-1+H, circular):
 //   1. TMA (cp.async.bulk.tensor.3d) brings the channel's source box into
-//      shared memory. The box origin absorbs the integer part of the
-//      channel's motion vector, so the bilinear taps sit at fixed smem
-//      offsets; out-of-grid cells arrive as zeros (== the reference's
-//      "skip taps outside the grid"). NS-stage mbarrier pipeline.
-//   2. S = mask(shift(B)) for the tile plus an R-cell halo -> smem.
-//   3. Separable Gaussian: row pass from smem, column pass rolled over the
-//      thread's column in registers -> D_m (ROWS values per thread).
-//   4. D_m enters a (2H+1)-deep register ring; output channel k = m - H is
-//      out = sum_t w_t * D[k - off_t] (first tap initialises), masked,
-//      multiplied by the activation inverse, stored, and max-reduced.
+//      the warp's shared-memory stage. The box origin absorbs the integer
+//      part of the channel's motion vector, so the four bilinear taps sit at
+//      fixed offsets; out-of-grid cells arrive as zeros (== the reference's
+//      "skip taps outside the grid"). NS-stage mbarrier pipeline per warp.
+//   2. Rolling down the rows: S = mask(shift(B)) (2 smem loads per row), the
+//      row pass of the separable Gaussian from S(l-R..l+R) via warp shuffles,
+//      the column pass over a rolling window of row results -> D_m(row).
+//   3. As soon as D_m(row) exists, output channel k = m - H for that row is
+//      out = sum_t w_t * D[k - off_t] (first tap initialises) from a
+//      (2H+1)-slot register ring, masked, times the activation inverse,
+//      stored, max-reduced. Only 2H ring slots stay live across channels.
 // The last CTA turns the global max into the extinguish status and the
-// output buffer's pending 1/max rescale (see gl_internal.hpp: BufState).
+// output buffer's pending 1/max rescale (gl_internal.hpp: BufState).
 //
 // Built with --fmad=false; every arithmetic expression keeps the reference's
 // operand order, so the output is bit-identical to step().
@@ -26,11 +31,16 @@
 
 #include "gl_internal.hpp"
 
+#ifndef GL_FUSED_ROWS_H1
+#define GL_FUSED_ROWS_H1 8   // tile rows for angular half-width H <= 1
+#endif
+#ifndef GL_FUSED_MINB
+#define GL_FUSED_MINB 4      // min resident CTAs/SM -> register cap
+#endif
+
 namespace glb {
 
 namespace {
-
-constexpr int TW = 64;  // tile width == threads per CTA
 
 __device__ __forceinline__ double dmax_ref(double a, double b) {
   return (a < b) ? b : a;
@@ -55,6 +65,8 @@ __device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar,
       : "memory");
 }
 
+// Warp-uniform wait: the loop exits for all lanes together, so the code after
+// it is provably convergent (shuffles stay plain SHFL).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   do {
@@ -65,7 +77,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "=r"(done)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
-  } while (!done);
+  } while (!__all_sync(0xffffffffu, done));
 }
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map,
@@ -87,6 +99,7 @@ struct FusedParams {
   const double* inv;
   int inv_per_k;
   int w, h, c;
+  int tiles_x, n_tiles;
   const BufState* src_state;
   BufState* dst_state;
   StepState* step_state;
@@ -97,16 +110,15 @@ struct FusedParams {
 
 template <int R, int ROWS>
 struct Geo {
-  static constexpr int SW = TW + 2 * R;          // S tile width
-  static constexpr int SH = ROWS + 2 * R;        // S tile height
-  // TMA box width: TW+2R+1 source columns plus one for the even-aligned
-  // origin (TMA needs 16-B aligned inner coordinates), rounded to 16 B
-  static constexpr int BW = (TW + 2 * R + 1 + 1) & ~1;
-  static constexpr int BH = ROWS + 2 * R + 1;    // TMA box height
+  static constexpr int OW = 32 - 2 * R;     // output columns per warp
+  static constexpr int SH = ROWS + 2 * R;   // S rows per tile
+  // TMA box: 33 source columns (S columns -R..32-R need c0 and c1) plus one
+  // for the even-aligned origin (TMA needs 16-B aligned inner coordinates)
+  static constexpr int BW = 34;
+  static constexpr int BH = SH + 1;
   static constexpr int B_ELEMS = BW * BH;
-  static constexpr uint32_t B_BYTES = B_ELEMS * 8;   // TMA transaction bytes
+  static constexpr uint32_t B_BYTES = B_ELEMS * 8;    // TMA transaction bytes
   static constexpr int STAGE = (B_ELEMS + 15) & ~15;  // 128-B aligned stages
-  static constexpr int S_ELEMS = SW * SH;
 };
 
 // Per-channel bilinear weights from the motion vector (belief_tensor.cpp:
@@ -126,132 +138,107 @@ __device__ __forceinline__ ChanShift chan_shift(double2 mv) {
   s.w10 = ax * (1.0 - ay);
   s.w01 = (1.0 - ax) * ay;
   s.w11 = ax * ay;
-  // far-out shifts only ever read zeros; clamp keeps the int conversion sane
-  const double lim = 1073741824.0;
-  s.sx = static_cast<int>(fmin(fmax(fx, -lim), lim));
-  s.sy = static_cast<int>(fmin(fmax(fy, -lim), lim));
+  // cvt.rzi.s32.f64 saturates; far-out shifts only ever read zeros, and the
+  // integer clamp keeps the box-origin arithmetic free of overflow
+  s.sx = min(max(static_cast<int>(fx), -(1 << 29)), 1 << 29);
+  s.sy = min(max(static_cast<int>(fy), -(1 << 29)), 1 << 29);
   return s;
 }
 
-// One S cell from the four box taps: r0 = (lj+1), r1 = lj, c0 = (li+1),
-// c1 = li. Order w00, w10, w01, w11 from 0.0 (belief_tensor.cpp:112-120).
-template <bool SCALED>
-__device__ __forceinline__ double s_cell(const ChanShift& cs, double sc,
-                                         double r0c0, double r0c1, double r1c0,
+// integer part only (TMA box origin of a channel)
+__device__ __forceinline__ int2 chan_origin(double2 mv) {
+  return make_int2(min(max(static_cast<int>(floor(mv.x)), -(1 << 29)), 1 << 29),
+                   min(max(static_cast<int>(floor(mv.y)), -(1 << 29)), 1 << 29));
+}
+
+// One S value from the four taps: r0 = row j-sy, r1 = j-sy-1, c0 = i-sx,
+// c1 = i-sx-1; w00, w10, w01, w11 added to 0.0 in that order
+// (belief_tensor.cpp:112-120). Integral shifts copy r0c0 exactly (:71-86);
+// both forms are evaluated and selected, so there is no per-cell branch.
+__device__ __forceinline__ double s_cell(const ChanShift& cs, double r0c0,
+                                         double r0c1, double r1c0,
                                          double r1c1) {
-  if (SCALED) {
-    r0c0 = r0c0 * sc;
-    r0c1 = r0c1 * sc;
-    r1c0 = r1c0 * sc;
-    r1c1 = r1c1 * sc;
-  }
-  if (cs.integral) return r0c0;
   double acc = 0.0;
   acc += cs.w00 * r0c0;
   acc += cs.w10 * r0c1;
   acc += cs.w01 * r1c0;
   acc += cs.w11 * r1c1;
+  return cs.integral ? r0c0 : acc;
+}
+
+template <int R>
+__device__ __forceinline__ double row_pass(const FusedParams& p, double s) {
+  // acc = 0; acc += t[d+R] * S(i+d), d = -R..R (belief_tensor.cpp:211-214)
+  double nb[2 * R + 1];
+  nb[R] = s;
+#pragma unroll
+  for (int d = 1; d <= R; ++d) {
+    nb[R - d] = __shfl_up_sync(0xffffffffu, s, d);
+    nb[R + d] = __shfl_down_sync(0xffffffffu, s, d);
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int d = 0; d < 2 * R + 1; ++d) acc += p.sep[d] * nb[d];
   return acc;
 }
 
-template <int R, int ROWS, bool SCALED>
-__device__ __forceinline__ void compute_s_tile(
-    const double* __restrict__ Bb, double* __restrict__ Sb,
-    const uint8_t* __restrict__ occ_sh, const ChanShift& cs, double sc,
-    uint32_t own_mask, int tid) {
-  using G = Geo<R, ROWS>;
-  // own column li = tid + R, rolled down the rows: 2 new smem loads per row
-  const int li = tid + R;
-  double lo_c1 = Bb[li], lo_c0 = Bb[li + 1];  // box row 0 (= r1 of lj = 0)
-#pragma unroll
-  for (int lj = 0; lj < G::SH; ++lj) {
-    const double hi_c1 = Bb[(lj + 1) * G::BW + li];
-    const double hi_c0 = Bb[(lj + 1) * G::BW + li + 1];
-    double s = s_cell<SCALED>(cs, sc, hi_c0, hi_c1, lo_c0, lo_c1);
-    if ((own_mask >> lj) & 1u) s = 0.0;
-    Sb[lj * G::SW + li] = s;
-    lo_c1 = hi_c1;
-    lo_c0 = hi_c0;
-  }
-  if (R > 0) {
-    // halo columns [0, R) and [TW+R, TW+2R): 2R*SH cells, one per thread
-    constexpr int NH = 2 * R * G::SH;
-    for (int q = tid; q < NH; q += TW) {
-      const int side = q / (R * G::SH);
-      const int rem = q % (R * G::SH);
-      const int hc = rem / G::SH;
-      const int lj = rem % G::SH;
-      const int col = side == 0 ? hc : TW + R + hc;
-      double s = s_cell<SCALED>(cs, sc, Bb[(lj + 1) * G::BW + col + 1],
-                                Bb[(lj + 1) * G::BW + col],
-                                Bb[lj * G::BW + col + 1], Bb[lj * G::BW + col]);
-      if (occ_sh[lj * G::SW + col]) s = 0.0;
-      Sb[lj * G::SW + col] = s;
-    }
-  }
-}
-
 template <int R, int H, int ROWS, int NS>
-__global__ void __launch_bounds__(TW, 7)
-    k_fused_step(const __grid_constant__ CUtensorMap tmap,
-                 const FusedParams p) {
+__device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
+                                            const FusedParams& p, double* Bs,
+                                            uint64_t* mbar, int lane, int x0,
+                                            int y0, bool active) {
   using G = Geo<R, ROWS>;
   constexpr int NG = 2 * H + 1;  // ring depth == angular taps
-  extern __shared__ unsigned char smem_raw[];
-  // TMA destinations must be 128-B aligned: align the dynamic base by hand
-  unsigned char* smem_base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  double* Bs = reinterpret_cast<double*>(smem_base);             // NS boxes
-  double* Ss = Bs + NS * G::STAGE;                             // 2 S tiles
-  uint8_t* occ_sh = reinterpret_cast<uint8_t*>(Ss + (R > 0 ? 2 * G::S_ELEMS : 0));
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(occ_sh + G::S_ELEMS) + 15) & ~uintptr_t(15));
-  double* wmax = reinterpret_cast<double*>(mbar + NS);  // TW/32 warp maxima
-
-  const int tid = threadIdx.x;
-  const int x0 = blockIdx.x * TW;
-  const int y0 = blockIdx.y * ROWS;
   const int W = p.w, Hh = p.h, C = p.c;
   const size_t plane = static_cast<size_t>(W) * Hh;
   const int n_iter = C + 2 * H;
+  const bool scaled = p.src_state->scaled != 0;  // pending 1/max rescale
+  const double sc = p.src_state->scale;
 
-  auto issue = [&](int it, int stage) {
+  // circular channel of iteration it (m = it - H lies in [-H, C-1+H], H < C)
+  auto chan_of = [&](int it) {
     const int m = it - H;
-    const int kc = ((m % C) + C) % C;
-    const ChanShift cs = chan_shift(p.param_motion ? p.mv[kc] : p.motion[kc]);
+    return m < 0 ? m + C : (m >= C ? m - C : m);
+  };
+  auto motion_of = [&](int kc) { return p.param_motion ? p.mv[kc] : p.motion[kc]; };
+  auto issue = [&](int it, int stage) {
+    const int kc = chan_of(it);
+    const int2 o = chan_origin(motion_of(kc));
     mbar_arrive_expect(&mbar[stage], G::B_BYTES);
-    // the innermost TMA coordinate must be 16-B aligned (an even double
-    // index): round the box origin down; the consumer skips the odd column
-    tma_load_3d(Bs + stage * G::STAGE, &tmap, (x0 - cs.sx - 1 - R) & ~1,
-                y0 - cs.sy - 1 - R, kc, &mbar[stage]);
+    tma_load_3d(Bs + stage * G::STAGE, tmap, (x0 - R - o.x - 1) & ~1,
+                y0 - R - o.y - 1, kc, &mbar[stage]);
   };
 
-  if (tid == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  if (lane == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&mbar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < NS && s < n_iter; ++s) issue(s, s);
   }
-  // occupancy of the S tile (outside the grid counts as masked)
-  for (int q = tid; q < G::S_ELEMS; q += TW) {
-    const int lj = q / G::SW, li = q % G::SW;
-    const int i = x0 + li - R, j = y0 + lj - R;
-    occ_sh[q] = (i < 0 || i >= W || j < 0 || j >= Hh)
-                    ? 1
-                    : p.occ[static_cast<size_t>(j) * W + i];
-  }
-  const bool scaled = p.src_state->scaled != 0;
-  const double sc = scaled ? p.src_state->scale : 1.0;
-  __syncthreads();
+  __syncwarp();
 
-  // own column: S mask bits (lj) and output mask bits (row r = lj - R)
-  uint32_t own_mask = 0;
+  // Per-tile constants of this lane's column: S mask bits (occupied or
+  // outside the grid), store-valid bits, and the activation inverse of the
+  // output cells (one k-invariant plane on the fused path).
+  const int si = x0 - R + lane;
+  const bool col_in = si >= 0 && si < W;
+  uint32_t smask = 0;
 #pragma unroll
   for (int lj = 0; lj < G::SH; ++lj) {
-    own_mask |= static_cast<uint32_t>(occ_sh[lj * G::SW + tid + R] != 0) << lj;
+    const int j = y0 - R + lj;
+    const bool inside = col_in && j >= 0 && j < Hh;
+    const bool occ = !inside || p.occ[static_cast<size_t>(j) * W + si] != 0;
+    smask |= static_cast<uint32_t>(occ) << lj;
   }
-  const int gi = x0 + tid;
-  const bool col_in = gi < W;
+  const bool out_lane = active && lane >= R && lane < 32 - R && si < W;
+  double invr[ROWS];
+  uint32_t store_ok = 0;
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+    const bool ok = out_lane && (y0 + r) < Hh;
+    store_ok |= static_cast<uint32_t>(ok) << r;
+    invr[r] = ok ? __ldg(p.inv + static_cast<size_t>(y0 + r) * W + si) : 0.0;
+  }
+  double* const out_tile = p.dst + static_cast<size_t>(y0) * W + (out_lane ? si : 0);
 
   double ring[NG][ROWS];
   double vmax = 0.0;
@@ -263,97 +250,119 @@ __global__ void __launch_bounds__(TW, 7)
       if (it >= n_iter) break;
       const int stage = it % NS;
       const int m = it - H;
-      const int kc = ((m % C) + C) % C;
-      const ChanShift cs = chan_shift(p.param_motion ? p.mv[kc] : p.motion[kc]);
+      const ChanShift cs = chan_shift(motion_of(chan_of(it)));
+      double* stage_ptr = Bs + stage * G::STAGE;
       mbar_wait(&mbar[stage], static_cast<uint32_t>((it / NS) & 1));
-      const double* Bb = Bs + stage * G::STAGE + ((x0 - cs.sx - 1 - R) & 1);
+      if (scaled) {
+        // rare: the source buffer carries a pending rescale (stored values
+        // times sc are the reference's values), applied to the box in smem
+        for (int q = lane; q < G::B_ELEMS; q += 32) stage_ptr[q] = stage_ptr[q] * sc;
+        __syncwarp();
+      }
+      const double* Bb = stage_ptr + ((x0 - R - cs.sx - 1) & 1) + lane;
+      const bool emit = m >= H;
+      double* orow = out_tile + plane * (emit ? m - H : 0);  // advanced by W per row
 
-      if constexpr (R == 0) {
-        // rotation-only kernels: no spatial diffusion, S == D
-        const int li = tid;
-        double lo_c1 = Bb[li], lo_c0 = Bb[li + 1];
+      double lo_c0 = Bb[1], lo_c1 = Bb[0];
+      double rw[2 * R + 1];  // rolling window of row-pass results
 #pragma unroll
-        for (int r = 0; r < ROWS; ++r) {
-          const double hi_c1 = Bb[(r + 1) * G::BW + li];
-          const double hi_c0 = Bb[(r + 1) * G::BW + li + 1];
-          double s = scaled ? s_cell<true>(cs, sc, hi_c0, hi_c1, lo_c0, lo_c1)
-                            : s_cell<false>(cs, sc, hi_c0, hi_c1, lo_c0, lo_c1);
-          if ((own_mask >> r) & 1u) s = 0.0;
-          ring[u][r] = s;
-          lo_c1 = hi_c1;
-          lo_c0 = hi_c0;
-        }
-        __syncthreads();  // stage fully consumed
-        if (tid == 0 && it + NS < n_iter) issue(it + NS, stage);
-      } else {
-        double* Sb = Ss + (it & 1) * G::S_ELEMS;
-        if (scaled) {
-          compute_s_tile<R, ROWS, true>(Bb, Sb, occ_sh, cs, sc, own_mask, tid);
+      for (int lj = 0; lj < G::SH; ++lj) {
+        const double hi_c0 = Bb[(lj + 1) * G::BW + 1];
+        const double hi_c1 = Bb[(lj + 1) * G::BW];
+        double s = s_cell(cs, hi_c0, hi_c1, lo_c0, lo_c1);
+        s = ((smask >> lj) & 1u) ? 0.0 : s;
+        lo_c0 = hi_c0;
+        lo_c1 = hi_c1;
+        int r = -1;
+        double d = 0.0;
+        if constexpr (R == 0) {
+          r = lj;
+          d = s;
         } else {
-          compute_s_tile<R, ROWS, false>(Bb, Sb, occ_sh, cs, sc, own_mask, tid);
-        }
-        __syncthreads();  // S complete; stage fully consumed
-        if (tid == 0 && it + NS < n_iter) issue(it + NS, stage);
-        // row pass (belief_tensor.cpp:199-225) then column pass (:227-238)
-        const int li = tid + R;
-        double rr[G::SH];
 #pragma unroll
-        for (int lj = 0; lj < G::SH; ++lj) {
-          const double* srow = Sb + lj * G::SW + li - R;
-          double acc = 0.0;
-#pragma unroll
-          for (int d = 0; d < 2 * R + 1; ++d) acc += p.sep[d] * srow[d];
-          rr[lj] = acc;
+          for (int q = 0; q < 2 * R; ++q) rw[q] = rw[q + 1];
+          rw[2 * R] = row_pass<R>(p, s);
           if (lj >= 2 * R) {
-            const int r = lj - 2 * R;
+            // column pass: orow = 0; += t[d] * row(j+d) (:227-238)
             double col = 0.0;
 #pragma unroll
-            for (int d = 0; d < 2 * R + 1; ++d) col += p.sep[d] * rr[r + d];
-            ring[u][r] = col;
+            for (int q = 0; q < 2 * R + 1; ++q) col += p.sep[q] * rw[q];
+            r = lj - 2 * R;
+            d = col;
+          }
+        }
+        if (r >= 0) {
+          ring[u][r] = d;
+          if (emit) {
+            // angular taps, mask, x inverse, max (belief_tensor.cpp:454-474)
+            double o = p.ang[0] * ring[u][r];
+#pragma unroll
+            for (int t = 1; t < NG; ++t) o += p.ang[t] * ring[(u - t + NG) % NG][r];
+            const bool occ = (smask >> (r + R)) & 1u;
+            o = occ ? 0.0 : o * invr[r];
+            // the value of the max only feeds the <= 0 / < 1e-6 tests and
+            // 1/max, so fmax (NaN-ignoring, sign of zero irrelevant) matches
+            // the reference's std::max from 0.0 (belief_tensor.cpp:464-471)
+            vmax = fmax(vmax, o);
+            if ((store_ok >> r) & 1u) *orow = o;
+            orow += W;
           }
         }
       }
-
-      // output channel k = m - H (belief_tensor.cpp:440-475)
-      if (m >= H) {
-        const int k = m - H;
-        double* out = p.dst + plane * k;
-        const double* inv = p.inv + (p.inv_per_k ? plane * k : 0);
-#pragma unroll
-        for (int r = 0; r < ROWS; ++r) {
-          double o = p.ang[0] * ring[u][r];
-#pragma unroll
-          for (int t = 1; t < NG; ++t) o += p.ang[t] * ring[(u - t + NG) % NG][r];
-          const int gj = y0 + r;
-          if (col_in && gj < Hh) {
-            const size_t q = static_cast<size_t>(gj) * W + gi;
-            if ((own_mask >> (r + R)) & 1u) {
-              o = 0.0;
-            } else {
-              o = o * __ldg(inv + q);
-              vmax = (o > 0.0) ? dmax_ref(vmax, o) : vmax;
-            }
-            out[q] = o;
-          }
-        }
+      __syncwarp();  // every lane is done with this stage
+      if (lane == 0 && it + NS < n_iter) {
+        if (scaled) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(it + NS, stage);
       }
     }
   }
+  return vmax;
+}
 
-  // global max -> last CTA finalises status and the pending rescale
+template <int R, int H, int ROWS, int NS, int NWARP>
+__global__ void __launch_bounds__(32 * NWARP, GL_FUSED_MINB)
+    k_fused_step(const __grid_constant__ CUtensorMap tmap,
+                 const FusedParams p) {
+  using G = Geo<R, ROWS>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // TMA destinations must be 128-B aligned. Pad by an offset computed from
+  // the shared-window address, keeping the pointer in the shared space (so
+  // the compiler emits LDS with immediate offsets, not generic loads).
+  const uint32_t pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
+  double* stages = reinterpret_cast<double*>(smem_raw + pad);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  double* Bs = stages + warp * NS * G::STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + NWARP * NS * G::STAGE);
+  uint64_t* mbar = bars + warp * NS;
+  double* wmax = reinterpret_cast<double*>(bars + NWARP * NS);
+
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  }
+  // Surplus warps of the last CTA redo the last tile with stores disabled,
+  // so every warp runs the same control flow (the shuffles then compile to
+  // plain SHFL instead of the divergence-safe collective sequence).
+  const int tile_raw = blockIdx.x * NWARP + warp;
+  const bool active = tile_raw < p.n_tiles;
+  const int tile = active ? tile_raw : p.n_tiles - 1;
+  const int x0 = (tile % p.tiles_x) * G::OW;
+  const int y0 = (tile / p.tiles_x) * ROWS;
+  double vmax = warp_tile<R, H, ROWS, NS>(&tmap, p, Bs, mbar, lane, x0, y0, active);
+
+  // global max -> the last CTA finalises status and the pending rescale
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) vmax = dmax_ref(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
-  if ((tid & 31) == 0) wmax[tid >> 5] = vmax;
+  if (lane == 0) wmax[warp] = vmax;
   __syncthreads();
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     double bm = 0.0;
-    for (int q = 0; q < TW / 32; ++q) bm = dmax_ref(bm, wmax[q]);
+    for (int q = 0; q < NWARP; ++q) bm = dmax_ref(bm, wmax[q]);
     StepState* st = p.step_state;
     if (bm > 0.0) atomicMax(&st->gmax_bits, static_cast<unsigned long long>(__double_as_longlong(bm)));
     __threadfence();
-    const unsigned int total = gridDim.x * gridDim.y;
     const unsigned int prev = atomicAdd(&st->blocks_done, 1u);
-    if (prev == total - 1) {
+    if (prev == gridDim.x - 1) {
       __threadfence();
       const unsigned long long bits = atomicAdd(&st->gmax_bits, 0ull);
       const double g = __longlong_as_double(static_cast<long long>(bits));
@@ -371,19 +380,26 @@ __global__ void __launch_bounds__(TW, 7)
   }
 }
 
-template <int R, int ROWS, int NS>
-constexpr size_t smem_bytes() {
-  using G = Geo<R, ROWS>;
-  size_t b = NS * G::STAGE * 8 + (R > 0 ? 2 * G::S_ELEMS * 8 : 0) + G::S_ELEMS;
-  b = (b + 15) & ~size_t(15);
-  return 128 + b + NS * 8 + (TW / 32) * 8;  // + alignment slack
+constexpr int kNS = 2;     // TMA stages per warp
+constexpr int kNWARP = 4;  // warps (independent tiles) per CTA
+
+template <int H>
+constexpr int rows_for() {
+  return H <= 1 ? GL_FUSED_ROWS_H1 : 8;
 }
 
-template <int R, int H, int ROWS, int NS>
-void launch_variant(gl_context* ctx, const CUtensorMap* tmap,
-                    const FusedParams& fp) {
-  constexpr size_t smem = smem_bytes<R, ROWS, NS>();
-  auto kern = k_fused_step<R, H, ROWS, NS>;
+template <int R, int ROWS>
+constexpr size_t smem_bytes() {
+  using G = Geo<R, ROWS>;
+  return 128 + static_cast<size_t>(kNWARP) * kNS * G::STAGE * 8 + kNWARP * kNS * 8 + kNWARP * 8;
+}
+
+template <int R, int H>
+void launch_rh(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp) {
+  constexpr int ROWS = rows_for<H>();
+  using G = Geo<R, ROWS>;
+  constexpr size_t smem = smem_bytes<R, ROWS>();
+  auto kern = k_fused_step<R, H, ROWS, kNS, kNWARP>;
   static uint64_t configured = 0;  // bit per device: the attribute is per device
   const uint64_t bit = 1ull << (ctx->device & 63);
   if (!(configured & bit)) {
@@ -391,24 +407,15 @@ void launch_variant(gl_context* ctx, const CUtensorMap* tmap,
                          static_cast<int>(smem));
     configured |= bit;
   }
-  dim3 grid((fp.w + TW - 1) / TW, (fp.h + ROWS - 1) / ROWS, 1);
-  kern<<<grid, TW, smem, ctx->stream>>>(*tmap, fp);
+  fp.tiles_x = (fp.w + G::OW - 1) / G::OW;
+  fp.n_tiles = fp.tiles_x * ((fp.h + ROWS - 1) / ROWS);
+  const int blocks = (fp.n_tiles + kNWARP - 1) / kNWARP;
+  kern<<<blocks, 32 * kNWARP, smem, ctx->stream>>>(*tmap, fp);
   ctx->launches++;
 }
 
-template <int H>
-constexpr int rows_for() {
-  return H <= 1 ? 16 : 8;
-}
-
-template <int R, int H>
-void launch_rh(gl_context* ctx, const CUtensorMap* tmap, const FusedParams& fp) {
-  launch_variant<R, H, rows_for<H>(), 2>(ctx, tmap, fp);
-}
-
 template <int R>
-void launch_r(gl_context* ctx, const CUtensorMap* tmap, const FusedParams& fp,
-              int H) {
+void launch_r(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp, int H) {
   switch (H) {
     case 0: launch_rh<R, 0>(ctx, tmap, fp); break;
     case 1: launch_rh<R, 1>(ctx, tmap, fp); break;
@@ -437,7 +444,7 @@ bool fused_supported(int r, const AngTaps& ang, int c) {
 // the tensor map with it.
 void fused_box(int r, int H, int* bw, int* bh) {
   const int rows = H <= 1 ? rows_for<1>() : rows_for<3>();
-  *bw = (TW + 2 * r + 1 + 1) & ~1;
+  *bw = 34;
   *bh = rows + 2 * r + 1;
 }
 
