@@ -63,6 +63,11 @@ gl_status gl_context_last_step_ms(gl_context* ctx, double* ms);
 /* Path selection (GL_PATH_AUTO = fused when the kernel set allows it). */
 enum { GL_PATH_AUTO = 0, GL_PATH_FUSED = 1, GL_PATH_GENERIC = 2 };
 gl_status gl_context_set_path(gl_context* ctx, int path);
+/* Fused-kernel variant on "clean" tensors (all values finite and >= +0.0,
+ * which init_uniform and every library op preserve; uploads are scanned):
+ * 1 (default) drops the bitwise no-op 0.0 seeds / copy selects; 0 always
+ * runs the literal reference operation sequence. Results are identical. */
+gl_status gl_context_set_fast(gl_context* ctx, int enable);
 /* Number of kernels this context launched since creation. */
 gl_status gl_context_launch_count(gl_context* ctx, uint64_t* n);
 /* The context's cudaStream_t, as an opaque pointer (for NCCL / events). */

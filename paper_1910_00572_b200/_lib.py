@@ -64,6 +64,7 @@ SIGNATURES = {
     "gl_context_synchronize": [_vp],
     "gl_context_last_step_ms": [_vp, _dp],
     "gl_context_set_path": [_vp, C.c_int],
+    "gl_context_set_fast": [_vp, C.c_int],
     "gl_context_launch_count": [_vp, C.POINTER(C.c_uint64)],
     "gl_context_stream": [_vp, _pvp],
     "gl_context_time_steps": [_vp, C.c_int],

@@ -407,6 +407,13 @@ gl_status gl_context_set_path(gl_context* ctx, int path) {
   });
 }
 
+gl_status gl_context_set_fast(gl_context* ctx, int enable) {
+  return guard([&] {
+    need(ctx, "null context");
+    ctx->allow_fast = enable != 0;
+  });
+}
+
 gl_status gl_context_launch_count(gl_context* ctx, uint64_t* n) {
   return guard([&] {
     need(ctx && n, "null argument");
@@ -751,7 +758,12 @@ gl_status gl_tensor_upload(gl_context* ctx, gl_tensor* t, const double* host) {
     CK(cudaMemcpyAsync(t->d_buf[t->cur], host, elems_of(t) * sizeof(double),
                        cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemsetAsync(&t->d_block->buf[t->cur], 0, sizeof(glb::BufState), ctx->stream));
+    auto* flag = static_cast<unsigned int*>(ensure_misc(ctx, 64));
+    glb::launch_scan_unclean(ctx, t->d_buf[t->cur], elems_of(t), flag);
+    unsigned int unclean = 0;
+    CK(cudaMemcpyAsync(&unclean, flag, sizeof(unclean), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    t->clean[t->cur] = unclean == 0;
   });
 }
 
@@ -858,7 +870,8 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
     // r == 0 (impulse) kernels have no separable taps; the fused variant
     // then skips the spatial passes entirely
     const double one = 1.0;
-    glb::launch_fused_step(ctx, a, tm, r > 0 ? kernels->sep.data() : &one, r, ang);
+    glb::launch_fused_step(ctx, a, tm, r > 0 ? kernels->sep.data() : &one, r, ang,
+                           t->clean[src] && ctx->allow_fast);
   } else {
     const size_t n = elems_of(t);
     ensure_scratch(ctx, n);
@@ -888,6 +901,7 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
     ctx->ev_begin_last = ctx->ev_begin;
     ctx->ev_end_last = ctx->ev_end;
   }
+  t->clean[dst] = t->clean[src];  // clean in -> clean out (non-negative weights)
   t->cur = dst;
   t->theta_t = t->theta_t + w;  // belief_tensor.cpp:478
 }
@@ -937,6 +951,7 @@ gl_status gl_apply_motion(gl_context* ctx, gl_tensor* t, double u, double v,
     glb::launch_shift_mask(ctx, a, t->d_buf[dst], 2);
     CK(cudaMemsetAsync(&t->d_block->buf[dst], 0, sizeof(glb::BufState), ctx->stream));
     CK(cudaGetLastError());
+    t->clean[dst] = t->clean[src];
     t->cur = dst;
     t->theta_t = t->theta_t + w;
     CK(cudaStreamSynchronize(ctx->stream));

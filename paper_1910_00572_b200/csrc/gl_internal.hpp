@@ -56,6 +56,7 @@ struct gl_context {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   int path = GL_PATH_AUTO;
+  bool allow_fast = true;  // use the FAST fused variant on clean buffers
   uint64_t launches = 0;
   // generic-path scratch (S and D tensors), grown on demand
   double* d_s = nullptr;
@@ -125,6 +126,10 @@ struct gl_tensor {
   double theta_t = 0.0;
   double* d_buf[2] = {nullptr, nullptr};
   int cur = 0;
+  // "clean": every value finite and >= +0.0 (no -0.0). init_uniform and a
+  // zero tensor are clean; every kernel of this library maps clean input to
+  // clean output; uploads are scanned. Enables the FAST fused variant.
+  bool clean[2] = {true, true};
   glb::DeviceBlock* d_block = nullptr;
   int device = 0;
   CUtensorMap tmap[2];  // 3-D TMA descriptors over d_buf[0/1]
@@ -187,7 +192,10 @@ bool fused_supported(int r, const AngTaps& ang, int c);
 void fused_box(int r, int H, int* bw, int* bh);
 void launch_fused_step(gl_context* ctx, const StepArgs& a,
                        const CUtensorMap* tmap, const double* sep, int r,
-                       const AngTaps& ang);
+                       const AngTaps& ang, bool fast);
+// 1 if any value has its sign bit set or is not finite (buffer not "clean")
+void launch_scan_unclean(gl_context* ctx, const double* buf, size_t n,
+                         unsigned int* d_flag);
 
 // k_observe.cu
 void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,

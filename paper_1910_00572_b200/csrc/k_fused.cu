@@ -155,18 +155,49 @@ __device__ __forceinline__ int2 chan_origin(double2 mv) {
 // c1 = i-sx-1; w00, w10, w01, w11 added to 0.0 in that order
 // (belief_tensor.cpp:112-120). Integral shifts copy r0c0 exactly (:71-86);
 // both forms are evaluated and selected, so there is no per-cell branch.
+//
+// FAST (the source buffer is "clean": every value finite and >= +0.0, which
+// init_uniform and every step/update on a clean buffer preserve) drops two
+// bitwise no-ops: the 0.0 seed of each accumulation (0.0 + x == x unless
+// x == -0.0, and a product of non-negative finite values is never -0.0), and
+// the integral-copy select (weights (1,0,0,0) give a + (+0) + ... == a).
+template <bool FAST>
 __device__ __forceinline__ double s_cell(const ChanShift& cs, double r0c0,
                                          double r0c1, double r1c0,
                                          double r1c1) {
-  double acc = 0.0;
-  acc += cs.w00 * r0c0;
-  acc += cs.w10 * r0c1;
-  acc += cs.w01 * r1c0;
-  acc += cs.w11 * r1c1;
-  return cs.integral ? r0c0 : acc;
+  if constexpr (FAST) {
+    double acc = cs.w00 * r0c0;
+    acc += cs.w10 * r0c1;
+    acc += cs.w01 * r1c0;
+    acc += cs.w11 * r1c1;
+    return acc;
+  } else {
+    double acc = 0.0;
+    acc += cs.w00 * r0c0;
+    acc += cs.w10 * r0c1;
+    acc += cs.w01 * r1c0;
+    acc += cs.w11 * r1c1;
+    return cs.integral ? r0c0 : acc;
+  }
 }
 
-template <int R>
+// sum_t w[t] * x[t] in order from a 0.0 seed (FAST: seeded with the first
+// product, bitwise identical on clean data).
+template <int N, bool FAST>
+__device__ __forceinline__ double dot_seq(const double* w, const double* x) {
+  double acc;
+  if constexpr (FAST) {
+    acc = w[0] * x[0];
+  } else {
+    acc = 0.0;
+    acc += w[0] * x[0];
+  }
+#pragma unroll
+  for (int d = 1; d < N; ++d) acc += w[d] * x[d];
+  return acc;
+}
+
+template <int R, bool FAST>
 __device__ __forceinline__ double row_pass(const FusedParams& p, double s) {
   // acc = 0; acc += t[d+R] * S(i+d), d = -R..R (belief_tensor.cpp:211-214)
   double nb[2 * R + 1];
@@ -176,13 +207,10 @@ __device__ __forceinline__ double row_pass(const FusedParams& p, double s) {
     nb[R - d] = __shfl_up_sync(0xffffffffu, s, d);
     nb[R + d] = __shfl_down_sync(0xffffffffu, s, d);
   }
-  double acc = 0.0;
-#pragma unroll
-  for (int d = 0; d < 2 * R + 1; ++d) acc += p.sep[d] * nb[d];
-  return acc;
+  return dot_seq<2 * R + 1, FAST>(p.sep, nb);
 }
 
-template <int R, int H, int ROWS, int NS>
+template <int R, int H, int ROWS, int NS, bool FAST>
 __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
                                             const FusedParams& p, double* Bs,
                                             uint64_t* mbar, int lane, int x0,
@@ -237,6 +265,9 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
     const bool ok = out_lane && (y0 + r) < Hh;
     store_ok |= static_cast<uint32_t>(ok) << r;
     invr[r] = ok ? __ldg(p.inv + static_cast<size_t>(y0 + r) * W + si) : 0.0;
+    // FAST: fold the output mask into the inverse; out * 0.0 == +0.0 for the
+    // finite non-negative values of a clean buffer (== "out = 0.0", :466-467)
+    if (FAST && ((smask >> (r + R)) & 1u)) invr[r] = 0.0;
   }
   double* const out_tile = p.dst + static_cast<size_t>(y0) * W + (out_lane ? si : 0);
 
@@ -269,7 +300,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
       for (int lj = 0; lj < G::SH; ++lj) {
         const double hi_c0 = Bb[(lj + 1) * G::BW + 1];
         const double hi_c1 = Bb[(lj + 1) * G::BW];
-        double s = s_cell(cs, hi_c0, hi_c1, lo_c0, lo_c1);
+        double s = s_cell<FAST>(cs, hi_c0, hi_c1, lo_c0, lo_c1);
         s = ((smask >> lj) & 1u) ? 0.0 : s;
         lo_c0 = hi_c0;
         lo_c1 = hi_c1;
@@ -281,14 +312,11 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
         } else {
 #pragma unroll
           for (int q = 0; q < 2 * R; ++q) rw[q] = rw[q + 1];
-          rw[2 * R] = row_pass<R>(p, s);
+          rw[2 * R] = row_pass<R, FAST>(p, s);
           if (lj >= 2 * R) {
             // column pass: orow = 0; += t[d] * row(j+d) (:227-238)
-            double col = 0.0;
-#pragma unroll
-            for (int q = 0; q < 2 * R + 1; ++q) col += p.sep[q] * rw[q];
             r = lj - 2 * R;
-            d = col;
+            d = dot_seq<2 * R + 1, FAST>(p.sep, rw);
           }
         }
         if (r >= 0) {
@@ -298,12 +326,14 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
             double o = p.ang[0] * ring[u][r];
 #pragma unroll
             for (int t = 1; t < NG; ++t) o += p.ang[t] * ring[(u - t + NG) % NG][r];
-            const bool occ = (smask >> (r + R)) & 1u;
-            o = occ ? 0.0 : o * invr[r];
-            // the value of the max only feeds the <= 0 / < 1e-6 tests and
-            // 1/max, so fmax (NaN-ignoring, sign of zero irrelevant) matches
-            // the reference's std::max from 0.0 (belief_tensor.cpp:464-471)
-            vmax = fmax(vmax, o);
+            if constexpr (FAST) {
+              o = o * invr[r];
+            } else {
+              o = ((smask >> (r + R)) & 1u) ? 0.0 : o * invr[r];
+            }
+            // std::max from 0.0 over free cells (belief_tensor.cpp:464-471);
+            // masked cells contribute +0.0, which never raises the max
+            vmax = dmax_ref(vmax, o);
             if ((store_ok >> r) & 1u) *orow = o;
             orow += W;
           }
@@ -319,7 +349,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
   return vmax;
 }
 
-template <int R, int H, int ROWS, int NS, int NWARP>
+template <int R, int H, int ROWS, int NS, int NWARP, bool FAST>
 __global__ void __launch_bounds__(32 * NWARP, GL_FUSED_MINB)
     k_fused_step(const __grid_constant__ CUtensorMap tmap,
                  const FusedParams p) {
@@ -348,7 +378,7 @@ __global__ void __launch_bounds__(32 * NWARP, GL_FUSED_MINB)
   const int tile = active ? tile_raw : p.n_tiles - 1;
   const int x0 = (tile % p.tiles_x) * G::OW;
   const int y0 = (tile / p.tiles_x) * ROWS;
-  double vmax = warp_tile<R, H, ROWS, NS>(&tmap, p, Bs, mbar, lane, x0, y0, active);
+  double vmax = warp_tile<R, H, ROWS, NS, FAST>(&tmap, p, Bs, mbar, lane, x0, y0, active);
 
   // global max -> the last CTA finalises status and the pending rescale
 #pragma unroll
@@ -394,12 +424,12 @@ constexpr size_t smem_bytes() {
   return 128 + static_cast<size_t>(kNWARP) * kNS * G::STAGE * 8 + kNWARP * kNS * 8 + kNWARP * 8;
 }
 
-template <int R, int H>
-void launch_rh(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp) {
+template <int R, int H, bool FAST>
+void launch_rhf(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp) {
   constexpr int ROWS = rows_for<H>();
   using G = Geo<R, ROWS>;
   constexpr size_t smem = smem_bytes<R, ROWS>();
-  auto kern = k_fused_step<R, H, ROWS, kNS, kNWARP>;
+  auto kern = k_fused_step<R, H, ROWS, kNS, kNWARP, FAST>;
   static uint64_t configured = 0;  // bit per device: the attribute is per device
   const uint64_t bit = 1ull << (ctx->device & 63);
   if (!(configured & bit)) {
@@ -414,13 +444,23 @@ void launch_rh(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp) {
   ctx->launches++;
 }
 
+template <int R, int H>
+void launch_rh(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp, bool fast) {
+  if (fast) {
+    launch_rhf<R, H, true>(ctx, tmap, fp);
+  } else {
+    launch_rhf<R, H, false>(ctx, tmap, fp);
+  }
+}
+
 template <int R>
-void launch_r(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp, int H) {
+void launch_r(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp, int H,
+              bool fast) {
   switch (H) {
-    case 0: launch_rh<R, 0>(ctx, tmap, fp); break;
-    case 1: launch_rh<R, 1>(ctx, tmap, fp); break;
-    case 2: launch_rh<R, 2>(ctx, tmap, fp); break;
-    default: launch_rh<R, 3>(ctx, tmap, fp); break;
+    case 0: launch_rh<R, 0>(ctx, tmap, fp, fast); break;
+    case 1: launch_rh<R, 1>(ctx, tmap, fp, fast); break;
+    case 2: launch_rh<R, 2>(ctx, tmap, fp, fast); break;
+    default: launch_rh<R, 3>(ctx, tmap, fp, fast); break;
   }
 }
 
@@ -450,7 +490,7 @@ void fused_box(int r, int H, int* bw, int* bh) {
 
 void launch_fused_step(gl_context* ctx, const StepArgs& a,
                        const CUtensorMap* tmap, const double* sep, int r,
-                       const AngTaps& ang) {
+                       const AngTaps& ang, bool fast) {
   FusedParams fp{};
   fp.dst = a.dst;
   fp.motion = a.motion;
@@ -471,9 +511,9 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
   for (int t = 0; t < ang.n; ++t) fp.ang[t] = ang.w[t];
   const int H = ang.n / 2;
   switch (r) {
-    case 0: launch_r<0>(ctx, tmap, fp, H); break;
-    case 1: launch_r<1>(ctx, tmap, fp, H); break;
-    default: launch_r<2>(ctx, tmap, fp, H); break;
+    case 0: launch_r<0>(ctx, tmap, fp, H, fast); break;
+    case 1: launch_r<1>(ctx, tmap, fp, H, fast); break;
+    default: launch_r<2>(ctx, tmap, fp, H, fast); break;
   }
 }
 

@@ -408,6 +408,19 @@ __global__ void k_plane_max(const double* __restrict__ B, size_t n,
   if ((threadIdx.x & 31) == 0) atomic_max_pos(gmax, m);
 }
 
+// Sign bit set (negative or -0.0) or exponent all ones (inf/NaN).
+__global__ void k_scan_unclean(const double* __restrict__ B, size_t n,
+                               unsigned int* flag) {
+  unsigned int bad = 0;
+  for (size_t q = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+       q < n; q += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long b =
+        static_cast<unsigned long long>(__double_as_longlong(B[q]));
+    bad |= ((b >> 63) != 0ull) || ((b & 0x7ff0000000000000ull) == 0x7ff0000000000000ull);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
 int grid_for(size_t n, int threads, int max_blocks = 148 * 16) {
   size_t b = (n + threads - 1) / threads;
   if (b > static_cast<size_t>(max_blocks)) b = max_blocks;
@@ -542,6 +555,13 @@ void launch_hash(gl_context* ctx, const double* buf, size_t n,
                  unsigned long long* d_out) {
   cudaMemsetAsync(d_out, 0, sizeof(unsigned long long), ctx->stream);
   k_hash<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(buf, n, d_out);
+  ctx->launches++;
+}
+
+void launch_scan_unclean(gl_context* ctx, const double* buf, size_t n,
+                         unsigned int* d_flag) {
+  cudaMemsetAsync(d_flag, 0, sizeof(unsigned int), ctx->stream);
+  k_scan_unclean<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(buf, n, d_flag);
   ctx->launches++;
 }
 

@@ -147,6 +147,10 @@ class Context:
     def set_path(self, path: int):
         check(self.lib.gl_context_set_path(self.h, path))
 
+    def set_fast(self, enable: bool):
+        """FAST fused variant on clean tensors (bitwise-identical results)."""
+        check(self.lib.gl_context_set_fast(self.h, int(enable)))
+
     def synchronize(self):
         check(self.lib.gl_context_synchronize(self.h))
 

@@ -123,6 +123,32 @@ def test_fused_tile_edges_bit_exact(ctx, port):
         _run_pair(ctx, port, occ, 72, (0.03, 0.03, 0.012), motions, GL_PATH_FUSED, B0=B0)
 
 
+@pytest.mark.parametrize("fast", [True, False])
+def test_fast_and_strict_variants_agree(ctx, port, fast):
+    """The FAST fused variant (clean tensors) and the literal STRICT sequence
+    are both bit-exact against the oracle."""
+    occ = make_floorplan(130, 70, seed=12)
+    rng = Rng(3)
+    motions = [random_motion(rng) for _ in range(4)] + [(0.1, 0.0, 0.0), (0.2, 0.1, 0.0)]
+    ctx.set_fast(fast)
+    try:
+        _run_pair(ctx, port, occ, 72, (0.03, 0.03, 0.012), motions, GL_PATH_FUSED)
+        _run_pair(ctx, port, occ, 72, (1e-4, 1e-4, 0.012), motions, GL_PATH_FUSED)
+    finally:
+        ctx.set_fast(True)
+
+
+def test_unclean_inputs_bit_exact(ctx, port):
+    """Uploaded tensors with -0.0 and negative values are detected and run
+    the strict variant: still bit-identical, including integral shifts."""
+    occ = make_floorplan(96, 64, seed=13)
+    B0 = random_tensor(occ, 72, seed=5, free_only=False) - 0.3
+    B0[0, 10:20, 10:20] = -0.0
+    motions = [(0.1, 0.0, 0.0), (0.2, 0.1, 0.0), (0.05, 0.03, 0.02)]
+    for path in (GL_PATH_FUSED, GL_PATH_GENERIC):
+        _run_pair(ctx, port, occ, 72, (0.03, 0.03, 0.012), motions, path, B0=B0)
+
+
 def test_large_shifts_bit_exact(ctx, port):
     """Multi-cell and far-out-of-grid shifts (observe() can flush any motion)."""
     occ = make_floorplan(96, 64, seed=9)
