@@ -628,6 +628,10 @@ gl_status gl_make_activation(gl_context* ctx, const gl_map* map,
     glb::launch_make_activation(ctx, map->d_occ, map->w, map->h, channels, kk,
                                 a->d_values, a->d_inverse, a->k_invariant,
                                 d_scratch);
+    if (a->k_invariant) {
+      CK(cudaMalloc(&a->d_inverse_masked, plane * sizeof(double)));
+      glb::launch_mask_plane(ctx, a->d_inverse, map->d_occ, plane, a->d_inverse_masked);
+    }
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaGetLastError());
     *out = a.release();
@@ -639,6 +643,7 @@ gl_status gl_activation_destroy(gl_activation* a) {
     if (!a) return;
     cudaFree(a->d_values);
     cudaFree(a->d_inverse);
+    if (a->d_inverse_masked) cudaFree(a->d_inverse_masked);
     delete a;
   });
 }
@@ -825,6 +830,7 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
   a.step_state = &t->d_block->step;
   a.occ = map->d_occ;
   a.inv = act->d_inverse;
+  a.inv_masked = act->d_inverse_masked;
   a.inv_per_channel = act->k_invariant ? 0 : 1;
   a.w = t->w;
   a.h = t->h;

@@ -118,6 +118,7 @@ struct gl_activation {
   bool k_invariant = false;  // one W*H plane serves every channel
   double* d_values = nullptr;
   double* d_inverse = nullptr;
+  double* d_inverse_masked = nullptr;  // k-invariant: inverse, 0.0 where occupied
 };
 
 struct gl_tensor {
@@ -154,6 +155,7 @@ struct StepArgs {
   const double* h_motion;  // same table on the host (fused path: params)
   const uint8_t* occ;
   const double* inv;       // activation inverse
+  const double* inv_masked;  // same with occupied cells 0.0 (k-invariant only)
   int inv_per_channel;     // 0: one plane for all k
   int w, h, c;
 };
@@ -179,6 +181,8 @@ void launch_make_activation(gl_context* ctx, const uint8_t* occ, int w, int h,
                             double* inverse, bool k_invariant, double* scratch);
 void launch_belief_map(gl_context* ctx, const double* buf, int w, int h,
                        int c, double* out);
+void launch_mask_plane(gl_context* ctx, const double* in, const uint8_t* occ,
+                       size_t plane, double* out);
 size_t argmax_scratch_bytes(size_t n);
 void launch_argmax(gl_context* ctx, const double* buf, size_t n,
                    void* d_scratch, size_t scratch_bytes, void* d_out);

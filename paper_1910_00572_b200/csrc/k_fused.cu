@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "gl_internal.hpp"
 
@@ -37,6 +38,9 @@
 #ifndef GL_FUSED_MINB
 #define GL_FUSED_MINB 4      // min resident CTAs/SM -> register cap
 #endif
+#ifndef GL_FUSED_INVREG_ROWS
+#define GL_FUSED_INVREG_ROWS 8  // tiles up to this height keep inv in registers
+#endif
 
 namespace glb {
 
@@ -44,6 +48,15 @@ namespace {
 
 __device__ __forceinline__ double dmax_ref(double a, double b) {
   return (a < b) ? b : a;
+}
+
+// compile-time loop: f(integral_constant<int, B>), ..., f(<E-1>)
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -97,6 +110,7 @@ struct FusedParams {
   int param_motion;       // 1: motion vectors are in mv[] below
   const uint8_t* occ;
   const double* inv;
+  const double* inv_masked;  // inv with occupied cells set to 0.0 (FAST)
   int inv_per_k;
   int w, h, c;
   int tiles_x, n_tiles;
@@ -258,93 +272,113 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
     smask |= static_cast<uint32_t>(occ) << lj;
   }
   const bool out_lane = active && lane >= R && lane < 32 - R && si < W;
-  double invr[ROWS];
+  // The inverse is held in registers for short tiles (INVREG) or re-read from
+  // L1 per channel for tall ones. FAST folds the output mask into it: for the
+  // finite non-negative values of a clean buffer out * 0.0 == +0.0, which is
+  // the reference's "out = 0.0" for occupied cells (:466-467).
+  constexpr bool INVREG = ROWS <= GL_FUSED_INVREG_ROWS;
+  const double* inv_col = (FAST ? p.inv_masked : p.inv) + (out_lane ? si : 0);
+  double invr[INVREG ? ROWS : 1];
   uint32_t store_ok = 0;
 #pragma unroll
   for (int r = 0; r < ROWS; ++r) {
     const bool ok = out_lane && (y0 + r) < Hh;
     store_ok |= static_cast<uint32_t>(ok) << r;
-    invr[r] = ok ? __ldg(p.inv + static_cast<size_t>(y0 + r) * W + si) : 0.0;
-    // FAST: fold the output mask into the inverse; out * 0.0 == +0.0 for the
-    // finite non-negative values of a clean buffer (== "out = 0.0", :466-467)
-    if (FAST && ((smask >> (r + R)) & 1u)) invr[r] = 0.0;
+    if constexpr (INVREG) invr[r] = ok ? __ldg(inv_col + static_cast<size_t>(y0 + r) * W) : 0.0;
   }
+  const double* inv_tile = inv_col + static_cast<size_t>(y0) * W;
   double* const out_tile = p.dst + static_cast<size_t>(y0) * W + (out_lane ? si : 0);
 
   double ring[NG][ROWS];
   double vmax = 0.0;
 
-  for (int base = 0; base < n_iter; base += NG) {
-#pragma unroll
-    for (int u = 0; u < NG; ++u) {
-      const int it = base + u;
-      if (it >= n_iter) break;
-      const int stage = it % NS;
-      const int m = it - H;
-      const ChanShift cs = chan_shift(motion_of(chan_of(it)));
-      double* stage_ptr = Bs + stage * G::STAGE;
-      mbar_wait(&mbar[stage], static_cast<uint32_t>((it / NS) & 1));
-      if (scaled) {
-        // rare: the source buffer carries a pending rescale (stored values
-        // times sc are the reference's values), applied to the box in smem
-        for (int q = lane; q < G::B_ELEMS; q += 32) stage_ptr[q] = stage_ptr[q] * sc;
-        __syncwarp();
-      }
-      const double* Bb = stage_ptr + ((x0 - R - cs.sx - 1) & 1) + lane;
-      const bool emit = m >= H;
-      double* orow = out_tile + plane * (emit ? m - H : 0);  // advanced by W per row
+  // One channel: wait for its box, S -> row pass -> column pass -> D_m into
+  // ring slot U; with EMIT, output channel k = it - 2H row by row.
+  auto channel = [&](const int it, auto Ut, auto Et) {
+    constexpr int u = decltype(Ut)::value;
+    constexpr bool emit = decltype(Et)::value;
+    const int stage = it % NS;
+    const ChanShift cs = chan_shift(motion_of(chan_of(it)));
+    double* stage_ptr = Bs + stage * G::STAGE;
+    mbar_wait(&mbar[stage], static_cast<uint32_t>((it / NS) & 1));
+    if (scaled) {
+      // rare: the source buffer carries a pending rescale (stored values
+      // times sc are the reference's values), applied to the box in smem
+      for (int q = lane; q < G::B_ELEMS; q += 32) stage_ptr[q] = stage_ptr[q] * sc;
+      __syncwarp();
+    }
+    const double* Bb = stage_ptr + ((x0 - R - cs.sx - 1) & 1) + lane;
+    double* orow = out_tile + plane * static_cast<size_t>(emit ? it - 2 * H : 0);  // += W per row
 
-      double lo_c0 = Bb[1], lo_c1 = Bb[0];
-      double rw[2 * R + 1];  // rolling window of row-pass results
+    double lo_c0 = Bb[1], lo_c1 = Bb[0];
+    double rw[2 * R + 1];  // rolling window of row-pass results
 #pragma unroll
-      for (int lj = 0; lj < G::SH; ++lj) {
-        const double hi_c0 = Bb[(lj + 1) * G::BW + 1];
-        const double hi_c1 = Bb[(lj + 1) * G::BW];
-        double s = s_cell<FAST>(cs, hi_c0, hi_c1, lo_c0, lo_c1);
-        s = ((smask >> lj) & 1u) ? 0.0 : s;
-        lo_c0 = hi_c0;
-        lo_c1 = hi_c1;
-        int r = -1;
-        double d = 0.0;
-        if constexpr (R == 0) {
-          r = lj;
-          d = s;
-        } else {
+    for (int lj = 0; lj < G::SH; ++lj) {
+      const double hi_c0 = Bb[(lj + 1) * G::BW + 1];
+      const double hi_c1 = Bb[(lj + 1) * G::BW];
+      double s = s_cell<FAST>(cs, hi_c0, hi_c1, lo_c0, lo_c1);
+      s = ((smask >> lj) & 1u) ? 0.0 : s;
+      lo_c0 = hi_c0;
+      lo_c1 = hi_c1;
+      int r = -1;
+      double d = 0.0;
+      if constexpr (R == 0) {
+        r = lj;
+        d = s;
+      } else {
 #pragma unroll
-          for (int q = 0; q < 2 * R; ++q) rw[q] = rw[q + 1];
-          rw[2 * R] = row_pass<R, FAST>(p, s);
-          if (lj >= 2 * R) {
-            // column pass: orow = 0; += t[d] * row(j+d) (:227-238)
-            r = lj - 2 * R;
-            d = dot_seq<2 * R + 1, FAST>(p.sep, rw);
-          }
-        }
-        if (r >= 0) {
-          ring[u][r] = d;
-          if (emit) {
-            // angular taps, mask, x inverse, max (belief_tensor.cpp:454-474)
-            double o = p.ang[0] * ring[u][r];
-#pragma unroll
-            for (int t = 1; t < NG; ++t) o += p.ang[t] * ring[(u - t + NG) % NG][r];
-            if constexpr (FAST) {
-              o = o * invr[r];
-            } else {
-              o = ((smask >> (r + R)) & 1u) ? 0.0 : o * invr[r];
-            }
-            // std::max from 0.0 over free cells (belief_tensor.cpp:464-471);
-            // masked cells contribute +0.0, which never raises the max
-            vmax = dmax_ref(vmax, o);
-            if ((store_ok >> r) & 1u) *orow = o;
-            orow += W;
-          }
+        for (int q = 0; q < 2 * R; ++q) rw[q] = rw[q + 1];
+        rw[2 * R] = row_pass<R, FAST>(p, s);
+        if (lj >= 2 * R) {
+          // column pass: orow = 0; += t[d] * row(j+d) (:227-238)
+          r = lj - 2 * R;
+          d = dot_seq<2 * R + 1, FAST>(p.sep, rw);
         }
       }
-      __syncwarp();  // every lane is done with this stage
-      if (lane == 0 && it + NS < n_iter) {
-        if (scaled) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(it + NS, stage);
+      if (r >= 0) {
+        ring[u][r] = d;
+        if constexpr (emit) {
+          // angular taps, mask, x inverse, max (belief_tensor.cpp:454-474)
+          double o = p.ang[0] * ring[u][r];
+#pragma unroll
+          for (int t = 1; t < NG; ++t) o += p.ang[t] * ring[(u - t + NG) % NG][r];
+          double iv;
+          if constexpr (INVREG) {
+            iv = invr[r];
+          } else {
+            iv = ((store_ok >> r) & 1u) ? __ldg(inv_tile + r * W) : 0.0;
+          }
+          if constexpr (FAST) {
+            o = o * iv;
+          } else {
+            o = ((smask >> (r + R)) & 1u) ? 0.0 : o * iv;
+          }
+          // std::max from 0.0 over free cells (belief_tensor.cpp:464-471);
+          // masked cells contribute +0.0, which never raises the max
+          vmax = dmax_ref(vmax, o);
+          if ((store_ok >> r) & 1u) *orow = o;
+          orow += W;
+        }
       }
     }
+    __syncwarp();  // every lane is done with this stage
+    if (lane == 0 && it + NS < n_iter) {
+      if (scaled) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(it + NS, stage);
+    }
+  };
+
+  // channels m = -H .. H-1 only fill the ring (slots 0 .. 2H-1) ...
+  static_for<0, 2 * H>([&](auto U) {
+    channel(decltype(U)::value, U, std::false_type{});
+  });
+  // ... then every channel emits output channel it - 2H; slot = it % NG
+  for (int base = 2 * H; base < n_iter; base += NG) {
+    static_for<0, NG>([&](auto V) {
+      constexpr int v = decltype(V)::value;
+      const int it = base + v;
+      if (it < n_iter) channel(it, std::integral_constant<int, (2 * H + v) % NG>{}, std::true_type{});
+    });
   }
   return vmax;
 }
@@ -410,7 +444,10 @@ __global__ void __launch_bounds__(32 * NWARP, GL_FUSED_MINB)
   }
 }
 
-constexpr int kNS = 2;     // TMA stages per warp
+#ifndef GL_FUSED_NS
+#define GL_FUSED_NS 2
+#endif
+constexpr int kNS = GL_FUSED_NS;  // TMA stages per warp
 constexpr int kNWARP = 4;  // warps (independent tiles) per CTA
 
 template <int H>
@@ -500,6 +537,7 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
   }
   fp.occ = a.occ;
   fp.inv = a.inv;
+  fp.inv_masked = a.inv_masked;
   fp.inv_per_k = a.inv_per_channel;
   fp.w = a.w;
   fp.h = a.h;

@@ -558,6 +558,21 @@ void launch_hash(gl_context* ctx, const double* buf, size_t n,
   ctx->launches++;
 }
 
+__global__ void k_mask_plane(const double* __restrict__ in,
+                             const uint8_t* __restrict__ occ, size_t plane,
+                             double* __restrict__ out) {
+  for (size_t q = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+       q < plane; q += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    out[q] = occ[q] ? 0.0 : in[q];
+  }
+}
+
+void launch_mask_plane(gl_context* ctx, const double* in, const uint8_t* occ,
+                       size_t plane, double* out) {
+  k_mask_plane<<<grid_for(plane, kThreads), kThreads, 0, ctx->stream>>>(in, occ, plane, out);
+  ctx->launches++;
+}
+
 void launch_scan_unclean(gl_context* ctx, const double* buf, size_t n,
                          unsigned int* d_flag) {
   cudaMemsetAsync(d_flag, 0, sizeof(unsigned int), ctx->stream);
