@@ -157,7 +157,16 @@ gl_status gl_tensor_set_theta(gl_tensor* t, double theta_t);
 /* Host <-> device copies of the whole tensor, [k][j][i] FP64. */
 gl_status gl_tensor_upload(gl_context* ctx, gl_tensor* t, const double* host);
 gl_status gl_tensor_download(gl_context* ctx, gl_tensor* t, double* host);
-/* 64-bit FNV-1a over the tensor's bytes, computed on the device (parity). */
+/* Element-range access, flat [k][j][i] offset (BeliefTensor::at / plane()). */
+gl_status gl_tensor_read(gl_context* ctx, gl_tensor* t, size_t offset,
+                         size_t count, double* host);
+gl_status gl_tensor_write(gl_context* ctx, gl_tensor* t, size_t offset,
+                          size_t count, const double* host);
+/* Deep copy on the device (BeliefTensor is value-semantic in the reference,
+ * test_belief_engine.cpp:353,385). */
+gl_status gl_tensor_clone(gl_context* ctx, gl_tensor* src, gl_tensor** out);
+/* Order-independent 64-bit hash of the tensor's bits, computed on the device:
+ * sum over p of splitmix64(bits_p + p * 0x9e3779b97f4a7c15) (parity checks). */
 gl_status gl_tensor_hash(gl_context* ctx, gl_tensor* t, uint64_t* hash);
 /* Raw device pointer of the current buffer (for NCCL halo exchange). */
 gl_status gl_tensor_device_ptr(gl_context* ctx, gl_tensor* t, double** dptr);

@@ -96,6 +96,9 @@ SIGNATURES = {
     "gl_tensor_upload": [_vp, _vp, _dp],
     "gl_tensor_download": [_vp, _vp, _dp],
     "gl_tensor_hash": [_vp, _vp, C.POINTER(C.c_uint64)],
+    "gl_tensor_read": [_vp, _vp, C.c_size_t, C.c_size_t, _dp],
+    "gl_tensor_write": [_vp, _vp, C.c_size_t, C.c_size_t, _dp],
+    "gl_tensor_clone": [_vp, _vp, _pvp],
     "gl_tensor_device_ptr": [_vp, _vp, C.POINTER(_dp)],
     "gl_step": [_vp, _vp, C.c_double, C.c_double, C.c_double, _vp, _vp, _vp],
     "gl_step_async": [_vp, _vp, C.c_double, C.c_double, C.c_double, _vp, _vp, _vp],

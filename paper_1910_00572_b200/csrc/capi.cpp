@@ -506,6 +506,7 @@ gl_status gl_field_destroy(gl_field* f) {
   return guard([&] {
     if (!f) return;
     cudaFree(f->d_values);
+    if (f->d_score) cudaFree(f->d_score);
     delete f;
   });
 }
@@ -780,6 +781,51 @@ gl_status gl_tensor_download(gl_context* ctx, gl_tensor* t, double* host) {
     CK(cudaMemcpyAsync(host, t->d_buf[t->cur], elems_of(t) * sizeof(double),
                        cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+gl_status gl_tensor_read(gl_context* ctx, gl_tensor* t, size_t offset,
+                         size_t count, double* host) {
+  return guard([&] {
+    need(ctx && t && (host || count == 0), "null argument");
+    need(offset <= elems_of(t) && count <= elems_of(t) - offset, "range out of bounds");
+    DeviceGuard g(ctx->device);
+    materialize(ctx, t);
+    CK(cudaMemcpyAsync(host, t->d_buf[t->cur] + offset, count * sizeof(double),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+gl_status gl_tensor_write(gl_context* ctx, gl_tensor* t, size_t offset,
+                          size_t count, const double* host) {
+  return guard([&] {
+    need(ctx && t && (host || count == 0), "null argument");
+    need(offset <= elems_of(t) && count <= elems_of(t) - offset, "range out of bounds");
+    DeviceGuard g(ctx->device);
+    materialize(ctx, t);
+    CK(cudaMemcpyAsync(t->d_buf[t->cur] + offset, host, count * sizeof(double),
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (size_t q = 0; q < count; ++q) {
+      const double v = host[q];
+      if (std::signbit(v) || !std::isfinite(v)) t->clean[t->cur] = false;
+    }
+  });
+}
+
+gl_status gl_tensor_clone(gl_context* ctx, gl_tensor* src, gl_tensor** out) {
+  return guard([&] {
+    need(ctx && src && out, "null argument");
+    DeviceGuard g(ctx->device);
+    materialize(ctx, src);
+    gl_tensor* t = new_tensor(ctx, src->w, src->h, src->c, src->cell, src->ox, src->oy);
+    CK(cudaMemcpyAsync(t->d_buf[0], src->d_buf[src->cur], elems_of(src) * sizeof(double),
+                       cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    t->theta_t = src->theta_t;
+    t->clean[0] = src->clean[src->cur];
+    *out = t;
   });
 }
 
@@ -1074,46 +1120,32 @@ gl_status gl_dither_tensor(gl_context* ctx, gl_tensor* t, int budget,
 // ----------------------------------------------------------- observation
 namespace {
 
+// Per-cell likelihood-field beam score with the reference's libm:
+// log((1 - f) * exp(-d*d*inv2s2) + f) (observation.cpp:101-106), cached on
+// the field for the last LikelihoodParams used.
 struct ObsTables {
-  std::vector<double> score;  // per cell beam log-score
-  double oob = 0.0;
-  double sigma_hit = -1.0, floor_w = -1.0;
-  double* d_score = nullptr;
+  const double* d_score;
+  double oob;
 };
 
-std::mutex g_obs_mu;
-std::vector<std::pair<const gl_field*, std::unique_ptr<ObsTables>>> g_obs;
-
-// Per-cell likelihood-field beam score with the reference's libm:
-// log((1 - f) * exp(-d*d*inv2s2) + f) (observation.cpp:101-106).
-ObsTables* obs_tables(gl_context* ctx, const gl_field* f, gl_likelihood p) {
-  std::lock_guard<std::mutex> lk(g_obs_mu);
-  ObsTables* tb = nullptr;
-  for (auto& e : g_obs)
-    if (e.first == f) tb = e.second.get();
-  if (!tb) {
-    g_obs.emplace_back(f, std::make_unique<ObsTables>());
-    tb = g_obs.back().second.get();
+ObsTables obs_tables(gl_context* ctx, const gl_field* cf, gl_likelihood p) {
+  auto* f = const_cast<gl_field*>(cf);
+  if (!(f->score_sigma == p.sigma_hit && f->score_floor == p.weight_floor && f->d_score)) {
+    const double fl = p.weight_floor;
+    const double inv2s2 = 1.0 / (2.0 * p.sigma_hit * p.sigma_hit);
+    std::vector<double> score(f->values.size());
+    for (size_t q = 0; q < f->values.size(); ++q) {
+      const double d = f->values[q];
+      const double gauss = std::exp(-d * d * inv2s2);
+      score[q] = std::log((1.0 - fl) * gauss + fl);
+    }
+    if (!f->d_score) CK(cudaMalloc(&f->d_score, score.size() * sizeof(double)));
+    CK(cudaMemcpy(f->d_score, score.data(), score.size() * sizeof(double), cudaMemcpyHostToDevice));
+    f->score_oob = std::log((1.0 - fl) * 0.0 + fl);
+    f->score_sigma = p.sigma_hit;
+    f->score_floor = p.weight_floor;
   }
-  if (tb->sigma_hit == p.sigma_hit && tb->floor_w == p.weight_floor && tb->d_score)
-    return tb;
-  const double fl = p.weight_floor;
-  const double inv2s2 = 1.0 / (2.0 * p.sigma_hit * p.sigma_hit);
-  tb->score.resize(f->values.size());
-  for (size_t q = 0; q < f->values.size(); ++q) {
-    const double d = f->values[q];
-    const double gauss = std::exp(-d * d * inv2s2);
-    tb->score[q] = std::log((1.0 - fl) * gauss + fl);
-  }
-  tb->oob = std::log((1.0 - fl) * 0.0 + fl);
-  if (tb->d_score) cudaFree(tb->d_score);
-  tb->d_score = nullptr;
-  CK(cudaMalloc(&tb->d_score, tb->score.size() * sizeof(double)));
-  CK(cudaMemcpyAsync(tb->d_score, tb->score.data(), tb->score.size() * sizeof(double),
-                     cudaMemcpyHostToDevice, ctx->stream));
-  tb->sigma_hit = p.sigma_hit;
-  tb->floor_w = p.weight_floor;
-  return tb;
+  return ObsTables{f->d_score, f->score_oob};
 }
 
 }  // namespace
@@ -1130,7 +1162,7 @@ gl_status gl_scan_likelihood(gl_context* ctx, const gl_map* map,
     need(ctx && map && field && out, "null argument");
     need(n_beams >= 1 && angles && ranges, "scan must have matching, nonempty beams");
     DeviceGuard g(ctx->device);
-    ObsTables* tb = obs_tables(ctx, field, params);
+    const ObsTables tb = obs_tables(ctx, field, params);
     const int stride = std::max(1, params.beam_stride);
     std::vector<double> dirs, reach;
     const double half = 0.5 * map->res;
@@ -1158,7 +1190,7 @@ gl_status gl_scan_likelihood(gl_context* ctx, const gl_map* map,
       CK(cudaMemcpyAsync(d_dir, dirs.data(), ns * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     }
     // x = tox + (0 + 0.5) * 0.0 ... use cell = 0 so the pose is exactly (x, y)
-    glb::launch_likelihoods(ctx, map->d_occ, tb->d_score, tb->oob, map->w, map->h,
+    glb::launch_likelihoods(ctx, map->d_occ, tb.d_score, tb.oob, map->w, map->h,
                             map->res, map->ox, map->oy, 0.0, x, y, d_s, 1, 1,
                             d_dir, ns, d_reach, params.weight_floor, d_L);
     CK(cudaGetLastError());
@@ -1179,7 +1211,7 @@ gl_status gl_observation_update(gl_context* ctx, gl_tensor* t,
     need(cells != nullptr && n > 0, "bad sample set");
     need(n_beams >= 1 && angles && ranges, "scan must have matching, nonempty beams");
     DeviceGuard g(ctx->device);
-    ObsTables* tb = obs_tables(ctx, field, params);
+    const ObsTables tb = obs_tables(ctx, field, params);
     const int C = t->c;
     // scored beams and per-(channel, beam) directions with host libm
     const int stride = std::max(1, params.beam_stride);
@@ -1217,7 +1249,7 @@ gl_status gl_observation_update(gl_context* ctx, gl_tensor* t,
     CK(cudaMemcpyAsync(d_reach, reach.data(), sizeof(double) * reach.size(), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(d_dir, dirs.data(), sizeof(double) * dirs.size(), cudaMemcpyHostToDevice, ctx->stream));
     materialize(ctx, t);
-    glb::launch_likelihoods(ctx, map->d_occ, tb->d_score, tb->oob, map->w, map->h,
+    glb::launch_likelihoods(ctx, map->d_occ, tb.d_score, tb.oob, map->w, map->h,
                             map->res, map->ox, map->oy, t->cell, t->ox, t->oy, d_s,
                             n, C, d_dir, ns, d_reach, params.weight_floor, d_L);
     glb::launch_observe_apply(ctx, t->d_buf[t->cur], t->w, t->h, C, d_s, n, d_L, d_mean);

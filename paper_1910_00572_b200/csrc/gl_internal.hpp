@@ -98,6 +98,10 @@ struct gl_field {
   int w = 0, h = 0;
   std::vector<double> values;  // meters
   double* d_values = nullptr;
+  // per-cell beam log-score table for one LikelihoodParams (host libm),
+  // owned by the field so it dies with it
+  double score_sigma = -1.0, score_floor = -1.0, score_oob = 0.0;
+  double* d_score = nullptr;
 };
 
 struct gl_kernels {
