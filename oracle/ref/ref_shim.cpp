@@ -309,6 +309,17 @@ int ref_simulate_scan(void* map, double x, double y, double th, int beams,
   });
 }
 
+// ---- rng (rng.hpp:10-74): draw sequences for the Python restatement -------
+void ref_rng_draws(uint64_t seed, int n, uint64_t* u64, double* uni,
+                   double* nrm) {
+  Rng a(seed), b(seed), c(seed);
+  for (int q = 0; q < n; ++q) {
+    u64[q] = a.next_u64();
+    uni[q] = b.uniform();
+    nrm[q] = c.normal();
+  }
+}
+
 // ---- trace recorder --------------------------------------------------------
 // Runs the reference simulator (RandomWalkPolicy, step_robot,
 // odometry_measurement; evaluation.cpp:135-162) from a given start pose and
