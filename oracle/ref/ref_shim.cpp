@@ -208,6 +208,22 @@ void ref_tensor_get(void* t, double* vals, double* theta_t) {
   if (theta_t) *theta_t = bt->theta_t();
 }
 
+// Same order-independent hash as gl_tensor_hash: sum of splitmix64(bits_p +
+// p * golden) over the tensor.
+uint64_t ref_tensor_hash(void* t) {
+  const auto& v = static_cast<BeliefTensor*>(t)->values();
+  uint64_t acc = 0;
+  for (std::size_t p = 0; p < v.size(); ++p) {
+    uint64_t bits;
+    std::memcpy(&bits, &v[p], 8);
+    uint64_t z = bits + static_cast<uint64_t>(p) * 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    acc += z ^ (z >> 31);
+  }
+  return acc;
+}
+
 void* ref_scratch_new() { return new StepScratch(); }
 void ref_scratch_free(void* s) { delete static_cast<StepScratch*>(s); }
 void ref_scratch_times(void* s, double* t3) {
