@@ -68,6 +68,11 @@ gl_status gl_context_set_path(gl_context* ctx, int path);
  * 1 (default) drops the bitwise no-op 0.0 seeds / copy selects; 0 always
  * runs the literal reference operation sequence. Results are identical. */
 gl_status gl_context_set_fast(gl_context* ctx, int enable);
+/* scan_likelihood's final exp (the per-pose geometric mean,
+ * observation.cpp:110): 1 (default) evaluates it with the host's libm like the
+ * reference (bit-exact; one D2H/H2D of <= 512*Theta doubles per observation),
+ * 0 with CUDA's exp on the device (<= 1 ulp). Everything else is device. */
+gl_status gl_context_set_host_exp(gl_context* ctx, int enable);
 /* Number of kernels this context launched since creation. */
 gl_status gl_context_launch_count(gl_context* ctx, uint64_t* n);
 /* The context's cudaStream_t, as an opaque pointer (for NCCL / events). */
@@ -184,6 +189,31 @@ gl_status gl_step_async(gl_context* ctx, gl_tensor* t, double u, double v,
                         double w, const gl_map* map, const gl_kernels* kernels,
                         const gl_activation* act);
 gl_status gl_tensor_status(gl_context* ctx, gl_tensor* t);
+/* ---- theta-slab shards ----------------------------------
+ * A shard holds global channels [c_begin, c_end) of a c_total-channel belief,
+ * stored with `halo` neighbour planes per side: storage plane q is channel
+ * (c_begin - halo + q) mod c_total; the user-visible planes (download, hash,
+ * argmax, belief_map) are the interior ones. One sharded step is:
+ *   gl_step_async                          (fused kernel, local max only)
+ *   all-reduce MAX of *gl_tensor_max_ptr   (uint64 bits of a double >= 0)
+ *   gl_shard_finalize                      (status + pending 1/max rescale)
+ *   halo exchange of storage planes        (gl_tensor_plane_ptr; NCCL)
+ * Sharding does not change any per-element operation: results are bitwise
+ * those of the unsharded tensor. */
+gl_status gl_shard_init_uniform(gl_context* ctx, const gl_map* map, int c_total,
+                                int c_begin, int c_end, int halo,
+                                gl_tensor** out);
+gl_status gl_shard_info(const gl_tensor* t, int* c_total, int* c_begin,
+                        int* c_count, int* halo);
+gl_status gl_tensor_plane_ptr(gl_context* ctx, gl_tensor* t, int q,
+                              double** dptr);
+gl_status gl_tensor_max_ptr(gl_context* ctx, gl_tensor* t,
+                            unsigned long long** dptr);
+gl_status gl_shard_finalize(gl_context* ctx, gl_tensor* t);
+/* device-to-device plane copy (single-device halo exchange) */
+gl_status gl_tensor_copy_planes(gl_context* ctx, gl_tensor* dst, int dst_q,
+                                gl_tensor* src, int src_q, int count);
+
 /* apply_motion (belief_tensor.cpp:340-352): shift only, no mask/diffusion. */
 gl_status gl_apply_motion(gl_context* ctx, gl_tensor* t, double u, double v,
                           double w);

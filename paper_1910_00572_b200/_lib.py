@@ -65,6 +65,13 @@ SIGNATURES = {
     "gl_context_last_step_ms": [_vp, _dp],
     "gl_context_set_path": [_vp, C.c_int],
     "gl_context_set_fast": [_vp, C.c_int],
+    "gl_context_set_host_exp": [_vp, C.c_int],
+    "gl_shard_init_uniform": [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _pvp],
+    "gl_shard_info": [_vp, _ip, _ip, _ip, _ip],
+    "gl_tensor_plane_ptr": [_vp, _vp, C.c_int, C.POINTER(_dp)],
+    "gl_tensor_max_ptr": [_vp, _vp, C.POINTER(C.POINTER(C.c_uint64))],
+    "gl_shard_finalize": [_vp, _vp],
+    "gl_tensor_copy_planes": [_vp, _vp, C.c_int, _vp, C.c_int, C.c_int],
     "gl_context_launch_count": [_vp, C.POINTER(C.c_uint64)],
     "gl_context_stream": [_vp, _pvp],
     "gl_context_time_steps": [_vp, C.c_int],

@@ -134,7 +134,12 @@ const CUtensorMap* tensor_tmap(gl_tensor* t, int buf, int bw, int bh);
 
 // ------------------------------------------------------------- helpers
 size_t plane_of(const gl_tensor* t) { return static_cast<size_t>(t->w) * t->h; }
+// user-visible elements: a theta-slab shard's interior planes (its halo
+// planes are storage only)
 size_t elems_of(const gl_tensor* t) { return plane_of(t) * t->c; }
+int halo_of(const gl_tensor* t) { return t->halo > 0 ? t->halo : 0; }
+size_t storage_elems(const gl_tensor* t) { return plane_of(t) * (t->c + 2 * halo_of(t)); }
+double* interior(const gl_tensor* t) { return t->d_buf[t->cur] + plane_of(t) * halo_of(t); }
 
 void* ensure_misc(gl_context* ctx, size_t bytes) {
   if (ctx->misc_bytes < bytes) {
@@ -227,7 +232,7 @@ void upload_kernels(gl_kernels* k, int device) {
 // Apply a pending 1/max rescale to the current buffer in place (consumers
 // other than the step read the tensor as stored).
 void materialize(gl_context* ctx, gl_tensor* t) {
-  glb::launch_apply_scale(ctx, t->d_buf[t->cur], elems_of(t),
+  glb::launch_apply_scale(ctx, t->d_buf[t->cur], storage_elems(t),
                           &t->d_block->buf[t->cur]);
 }
 
@@ -272,7 +277,7 @@ const CUtensorMap* tensor_tmap(gl_tensor* t, int buf, int bw, int bh) {
   c.base = t->d_buf[buf];
   c.bw = bw;
   c.bh = bh;
-  if (!make_tmap(&c.map, c.base, t->w, t->h, t->c, bw, bh)) return nullptr;
+  if (!make_tmap(&c.map, c.base, t->w, t->h, t->c + 2 * halo_of(t), bw, bh)) return nullptr;
   x->maps.push_back(c);
   return &x->maps.back().map;
 }
@@ -315,6 +320,9 @@ gl_status gl_context_destroy(gl_context* ctx) {
     if (ctx->h_block) cudaFreeHost(ctx->h_block);
     if (ctx->d_misc) cudaFree(ctx->d_misc);
     if (ctx->h_misc) cudaFreeHost(ctx->h_misc);
+    if (ctx->d_kind) cudaFree(ctx->d_kind);
+    for (auto& e : ctx->marks)
+      if (e) cudaEventDestroy(e);
     for (auto& e : ctx->ring_ev) cudaEventDestroy(e);
     for (auto& e : ctx->tev) cudaEventDestroy(e);
     cudaEventDestroy(ctx->ev_begin);
@@ -404,6 +412,13 @@ gl_status gl_context_set_path(gl_context* ctx, int path) {
     need(ctx, "null context");
     need(path >= GL_PATH_AUTO && path <= GL_PATH_GENERIC, "bad path");
     ctx->path = path;
+  });
+}
+
+gl_status gl_context_set_host_exp(gl_context* ctx, int enable) {
+  return guard([&] {
+    need(ctx, "null context");
+    ctx->host_exp = enable != 0;
   });
 }
 
@@ -670,7 +685,8 @@ gl_status gl_activation_get(gl_context* ctx, const gl_activation* a,
 
 // ---------------------------------------------------------------- tensors
 static gl_tensor* new_tensor(gl_context* ctx, int w, int h, int c, double cell,
-                             double ox, double oy) {
+                             double ox, double oy, int halo = -1, int c_total = 0,
+                             int c_begin = 0) {
   need(w >= 1 && h >= 1 && c >= 1, "belief tensor dimensions must be positive");
   auto t = std::make_unique<gl_tensor>();
   t->w = w;
@@ -680,7 +696,10 @@ static gl_tensor* new_tensor(gl_context* ctx, int w, int h, int c, double cell,
   t->ox = ox;
   t->oy = oy;
   t->device = ctx->device;
-  const size_t n = static_cast<size_t>(w) * h * c;
+  t->halo = halo;
+  t->c_total = halo >= 0 ? c_total : c;
+  t->c_begin = halo >= 0 ? c_begin : 0;
+  const size_t n = storage_elems(t.get());
   CK(cudaMalloc(&t->d_buf[0], n * sizeof(double)));
   CK(cudaMalloc(&t->d_buf[1], n * sizeof(double)));
   CK(cudaMalloc(&t->d_block, sizeof(glb::DeviceBlock)));
@@ -761,11 +780,11 @@ gl_status gl_tensor_upload(gl_context* ctx, gl_tensor* t, const double* host) {
   return guard([&] {
     need(ctx && t && host, "null argument");
     DeviceGuard g(ctx->device);
-    CK(cudaMemcpyAsync(t->d_buf[t->cur], host, elems_of(t) * sizeof(double),
+    CK(cudaMemcpyAsync(interior(t), host, elems_of(t) * sizeof(double),
                        cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemsetAsync(&t->d_block->buf[t->cur], 0, sizeof(glb::BufState), ctx->stream));
     auto* flag = static_cast<unsigned int*>(ensure_misc(ctx, 64));
-    glb::launch_scan_unclean(ctx, t->d_buf[t->cur], elems_of(t), flag);
+    glb::launch_scan_unclean(ctx, interior(t), elems_of(t), flag);
     unsigned int unclean = 0;
     CK(cudaMemcpyAsync(&unclean, flag, sizeof(unclean), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -778,7 +797,7 @@ gl_status gl_tensor_download(gl_context* ctx, gl_tensor* t, double* host) {
     need(ctx && t && host, "null argument");
     DeviceGuard g(ctx->device);
     materialize(ctx, t);
-    CK(cudaMemcpyAsync(host, t->d_buf[t->cur], elems_of(t) * sizeof(double),
+    CK(cudaMemcpyAsync(host, interior(t), elems_of(t) * sizeof(double),
                        cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   });
@@ -791,7 +810,7 @@ gl_status gl_tensor_read(gl_context* ctx, gl_tensor* t, size_t offset,
     need(offset <= elems_of(t) && count <= elems_of(t) - offset, "range out of bounds");
     DeviceGuard g(ctx->device);
     materialize(ctx, t);
-    CK(cudaMemcpyAsync(host, t->d_buf[t->cur] + offset, count * sizeof(double),
+    CK(cudaMemcpyAsync(host, interior(t) + offset, count * sizeof(double),
                        cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   });
@@ -804,7 +823,7 @@ gl_status gl_tensor_write(gl_context* ctx, gl_tensor* t, size_t offset,
     need(offset <= elems_of(t) && count <= elems_of(t) - offset, "range out of bounds");
     DeviceGuard g(ctx->device);
     materialize(ctx, t);
-    CK(cudaMemcpyAsync(t->d_buf[t->cur] + offset, host, count * sizeof(double),
+    CK(cudaMemcpyAsync(interior(t) + offset, host, count * sizeof(double),
                        cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     for (size_t q = 0; q < count; ++q) {
@@ -819,8 +838,9 @@ gl_status gl_tensor_clone(gl_context* ctx, gl_tensor* src, gl_tensor** out) {
     need(ctx && src && out, "null argument");
     DeviceGuard g(ctx->device);
     materialize(ctx, src);
-    gl_tensor* t = new_tensor(ctx, src->w, src->h, src->c, src->cell, src->ox, src->oy);
-    CK(cudaMemcpyAsync(t->d_buf[0], src->d_buf[src->cur], elems_of(src) * sizeof(double),
+    gl_tensor* t = new_tensor(ctx, src->w, src->h, src->c, src->cell, src->ox, src->oy,
+                              src->halo, src->c_total, src->c_begin);
+    CK(cudaMemcpyAsync(t->d_buf[0], src->d_buf[src->cur], storage_elems(src) * sizeof(double),
                        cudaMemcpyDeviceToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     t->theta_t = src->theta_t;
@@ -835,7 +855,7 @@ gl_status gl_tensor_hash(gl_context* ctx, gl_tensor* t, uint64_t* hash) {
     DeviceGuard g(ctx->device);
     materialize(ctx, t);
     auto* d = static_cast<unsigned long long*>(ensure_misc(ctx, 64));
-    glb::launch_hash(ctx, t->d_buf[t->cur], elems_of(t), d);
+    glb::launch_hash(ctx, interior(t), elems_of(t), d);
     unsigned long long hv = 0;
     CK(cudaMemcpyAsync(&hv, d, sizeof(hv), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -849,7 +869,7 @@ gl_status gl_tensor_device_ptr(gl_context* ctx, gl_tensor* t, double** dptr) {
     DeviceGuard g(ctx->device);
     materialize(ctx, t);
     CK(cudaStreamSynchronize(ctx->stream));
-    *dptr = t->d_buf[t->cur];
+    *dptr = interior(t);
   });
 }
 
@@ -859,7 +879,7 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
                          const gl_activation* act) {
   need(ctx && t && map && kernels && act, "null argument");
   need(map->w == t->w && map->h == t->h, "map and tensor sizes differ");
-  need(act->w == t->w && act->h == t->h && act->channels == t->c,
+  need(act->w == t->w && act->h == t->h && act->channels == t->c_total,
        "activation does not match the tensor");
   need(kernels->info.separable || kernels->info.channels >= t->c,
        "kernel set has fewer channels than the tensor");
@@ -893,7 +913,7 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
       ang.off[q] = kernels->ang_off[q];
       ang.w[q] = kernels->ang_w[q];
     }
-    fused = glb::fused_supported(r, ang, t->c);
+    fused = glb::fused_supported(r, ang, t->c) && (t->halo < 0 || ang.n / 2 <= t->halo);
   }
   const CUtensorMap* tm = nullptr;
   if (fused) {
@@ -908,7 +928,22 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
   // motion vectors (host libm): carried in the launch parameters on the
   // fused path, otherwise uploaded through the pinned ring
   thread_local std::vector<double> hm;
-  if (fused && t->c <= glb::kParamChannels) {
+  if (t->halo >= 0) {
+    // theta-slab shard: one motion vector per storage plane (global channel
+    // (c_begin - halo + q) mod c_total), carried in the launch parameters
+    if (!fused) fail(GL_E_INVALID, "sharded tensors need the fused path (separable/impulse kernels, H <= halo)");
+    const int planes = t->c + 2 * t->halo;
+    need(planes <= glb::kParamChannels, "too many planes per shard for the launch-parameter motion table");
+    hm.resize(2 * static_cast<size_t>(planes));
+    const double dtheta = 2.0 * M_PI / t->c_total;
+    for (int q = 0; q < planes; ++q) {
+      const int k = ((t->c_begin - t->halo + q) % t->c_total + t->c_total) % t->c_total;
+      glb::motion_table(u, v, k, 1, t->theta_t, dtheta, t->cell, hm.data() + 2 * q);
+    }
+    a.h_motion = hm.data();
+    a.motion = nullptr;
+    a.halo = t->halo;
+  } else if (fused && t->c <= glb::kParamChannels) {
     hm.resize(2 * static_cast<size_t>(t->c));
     glb::motion_table(u, v, 0, t->c, t->theta_t, 2.0 * M_PI / t->c, t->cell, hm.data());
     a.h_motion = hm.data();
@@ -977,6 +1012,79 @@ gl_status gl_step_async(gl_context* ctx, gl_tensor* t, double u, double v,
   return guard([&] { enqueue_step(ctx, t, u, v, w, map, kernels, act); });
 }
 
+// ---------------------------------------------------------- theta shards
+gl_status gl_shard_init_uniform(gl_context* ctx, const gl_map* map, int c_total,
+                                int c_begin, int c_end, int halo, gl_tensor** out) {
+  return guard([&] {
+    need(ctx && map && out, "null argument");
+    need(c_total >= 4 && c_total % 2 == 0, "channel count must be even and >= 4");
+    need(0 <= c_begin && c_begin < c_end && c_end <= c_total, "bad channel range");
+    need(halo >= 0 && 2 * halo < c_total, "bad halo");
+    need(map->free_count > 0, "map has no free cells to initialize from");
+    DeviceGuard g(ctx->device);
+    gl_tensor* t = new_tensor(ctx, map->w, map->h, c_end - c_begin, map->res, map->ox, map->oy, halo,
+                              c_total, c_begin);
+    // every storage plane (interior and halo) starts as the free indicator
+    glb::launch_init_uniform(ctx, t->d_buf[0], map->d_occ, map->w, map->h, t->c + 2 * halo);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    *out = t;
+  });
+}
+
+gl_status gl_shard_info(const gl_tensor* t, int* c_total, int* c_begin, int* c_count, int* halo) {
+  return guard([&] {
+    need(t, "null tensor");
+    if (c_total) *c_total = t->c_total;
+    if (c_begin) *c_begin = t->c_begin;
+    if (c_count) *c_count = t->c;
+    if (halo) *halo = t->halo;
+  });
+}
+
+gl_status gl_tensor_plane_ptr(gl_context* ctx, gl_tensor* t, int q, double** dptr) {
+  return guard([&] {
+    need(ctx && t && dptr, "null argument");
+    need(q >= 0 && q < t->c + 2 * halo_of(t), "storage plane out of range");
+    *dptr = t->d_buf[t->cur] + plane_of(t) * q;  // raw: a pending rescale stays pending
+  });
+}
+
+gl_status gl_tensor_max_ptr(gl_context* ctx, gl_tensor* t, unsigned long long** dptr) {
+  return guard([&] {
+    need(ctx && t && dptr, "null argument");
+    *dptr = &t->d_block->step.gmax_bits;
+  });
+}
+
+gl_status gl_shard_finalize(gl_context* ctx, gl_tensor* t) {
+  return guard([&] {
+    need(ctx && t, "null argument");
+    need(t->halo >= 0, "not a sharded tensor");
+    DeviceGuard g(ctx->device);
+    glb::StepArgs a{};
+    a.step_state = &t->d_block->step;
+    a.dst_state = &t->d_block->buf[t->cur];  // the step already flipped cur
+    glb::launch_step_finalize(ctx, a);
+    CK(cudaGetLastError());
+  });
+}
+
+gl_status gl_tensor_copy_planes(gl_context* ctx, gl_tensor* dst, int dst_q, gl_tensor* src,
+                                int src_q, int count) {
+  return guard([&] {
+    need(ctx && dst && src, "null argument");
+    need(dst->w == src->w && dst->h == src->h, "plane sizes differ");
+    need(count >= 0 && dst_q >= 0 && src_q >= 0 && dst_q + count <= dst->c + 2 * halo_of(dst) &&
+             src_q + count <= src->c + 2 * halo_of(src),
+         "plane range out of bounds");
+    DeviceGuard g(ctx->device);
+    const size_t plane = plane_of(dst);
+    CK(cudaMemcpyAsync(dst->d_buf[dst->cur] + plane * dst_q, src->d_buf[src->cur] + plane * src_q,
+                       plane * count * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  });
+}
+
 gl_status gl_tensor_status(gl_context* ctx, gl_tensor* t) {
   return guard([&] {
     need(ctx && t, "null argument");
@@ -1024,7 +1132,7 @@ gl_status gl_belief_map(gl_context* ctx, gl_tensor* t, double* host_out) {
     DeviceGuard g(ctx->device);
     materialize(ctx, t);
     double* d = static_cast<double*>(ensure_misc(ctx, plane_of(t) * sizeof(double)));
-    glb::launch_belief_map(ctx, t->d_buf[t->cur], t->w, t->h, t->c, d);
+    glb::launch_belief_map(ctx, interior(t), t->w, t->h, t->c, d);
     CK(cudaMemcpyAsync(host_out, d, plane_of(t) * sizeof(double),
                        cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -1039,7 +1147,7 @@ gl_status gl_argmax(gl_context* ctx, gl_tensor* t, gl_pose_estimate* out) {
     const size_t n = elems_of(t);
     const size_t sb = glb::argmax_scratch_bytes(n);
     char* d = static_cast<char*>(ensure_misc(ctx, sb + 256));
-    glb::launch_argmax(ctx, t->d_buf[t->cur], n, d, sb, d + sb);
+    glb::launch_argmax(ctx, interior(t), n, d, sb, d + sb);
     struct {
       double v;
       long long idx;
@@ -1112,7 +1220,7 @@ gl_status gl_dither_tensor(gl_context* ctx, gl_tensor* t, int budget,
     const size_t plane = plane_of(t);
     double* d = static_cast<double*>(
         ensure_misc(ctx, plane * sizeof(double) + 64 + std::min<size_t>(plane, std::max(cap, 1)) * 8));
-    glb::launch_belief_map(ctx, t->d_buf[t->cur], t->w, t->h, t->c, d);
+    glb::launch_belief_map(ctx, interior(t), t->w, t->h, t->c, d);
     run_dither(ctx, d, t->w, t->h, budget, cells, cap, n, source_mass);
   });
 }
@@ -1127,6 +1235,33 @@ struct ObsTables {
   const double* d_score;
   double oob;
 };
+
+void* ensure_kind(gl_context* ctx, size_t n) {
+  if (ctx->kind_bytes < n) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->d_kind) CK(cudaFree(ctx->d_kind));
+    ctx->d_kind = nullptr;
+    CK(cudaMalloc(&ctx->d_kind, n));
+    ctx->kind_bytes = n;
+  }
+  return ctx->d_kind;
+}
+
+// The geometric mean's final exp with the host's glibc, like the reference
+// (observation.cpp:110): the kernel left the exponent and a case code.
+void finish_likelihoods_on_host(gl_context* ctx, double* d_L, const uint8_t* d_kind, size_t n,
+                                double floor_w) {
+  std::vector<double> L(n);
+  std::vector<uint8_t> kind(n);
+  CK(cudaMemcpyAsync(L.data(), d_L, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(kind.data(), d_kind, n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (size_t q = 0; q < n; ++q) {
+    L[q] = kind[q] == 0 ? std::exp(L[q]) : (kind[q] == 1 ? floor_w : 1.0);
+  }
+  CK(cudaMemcpyAsync(d_L, L.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+}
 
 ObsTables obs_tables(gl_context* ctx, const gl_field* cf, gl_likelihood p) {
   auto* f = const_cast<gl_field*>(cf);
@@ -1190,10 +1325,12 @@ gl_status gl_scan_likelihood(gl_context* ctx, const gl_map* map,
       CK(cudaMemcpyAsync(d_dir, dirs.data(), ns * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     }
     // x = tox + (0 + 0.5) * 0.0 ... use cell = 0 so the pose is exactly (x, y)
+    uint8_t* d_kind = ctx->host_exp ? static_cast<uint8_t*>(ensure_kind(ctx, 1)) : nullptr;
     glb::launch_likelihoods(ctx, map->d_occ, tb.d_score, tb.oob, map->w, map->h,
                             map->res, map->ox, map->oy, 0.0, x, y, d_s, 1, 1,
-                            d_dir, ns, d_reach, params.weight_floor, d_L);
+                            d_dir, ns, d_reach, params.weight_floor, d_L, d_kind);
     CK(cudaGetLastError());
+    if (ctx->host_exp) finish_likelihoods_on_host(ctx, d_L, d_kind, 1, params.weight_floor);
     CK(cudaMemcpyAsync(out, d_L, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   });
@@ -1249,11 +1386,13 @@ gl_status gl_observation_update(gl_context* ctx, gl_tensor* t,
     CK(cudaMemcpyAsync(d_reach, reach.data(), sizeof(double) * reach.size(), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(d_dir, dirs.data(), sizeof(double) * dirs.size(), cudaMemcpyHostToDevice, ctx->stream));
     materialize(ctx, t);
+    uint8_t* d_kind = ctx->host_exp ? static_cast<uint8_t*>(ensure_kind(ctx, nL)) : nullptr;
     glb::launch_likelihoods(ctx, map->d_occ, tb.d_score, tb.oob, map->w, map->h,
                             map->res, map->ox, map->oy, t->cell, t->ox, t->oy, d_s,
-                            n, C, d_dir, ns, d_reach, params.weight_floor, d_L);
-    glb::launch_observe_apply(ctx, t->d_buf[t->cur], t->w, t->h, C, d_s, n, d_L, d_mean);
-    glb::launch_plane_max(ctx, t->d_buf[t->cur], elems_of(t), &t->d_block->step.gmax_bits);
+                            n, C, d_dir, ns, d_reach, params.weight_floor, d_L, d_kind);
+    if (ctx->host_exp) finish_likelihoods_on_host(ctx, d_L, d_kind, nL, params.weight_floor);
+    glb::launch_observe_apply(ctx, interior(t), t->w, t->h, C, d_s, n, d_L, d_mean);
+    glb::launch_plane_max(ctx, interior(t), elems_of(t), &t->d_block->step.gmax_bits);
     glb::launch_observe_finalize(ctx, &t->d_block->step, &t->d_block->buf[t->cur]);
     CK(cudaGetLastError());
     if (read_status(ctx, t) == GL_E_EXTINGUISHED) {

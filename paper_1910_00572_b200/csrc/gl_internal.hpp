@@ -57,6 +57,9 @@ struct gl_context {
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   int path = GL_PATH_AUTO;
   bool allow_fast = true;  // use the FAST fused variant on clean buffers
+  bool host_exp = true;    // likelihood geometric mean: exp by host glibc (exact)
+  void* d_kind = nullptr;  // likelihood case codes
+  size_t kind_bytes = 0;
   uint64_t launches = 0;
   // generic-path scratch (S and D tensors), grown on demand
   double* d_s = nullptr;
@@ -126,7 +129,12 @@ struct gl_activation {
 };
 
 struct gl_tensor {
-  int w = 0, h = 0, c = 0;
+  int w = 0, h = 0, c = 0;  // c = channels held (a shard's interior planes)
+  // theta-slab shard: this tensor holds global channels
+  // [c_begin, c_begin + c) of c_total, stored with `halo` neighbour planes on
+  // each side: storage plane q <-> channel (c_begin - halo + q) mod c_total.
+  int halo = -1;  // -1: a whole (unsharded) tensor
+  int c_total = 0, c_begin = 0;
   double cell = 0.1, ox = 0.0, oy = 0.0;
   double theta_t = 0.0;
   double* d_buf[2] = {nullptr, nullptr};
@@ -161,7 +169,8 @@ struct StepArgs {
   const double* inv;       // activation inverse
   const double* inv_masked;  // same with occupied cells 0.0 (k-invariant only)
   int inv_per_channel;     // 0: one plane for all k
-  int w, h, c;
+  int w, h, c;             // c = output channels (a shard's interior planes)
+  int halo = -1;           // theta-slab shard: halo planes per side; -1 = whole tensor
 };
 
 // k_generic.cu
@@ -213,7 +222,8 @@ void launch_likelihoods(gl_context* ctx, const uint8_t* occ, const double* score
                         double oy, double cell, double tox, double toy,
                         const int* d_samples, int n, int c,
                         const double2* d_dir, int n_scored,
-                        const double* d_reach, double floor_w, double* d_L);
+                        const double* d_reach, double floor_w, double* d_L,
+                        uint8_t* d_kind);
 void launch_observe_apply(gl_context* ctx, double* buf, int w, int h, int c,
                           const int* d_samples, int n, const double* d_L,
                           double* d_mean);

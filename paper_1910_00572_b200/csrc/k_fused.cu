@@ -41,6 +41,15 @@
 #ifndef GL_FUSED_INVREG_ROWS
 #define GL_FUSED_INVREG_ROWS 8  // tiles up to this height keep inv in registers
 #endif
+#ifndef GL_FUSED_ROWS_H3
+#define GL_FUSED_ROWS_H3 4      // tile rows for H >= 2 (Theta = 360: H = 3)
+#endif
+#ifndef GL_FUSED_MINB_H3
+#define GL_FUSED_MINB_H3 4
+#endif
+#ifndef GL_FUSED_INVREG_ROWS_H3
+#define GL_FUSED_INVREG_ROWS_H3 8
+#endif
 
 namespace glb {
 
@@ -112,7 +121,11 @@ struct FusedParams {
   const double* inv;
   const double* inv_masked;  // inv with occupied cells set to 0.0 (FAST)
   int inv_per_k;
-  int w, h, c;
+  int w, h, c;               // c = output channels (interior planes of a shard)
+  int shard;                 // 1: theta-slab storage with halo planes
+  int plane_off;             // shard: storage plane of iteration 0 (= halo - H)
+  int out_off;               // shard: storage plane of output channel 0 (= halo)
+  int defer_finalize;        // shard: leave the local max for a cross-rank all-reduce
   int tiles_x, n_tiles;
   const BufState* src_state;
   BufState* dst_state;
@@ -237,8 +250,11 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
   const bool scaled = p.src_state->scaled != 0;  // pending 1/max rescale
   const double sc = p.src_state->scale;
 
-  // circular channel of iteration it (m = it - H lies in [-H, C-1+H], H < C)
+  // storage plane of iteration it. One GPU: circular channel m = it - H in
+  // [-H, C-1+H] (H < C). theta-slab shard: planes are stored with their
+  // neighbours' halo planes, so the walk is linear from plane_off.
   auto chan_of = [&](int it) {
+    if (p.shard) return p.plane_off + it;
     const int m = it - H;
     return m < 0 ? m + C : (m >= C ? m - C : m);
   };
@@ -276,7 +292,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
   // L1 per channel for tall ones. FAST folds the output mask into it: for the
   // finite non-negative values of a clean buffer out * 0.0 == +0.0, which is
   // the reference's "out = 0.0" for occupied cells (:466-467).
-  constexpr bool INVREG = ROWS <= GL_FUSED_INVREG_ROWS;
+  constexpr bool INVREG = ROWS <= (H <= 1 ? GL_FUSED_INVREG_ROWS : GL_FUSED_INVREG_ROWS_H3);
   const double* inv_col = (FAST ? p.inv_masked : p.inv) + (out_lane ? si : 0);
   double invr[INVREG ? ROWS : 1];
   uint32_t store_ok = 0;
@@ -308,7 +324,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
       __syncwarp();
     }
     const double* Bb = stage_ptr + ((x0 - R - cs.sx - 1) & 1) + lane;
-    double* orow = out_tile + plane * static_cast<size_t>(emit ? it - 2 * H : 0);  // += W per row
+    double* orow = out_tile + plane * static_cast<size_t>(p.out_off + (emit ? it - 2 * H : 0));  // += W per row
 
     double lo_c0 = Bb[1], lo_c1 = Bb[0];
     double rw[2 * R + 1];  // rolling window of row-pass results
@@ -384,7 +400,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
 }
 
 template <int R, int H, int ROWS, int NS, int NWARP, bool FAST>
-__global__ void __launch_bounds__(32 * NWARP, GL_FUSED_MINB)
+__global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_MINB_H3)
     k_fused_step(const __grid_constant__ CUtensorMap tmap,
                  const FusedParams p) {
   using G = Geo<R, ROWS>;
@@ -426,7 +442,9 @@ __global__ void __launch_bounds__(32 * NWARP, GL_FUSED_MINB)
     if (bm > 0.0) atomicMax(&st->gmax_bits, static_cast<unsigned long long>(__double_as_longlong(bm)));
     __threadfence();
     const unsigned int prev = atomicAdd(&st->blocks_done, 1u);
-    if (prev == gridDim.x - 1) {
+    if (prev == gridDim.x - 1 && p.defer_finalize) {
+      st->blocks_done = 0u;  // gmax_bits stays for the cross-rank all-reduce
+    } else if (prev == gridDim.x - 1) {
       __threadfence();
       const unsigned long long bits = atomicAdd(&st->gmax_bits, 0ull);
       const double g = __longlong_as_double(static_cast<long long>(bits));
@@ -452,7 +470,7 @@ constexpr int kNWARP = 4;  // warps (independent tiles) per CTA
 
 template <int H>
 constexpr int rows_for() {
-  return H <= 1 ? GL_FUSED_ROWS_H1 : 8;
+  return H <= 1 ? GL_FUSED_ROWS_H1 : GL_FUSED_ROWS_H3;
 }
 
 template <int R, int ROWS>
@@ -533,7 +551,8 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
   fp.motion = a.motion;
   fp.param_motion = (a.c <= kParamChannels && a.h_motion != nullptr) ? 1 : 0;
   if (fp.param_motion) {
-    for (int k = 0; k < a.c; ++k) fp.mv[k] = make_double2(a.h_motion[2 * k], a.h_motion[2 * k + 1]);
+    const int planes = a.c + 2 * (a.halo > 0 ? a.halo : 0);  // one vector per storage plane
+    for (int k = 0; k < planes; ++k) fp.mv[k] = make_double2(a.h_motion[2 * k], a.h_motion[2 * k + 1]);
   }
   fp.occ = a.occ;
   fp.inv = a.inv;
@@ -542,6 +561,10 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
   fp.w = a.w;
   fp.h = a.h;
   fp.c = a.c;
+  fp.shard = a.halo >= 0 ? 1 : 0;
+  fp.plane_off = a.halo - ang.n / 2;
+  fp.out_off = a.halo >= 0 ? a.halo : 0;
+  fp.defer_finalize = a.halo >= 0 ? 1 : 0;
   fp.src_state = a.src_state;
   fp.dst_state = a.dst_state;
   fp.step_state = a.step_state;

@@ -116,8 +116,11 @@ __global__ void __launch_bounds__(32) k_dither(
 // Host precomputes, with the reference's libm: per-cell beam score
 // log((1-f)*exp(-d^2/(2 sigma^2)) + f) (and the out-of-map score), and per
 // (channel, scored beam) the (cos, sin) of channel_angle(k) + angle_b. The
-// device keeps the endpoint arithmetic and cell lookup in reference order;
-// the final geometric mean uses CUDA's exp (see DESIGN.md for parity).
+// device keeps the endpoint arithmetic and cell lookup in reference order.
+// The geometric mean's final exp: with `kind` != nullptr the kernel writes
+// the exponent (log_sum / counted) and a case code (0 exp, 1 floor, 2 one)
+// so the host applies glibc's exp, exactly like the reference (default);
+// otherwise CUDA's exp (<= 1 ulp from glibc).
 __global__ void k_likelihoods(const uint8_t* __restrict__ occ,
                               const double* __restrict__ score, double oob_score,
                               int w, int h, double res, double ox, double oy,
@@ -125,7 +128,8 @@ __global__ void k_likelihoods(const uint8_t* __restrict__ occ,
                               const int* __restrict__ samples,
                               int n, int c, const double2* __restrict__ dir,
                               int n_scored, const double* __restrict__ reach,
-                              double floor_w, double* __restrict__ L) {
+                              double floor_w, double* __restrict__ L,
+                              uint8_t* __restrict__ kind) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n * c) return;
   const int s = q / c, k = q % c;
@@ -136,6 +140,7 @@ __global__ void k_likelihoods(const uint8_t* __restrict__ occ,
   if (!(pi >= 0 && pi < w && pj >= 0 && pj < h) ||
       occ[static_cast<size_t>(pj) * w + pi]) {
     L[q] = floor_w;
+    if (kind) kind[q] = 1;
     return;
   }
   double log_sum = 0.0;
@@ -150,7 +155,12 @@ __global__ void k_likelihoods(const uint8_t* __restrict__ occ,
     log_sum += in ? score[static_cast<size_t>(cj) * w + ci] : oob_score;
     ++counted;
   }
-  L[q] = counted == 0 ? 1.0 : exp(log_sum / counted);
+  if (kind) {
+    kind[q] = counted == 0 ? 2 : 0;
+    L[q] = counted == 0 ? 1.0 : log_sum / counted;
+  } else {
+    L[q] = counted == 0 ? 1.0 : exp(log_sum / counted);
+  }
 }
 
 // Sequential mean over all sampled states (observation.cpp:139-141).
@@ -206,11 +216,12 @@ void launch_likelihoods(gl_context* ctx, const uint8_t* occ, const double* score
                         double oy, double cell, double tox, double toy,
                         const int* d_samples, int n,
                         int c, const double2* d_dir, int n_scored,
-                        const double* d_reach, double floor_w, double* d_L) {
+                        const double* d_reach, double floor_w, double* d_L,
+                        uint8_t* d_kind) {
   const int total = n * c;
   k_likelihoods<<<(total + 127) / 128, 128, 0, ctx->stream>>>(
       occ, score, oob_score, w, h, res, ox, oy, cell, tox, toy, d_samples, n, c, d_dir,
-      n_scored, d_reach, floor_w, d_L);
+      n_scored, d_reach, floor_w, d_L, d_kind);
   ctx->launches++;
 }
 

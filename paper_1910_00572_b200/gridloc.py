@@ -458,6 +458,13 @@ class BeliefTensor:
         check(self.ctx.lib.gl_tensor_download(self.ctx.h, self.h, _d(out)))
         return out
 
+    def at(self, i: int, j: int, k: int) -> float:
+        """One element (belief_tensor.hpp:55-60), read from the device."""
+        x = C.c_double()
+        off = (k * self._h + j) * self._w + i
+        check(self.ctx.lib.gl_tensor_read(self.ctx.h, self.h, off, 1, C.byref(x)))
+        return x.value
+
     def set_values(self, vals):
         v = np.ascontiguousarray(vals, dtype=np.float64).reshape(self._c, self._h, self._w)
         check(self.ctx.lib.gl_tensor_upload(self.ctx.h, self.h, _d(v)))

@@ -1,0 +1,180 @@
+"""theta-slab sharding of one belief tensor across ranks.
+
+Rank r of G owns global channels [r*C/G, (r+1)*C/G). The step is channel-
+local except the circular angular stencil (+-H channels,
+belief_tensor.cpp:449-451), so each rank stores `halo` neighbour planes per
+side and a step is
+
+  1. the fused kernel on the local slab (reads halo planes, writes interior
+     planes, leaves the local max),
+  2. an all-reduce MAX of the 8-byte max (uint64 bits of a double >= 0: the
+     integer order is the value order),
+  3. finalize (extinguish status, pending 1/max rescale — global, so every
+     rank scales identically),
+  4. the halo exchange: my first/last `halo` interior planes go to the
+     left/right neighbour's upper/lower halo (NCCL send/recv over NVLink).
+
+No per-element operation changes, so the sharded belief is bitwise the
+unsharded one. The exchange plan and the argmax combine are pure functions
+(tested with gloo on CPU); device memory is handed to torch.distributed
+through __cuda_array_interface__ (zero copy) on the library's own stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import check
+
+
+def partition(c_total: int, world: int, rank: int):
+    """[c_begin, c_end) of rank (contiguous, sizes differ by at most 1)."""
+    return rank * c_total // world, (rank + 1) * c_total // world
+
+
+@dataclass(frozen=True)
+class HaloPlan:
+    """Storage-plane ranges for one rank's halo exchange.
+
+    storage plane q <-> global channel (c_begin - halo + q) mod c_total."""
+    rank: int
+    world: int
+    left: int           # rank owning the channels just below mine (circular)
+    right: int          # rank owning the channels just above mine
+    send_left: tuple    # (q0, count): my first `halo` interior planes
+    send_right: tuple   # my last `halo` interior planes
+    recv_left: tuple    # my lower halo planes (from the left neighbour's last)
+    recv_right: tuple   # my upper halo planes (from the right neighbour's first)
+
+
+def halo_plan(c_total: int, world: int, rank: int, halo: int) -> HaloPlan:
+    c0, c1 = partition(c_total, world, rank)
+    n = c1 - c0
+    if halo > min(partition(c_total, world, r)[1] - partition(c_total, world, r)[0] for r in range(world)):
+        raise ValueError("halo wider than a shard: use fewer ranks or a larger channel count")
+    return HaloPlan(rank, world, (rank - 1) % world, (rank + 1) % world,
+                    send_left=(halo, halo), send_right=(n, halo),
+                    recv_left=(0, halo), recv_right=(halo + n, halo))
+
+
+def combine_argmax(cands):
+    """cands: per-rank (value, global flat index); the reference keeps the
+    first strict maximum in (k, j, i) order (belief_tensor.cpp:518-527), i.e.
+    the largest value with the lowest flat index."""
+    best = None
+    for v, idx in cands:
+        if not (v > -1.0):
+            continue
+        if best is None or v > best[0] or (v == best[0] and idx < best[1]):
+            best = (v, idx)
+    return best
+
+
+def exchange_planes(dist, planes, plan: HaloPlan, group=None):
+    """Halo exchange through torch.distributed point-to-point ops.
+    planes(q0, count) returns a tensor view of storage planes q0..q0+count-1
+    (a zero-copy device alias on GPUs, a CPU tensor under gloo in tests)."""
+    # Messages between one pair of ranks match in issue order (NCCL has no
+    # tags), and with two ranks left == right: every rank sends right-edge
+    # then left-edge and receives lower-halo then upper-halo, so the first
+    # message a rank gets from its left neighbour is that neighbour's right
+    # edge, the second from its right neighbour is that neighbour's left edge.
+    ops = [
+        dist.P2POp(dist.isend, planes(*plan.send_right), plan.right, group),
+        dist.P2POp(dist.isend, planes(*plan.send_left), plan.left, group),
+        dist.P2POp(dist.irecv, planes(*plan.recv_left), plan.left, group),
+        dist.P2POp(dist.irecv, planes(*plan.recv_right), plan.right, group),
+    ]
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+
+
+class _CAI:
+    """Zero-copy device view for torch.as_tensor(..., device='cuda')."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+class ThetaShard:
+    """This rank's slab. Collectives go through torch.distributed (NCCL) on
+    the library's stream; one process per GPU."""
+
+    def __init__(self, m, c_total: int, halo: int, rank: int, world: int, ctx, group=None):
+        import torch
+        import torch.distributed as dist
+        from .gridloc import BeliefTensor
+        self.torch, self.dist, self.group = torch, dist, group
+        self.ctx, self.map = ctx, m
+        self.c_total, self.halo, self.rank, self.world = c_total, halo, rank, world
+        self.c_begin, self.c_end = partition(c_total, world, rank)
+        self.plan = halo_plan(c_total, world, rank, halo)
+        h = C.c_void_p()
+        check(ctx.lib.gl_shard_init_uniform(ctx.h, m.h, c_total, self.c_begin, self.c_end, halo, C.byref(h)))
+        self.t = BeliefTensor(ctx=ctx, _handle=h)
+        self.stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", ctx.device))
+        self.plane_elems = m.width() * m.height()
+
+    def _planes(self, q0: int, count: int):
+        p = C.POINTER(C.c_double)()
+        check(self.ctx.lib.gl_tensor_plane_ptr(self.ctx.h, self.t.h, q0, C.byref(p)))
+        ptr = C.cast(p, C.c_void_p).value
+        return self.torch.as_tensor(_CAI(ptr, (count, self.plane_elems), "<f8"), device=f"cuda:{self.ctx.device}")
+
+    def _max_tensor(self):
+        p = C.POINTER(C.c_uint64)()
+        check(self.ctx.lib.gl_tensor_max_ptr(self.ctx.h, self.t.h, C.byref(p)))
+        return self.torch.as_tensor(_CAI(C.cast(p, C.c_void_p).value, (1,), "<i8"),
+                                    device=f"cuda:{self.ctx.device}")
+
+    def step(self, u, kernels, act):
+        """One sharded Algorithm-1 step (asynchronous on the device)."""
+        from .gridloc import step_async
+        step_async(self.t, u, self.map, kernels, act, self.ctx)
+        with self.torch.cuda.stream(self.stream):
+            if self.world > 1:
+                self.dist.all_reduce(self._max_tensor(), op=self.dist.ReduceOp.MAX, group=self.group)
+            check(self.ctx.lib.gl_shard_finalize(self.ctx.h, self.t.h))
+            self.exchange_halos()
+
+    def exchange_halos(self):
+        pl = self.plan
+        if self.world == 1:
+            lib = self.ctx.lib
+            # circular: lower halo <- my last planes, upper halo <- my first
+            check(lib.gl_tensor_copy_planes(self.ctx.h, self.t.h, pl.recv_left[0], self.t.h, pl.send_right[0],
+                                            self.halo))
+            check(lib.gl_tensor_copy_planes(self.ctx.h, self.t.h, pl.recv_right[0], self.t.h, pl.send_left[0],
+                                            self.halo))
+            return
+        exchange_planes(self.dist, self._planes, pl, self.group)
+
+    def status(self):
+        from .gridloc import tensor_status
+        tensor_status(self.t)
+
+    def argmax(self):
+        """Global argmax_state: local candidate, all-gather, lowest-index rule."""
+        from .gridloc import BeliefExtinguishedError, argmax_state
+        W = self.map.width()
+        try:
+            e = argmax_state(self.t)
+            flat = (self.c_begin + e.k) * self.plane_elems + e.j * W + e.i
+            val = self.t.at(e.i, e.j, e.k)
+        except BeliefExtinguishedError:
+            val, flat = -1.0, 0
+        t = self.torch.tensor([val, float(flat)], dtype=self.torch.float64, device=f"cuda:{self.ctx.device}")
+        out = [self.torch.zeros_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        best = combine_argmax([(float(o[0]), int(o[1])) for o in out])
+        if best is None:
+            raise RuntimeError("argmax on an all-zero belief tensor")
+        plane = self.plane_elems
+        k, p = divmod(best[1], plane)
+        j, i = divmod(p, self.map.width())
+        return best[0], (i, j, k)

@@ -1,0 +1,91 @@
+"""Multi-rank host logic of the theta-slab sharding, world size 2 and 3 with
+the gloo backend on CPU (one process per rank, 127.0.0.1 rendezvous):
+partitioning, the halo plan, the point-to-point exchange of storage planes,
+the MAX all-reduce on the uint64 bits of the step max, and the argmax
+combine rule. Device compute is covered by tests/test_gpu_sharding.py."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1910_00572_b200.sharding import combine_argmax, exchange_planes, halo_plan, partition
+
+PLANE = 12  # elements per plane in these host-only tests
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, c_total, halo, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        c0, c1 = partition(c_total, world, rank)
+        n = c1 - c0
+        plan = halo_plan(c_total, world, rank, halo)
+        # storage: halo | interior | halo; interior plane of channel k holds k
+        store = torch.full((n + 2 * halo, PLANE), -1.0, dtype=torch.float64)
+        for qq in range(halo, halo + n):
+            store[qq] = float(c0 + qq - halo)
+
+        exchange_planes(dist, lambda q0, cnt: store[q0:q0 + cnt], plan)
+        got = [float(store[qq, 0]) for qq in range(n + 2 * halo)]
+        want = [float((c0 - halo + qq) % c_total) for qq in range(n + 2 * halo)]
+
+        # MAX all-reduce of the step max as uint64 bits of doubles >= 0
+        local = np.array([0.25 * (rank + 1)], dtype=np.float64).view(np.int64)
+        t = torch.from_numpy(local.copy())
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gmax = float(t.numpy().view(np.float64)[0])
+
+        # argmax combine: ties across ranks resolve to the lowest flat index
+        cand = torch.tensor([1.0, float(1000 - rank)], dtype=torch.float64)
+        outs = [torch.zeros_like(cand) for _ in range(world)]
+        dist.all_gather(outs, cand)
+        best = combine_argmax([(float(o[0]), int(o[1])) for o in outs])
+        q.put((rank, got == want, got, want, gmax, best))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,c_total,halo", [(2, 8, 1), (3, 36, 1), (2, 360, 3), (3, 16, 2)])
+def test_halo_exchange_allreduce_argmax(world, c_total, halo):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, c_total, halo, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok, got, want, gmax, best in res:
+        assert ok, (rank, got, want)
+        assert gmax == 0.25 * world
+        assert best == (1.0, 1000 - (world - 1))
+
+
+def test_partition_and_plan():
+    assert [partition(72, 8, r) for r in range(8)] == [(9 * r, 9 * r + 9) for r in range(8)]
+    assert sum(b - a for a, b in (partition(10, 3, r) for r in range(3))) == 10
+    p = halo_plan(360, 8, 0, 3)
+    assert (p.left, p.right) == (7, 1)
+    assert p.send_left == (3, 3) and p.send_right == (45, 3)
+    assert p.recv_left == (0, 3) and p.recv_right == (48, 3)
+    with pytest.raises(ValueError):
+        halo_plan(8, 8, 0, 2)
+
+
+def test_combine_argmax_rules():
+    assert combine_argmax([(0.5, 10), (0.7, 99), (0.7, 3)]) == (0.7, 3)
+    assert combine_argmax([(-1.0, 0), (-1.0, 5)]) is None
+    assert combine_argmax([(float("nan"), 0), (0.1, 4)]) == (0.1, 4)
