@@ -46,6 +46,8 @@ CONFIGS = {
     "c1": dict(W=256, H=256, C=36, workload="256x256x36 floor-plan, odometry+map only (BASELINE configs[0])"),
     "c5": dict(W=512, H=512, C=72, workload="512x512x72 floor-plan (BASELINE configs[4], one robot)"),
     "c4s": dict(W=2048, H=2048, C=360, workload="2048x2048x360 floor-plan (config-4 angular width, 1/4 area)"),
+    "c5": dict(W=512, H=512, C=72, batch=64, workload="batch of 64 independent robots/maps at 512x512x72 "
+                                                      "(BASELINE configs[4])"),
     "c4": dict(W=4096, H=4096, C=360, workload="4096x4096x360 floor-plan on ONE B200 (BASELINE configs[3]; "
                                               "2 x 48.3 GB ping-pong in HBM)"),
 }
@@ -240,8 +242,188 @@ def run_reference(args, cfg, world, rank):
 
 
 # ------------------------------------------------------------------- ours
+def measure_extras(g, ctx, m, ks, act, t, cfg, args):
+    """Secondary numbers on the same engine (not the headline):
+    * trace_mix_hz: a recorded Localizer trace (reference simulator +
+      trigger, tests/golden/trace_*.npy) — ~80% rotation-only steps (r = 0
+      kernels, SURVEY.md §3.2), same algorithmic bytes per step;
+    * lidar: config 3's observation cycle (belief_map -> Floyd-Steinberg
+      (budget 512) -> likelihood update) latency, and the step rate with one
+      observation every 16 steps (the cmd_bench cadence, gridloc_main.cpp:236).
+    """
+    import numpy as np
+    from paper_1910_00572_b200.floorplan import make_floorplan, simple_scan
+    W, H, C = cfg["W"], cfg["H"], cfg["C"]
+    out = {}
+    path = os.path.join(ROOT, "tests", "golden", f"trace_{W}x{C}.npy")
+    if os.path.exists(path):
+        tr = np.load(path)
+        rk = g.build_kernels(g.MotionNoise(1e-4, 1e-4, 0.012), C, m.resolution(), 2.0 * math.pi / C)
+        ract = g.make_activation(m, rk, C, ctx)
+        n = min(len(tr), 1000)
+        for e in tr[:20]:
+            g.step_async(t, g.OdometryDelta(*e[:3]), m, (ks, rk)[int(e[3])], (act, ract)[int(e[3])], ctx)
+        ctx.synchronize()
+        ctx.mark(2)
+        for e in tr[:n]:
+            g.step_async(t, g.OdometryDelta(*e[:3]), m, (ks, rk)[int(e[3])], (act, ract)[int(e[3])], ctx)
+        ctx.mark(3)
+        ms = ctx.marks_ms(2, 3)
+        g.tensor_status(t)
+        out["trace_mix_hz"] = n / (ms / 1e3)
+        out["trace_mix_rotation_share"] = float(tr[:n, 3].mean())
+    if C <= 128:
+        occ = make_floorplan(W, H, seed=0)
+        js, is_ = np.nonzero(occ == 0)
+        q = len(is_) // 2
+        a, r = simple_scan(occ, is_[q] * 0.1 + 0.05, js[q] * 0.1 + 0.05, 0.3)
+        f = g.DistanceField(m, ctx)
+        scan = g.LidarScan(a, r, 8.0)
+        cycles = []
+        for _ in range(4):
+            t0 = time.perf_counter()
+            smp = g.dither_samples(t, 512)
+            g.observation_update(t, smp, scan, m, f, g.LikelihoodParams())
+            cycles.append(time.perf_counter() - t0)
+        cyc = statistics.median(cycles[1:])
+        step_s = 1.0 / out.get("trace_mix_hz", 1.0) if "trace_mix_hz" in out else None
+        out["lidar_cycle_ms"] = cyc * 1e3
+        out["lidar_samples"] = int(len(smp.cells))
+        if step_s:
+            out["lidar_config_hz"] = 16.0 / (16.0 * step_s + cyc)
+    return out
+
+
+def run_batch(args, cfg, world, rank, local):
+    """Config 5: a batch of independent robots (own map, tensor) on one GPU,
+    one CUDA stream per 8 robots; value = batch steps per second (every robot
+    stepped once per batch step)."""
+    import paper_1910_00572_b200 as g
+    from paper_1910_00572_b200.floorplan import make_floorplan, write_pgm
+    W, H, C, B = cfg["W"], cfg["H"], cfg["C"], cfg["batch"]
+    ctxs = [g.Context(local) for _ in range(max(1, B // 8))]
+    robots = []
+    for r in range(B):
+        ctx = ctxs[r % len(ctxs)]
+        m = g.load_map(write_pgm(make_floorplan(W, H, seed=100 + r + 1000 * rank)), 250, 0.1, ctx=ctx)
+        ks = g.build_kernels(g.MotionNoise(), C, 0.1, 2.0 * math.pi / C)
+        robots.append((ctx, m, ks, g.make_activation(m, ks, C, ctx), g.init_uniform(m, C, ctx)))
+    u = g.OdometryDelta(0.1, 0.0, 0.0)
+
+    def batch_step():
+        for ctx, m, ks, act, t in robots:
+            g.step_async(t, u, m, ks, act, ctx)
+
+    for _ in range(args.warmup):
+        batch_step()
+    for c in ctxs:
+        c.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    dist_barrier(world)
+    n0 = sum(c.launch_count() for c in ctxs)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        batch_step()
+    for c in ctxs:
+        c.synchronize()
+    dt = time.perf_counter() - t0
+    clk = clocks.stop()
+    for ctx, m, ks, act, t in robots:
+        g.tensor_status(t)
+    dt = dist_max(dt, world, "ours")
+    value = world * args.steps / dt
+    bytes_batch = B * algo_bytes(W, H, C)
+    peak, peak_src = measured_peak()
+    if rank != 0:
+        return 0
+    print(json.dumps({
+        "metric": "batch belief updates/sec (every robot stepped once) at 64 x 512^2x72", "value": value,
+        "unit": "batch-Hz", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "W": W, "H": H, "channels": C, "robots_per_gpu": B,
+                   "parallelism": f"{B} independent tensors per GPU on {len(ctxs)} streams",
+                   "timing": "host wall clock around K batch steps with device syncs"},
+        "e2e": None,
+        "roofline": {"bound": "hbm", "achieved": bytes_batch * value / world / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": bytes_batch * value / world / 1e9 / peak, "traffic": None, "peak_source": peak_src,
+                     "bytes_per_launch": algo_bytes(W, H, C), "note": "aggregate over the batch's launches"},
+        "cpu_baseline": None, "gpu_launches": sum(c.launch_count() for c in ctxs) - n0, "clocks": clk,
+    }))
+    return 0
+
+
+def run_sharded(args, cfg, world, rank, local):
+    """theta-slab sharding of ONE belief across the ranks (strong scaling):
+    per step the fused kernel on each slab, a MAX all-reduce of the 8-byte
+    step max and the halo-plane exchange, both over NCCL on the library's
+    stream (paper_1910_00572_b200/sharding.py)."""
+    import paper_1910_00572_b200 as g
+    from paper_1910_00572_b200.sharding import ThetaShard
+    W, H, C = cfg["W"], cfg["H"], cfg["C"]
+    ctx = g.Context(local)
+    m = g.load_map(make_map_bytes(W, H), 250, 0.1, ctx=ctx)
+    ks = g.build_kernels(g.MotionNoise(), C, m.resolution(), 2.0 * math.pi / C)
+    act = g.make_activation(m, ks, C, ctx)
+    halo = max(1, len(ks.angular) // 2)
+    shard = ThetaShard(m, C, halo, rank, world, ctx)
+    u = g.OdometryDelta(m.resolution(), 0.0, 0.0)
+    for _ in range(args.warmup):
+        shard.step(u, ks, act)
+    ctx.synchronize()
+    shard.status()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    dist_barrier(world)
+    ctx.synchronize()
+    n0 = ctx.launch_count()
+    ctx.time_steps(True)
+    ctx.mark(0)
+    for _ in range(args.steps):
+        shard.step(u, ks, act)
+    ctx.mark(1)
+    ms = ctx.marks_ms(0, 1)
+    launches = ctx.launch_count() - n0
+    kern_ms, kern_n = ctx.step_times()
+    ctx.time_steps(False)
+    clk = clocks.stop()
+    shard.status()
+    ms_max = dist_max(ms, world, "ours")
+    value = args.steps / (ms_max / 1e3)  # steps of the ONE sharded belief
+    n_local = shard.c_end - shard.c_begin
+    bytes_launch = 2 * 8 * W * H * n_local + W * H + 8 * W * H
+    achieved = bytes_launch / ((kern_ms / max(kern_n, 1)) / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    if rank != 0:
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": "Hz", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "W": W, "H": H, "channels": C,
+                   "parallelism": f"theta-slab sharding over {world} GPU(s), {n_local} channels + 2x{halo} "
+                                  "halo planes per GPU; NCCL all-reduce (8 B) + halo send/recv per step",
+                   "l2": "the per-GPU slab exceeds L2"},
+        "e2e": None,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_source": peak_src, "bytes_per_launch": bytes_launch,
+                     "avg_kernel_ms": kern_ms / max(kern_n, 1), "launches_timed": kern_n,
+                     "note": "per-GPU fused kernel on its slab"},
+        "cpu_baseline": None, "gpu_launches": launches, "clocks": clk,
+    }
+    print(json.dumps(line))
+    return 0
+
+
 def run_ours(args, cfg, world, rank, local):
     import paper_1910_00572_b200 as g
+    if args.shard:
+        return run_sharded(args, cfg, world, rank, local)
+    if "batch" in cfg:
+        return run_batch(args, cfg, world, rank, local)
     W, H, C = cfg["W"], cfg["H"], cfg["C"]
     ctx = g.Context(local)
     pgm = make_map_bytes(W, H)
@@ -287,6 +469,8 @@ def run_ours(args, cfg, world, rank, local):
     e2e_s = dist_max(e2e_s, world, "ours")
     e2e = world * n_e2e / e2e_s
 
+    extras = {} if args.no_extras else measure_extras(g, ctx, m, ks, act, t, cfg, args)
+
     bytes_launch = algo_bytes(W, H, C)
     avg_kern_s = (kern_ms / max(kern_n, 1)) / 1e3
     achieved = bytes_launch / avg_kern_s / 1e9
@@ -324,6 +508,7 @@ def run_ours(args, cfg, world, rank, local):
         "cpu_baseline": cpu,
         "gpu_launches": launches,
         "clocks": clk,
+        "extras": extras,
     }
     print(json.dumps(line))
     return 0
@@ -340,6 +525,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--ref-budget-s", type=float, default=90.0)
+    ap.add_argument("--no-extras", action="store_true", help="skip the trace-mix / LIDAR-cycle extras")
+    ap.add_argument("--shard", action="store_true",
+                    help="theta-shard ONE belief across the ranks (strong scaling; e.g. --config c4)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

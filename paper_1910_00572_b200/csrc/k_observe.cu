@@ -5,16 +5,15 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
 
 #include "gl_internal.hpp"
 
 namespace glb {
 
 namespace {
-
-__device__ __forceinline__ double dmax_ref(double a, double b) {
-  return (a < b) ? b : a;
-}
 
 // Floyd-Steinberg target weights, in the reference's target order:
 // (dir,0) 7/16, (-dir,1) 3/16, (0,1) 5/16, (dir,1) 1/16.
@@ -27,6 +26,329 @@ __device__ __forceinline__ double fs_wsum(int i, int j, int w, int h, int dir) {
     if (i + dir >= 0 && i + dir < w) ws += 1.0 / 16.0;
   }
   return ws;
+}
+
+// In-row carry coefficient (7/16)/wsum of pixel i in row j (direction dir);
+// 0 when its (dir,0) target is outside the grid or wsum == 0.
+__device__ __forceinline__ double fs_carry_coef(int i, int j, int w, int h, int dir) {
+  if (!(i + dir >= 0 && i + dir < w)) return 0.0;
+  const double ws = fs_wsum(i, j, w, h, dir);
+  if (ws == 1.0) return 7.0 / 16.0;  // interior rows: x / 1 == x, no division
+  return ws > 0.0 ? (7.0 / 16.0) / ws : 0.0;
+}
+
+// Pipelined serpentine Floyd-Steinberg (observation.cpp:11-71), bit-identical
+// to the reference's serial sweep:
+//   warp 0, lane 0: the sequential total (observation.cpp:16-17), then the
+//     in-row carry chain v = pre + carry; carry = e * (7/16)/wsum, run
+//     speculatively in groups that assume no emission (fs_spec_groups; the
+//     0.5 threshold on a support cell fires ~once per two rows) and replay a
+//     group exactly when one does: ~1 DADD + 1 DMUL latency per pixel;
+//   warp 1: pre-accumulates row j+1 (bm*scale plus row j's diffused errors in
+//     the reference's arrival order: upstream, centre, downstream source)
+//     while the chain is still in row j, a few pixels behind it, via a
+//     shared-memory progress counter.
+// Serpentine order has no inter-row wavefront (row j+1 starts where row j
+// ended), so the W*H chain of dependent FP64 ops is inherent.
+// acquire/release fence at CTA scope (MEMBAR.ALL.CTA; __threadfence_block
+// is sequentially consistent)
+__device__ __forceinline__ void fence_cta() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
+// Speculative in-row sweep of k_dither_pipe, G pixels per group, scan-order
+// rows at index q + 1: assumes "no emission in this group", so the chain is a
+// pure DADD->DMUL dependency (bit-identical to the exact sweep up to the
+// first emission); the threshold tests are reduced once per group:
+// v >= 0.5 <=> the high word of v, as a signed int, is >= 0x3FE00000
+// (negative v has the sign bit set), so an integer max over the
+// support-masked high words keeps predicates off the chain. Returns true,
+// with q/carry at the start of the offending group, when a group emits (its
+// err values are then rewritten by the exact replay); false at the row tail.
+// kConstC: the carry coefficient is 7/16 (every row but the last) and is
+// folded into the multiply as an immediate.
+template <int G, bool kConstC>
+__device__ __forceinline__ bool fs_spec_groups(const double* pre, double* err,
+                                               const unsigned int* sup, int& q,
+                                               double& carry, double c_reg, int w,
+                                               volatile int* progress) {
+  const double c = kConstC ? 7.0 / 16.0 : c_reg;
+  for (; q + G <= w - 1; q += G) {
+    double2 pv[G / 2];
+    const double2* p2 = reinterpret_cast<const double2*>(pre + q + 1);
+#pragma unroll
+    for (int k = 0; k < G / 2; ++k) pv[k] = p2[k];
+    double cr = carry;
+    int mx = 0;
+    double2* e2 = reinterpret_cast<double2*>(err + q + 1);
+    constexpr int GH = G < 32 ? G : 32;
+#pragma unroll
+    for (int hf = 0; hf < G / GH; ++hf) {
+      const int qh = q + 32 * hf;
+      const unsigned long long sw =
+          static_cast<unsigned long long>(sup[qh >> 5]) |
+          (static_cast<unsigned long long>(sup[(qh >> 5) + 1]) << 32);
+      const int sh = qh & 31;
+#pragma unroll
+      for (int k = 0; k < GH; k += 2) {
+        const double2 in = pv[(32 * hf + k) / 2];
+        const double v0 = in.x + cr;
+        cr = v0 * c;
+        const double v1 = in.y + cr;
+        cr = v1 * c;
+        e2[(32 * hf + k) / 2] = make_double2(v0, v1);
+        mx = max(mx, __double2hiint(v0) & -static_cast<int>((sw >> (sh + k)) & 1ull));
+        mx = max(mx, __double2hiint(v1) & -static_cast<int>((sw >> (sh + k + 1)) & 1ull));
+      }
+    }
+    if (__builtin_expect(mx >= 0x3FE00000, 0)) return true;
+    carry = cr;
+    fence_cta();
+    *progress = q + G;
+  }
+  return false;
+}
+
+__device__ long long g_dither_clk[4];  // phase timestamps (debug read-out)
+
+__global__ void __launch_bounds__(64) k_dither_pipe(
+    const double* __restrict__ bm, int w, int h, int budget,
+    int* __restrict__ cells, int cap, int* __restrict__ n_out,
+    double* __restrict__ mass_out) {
+  extern __shared__ double sh2[];
+  // rows of RS doubles (scan order at index q + 1; RS even keeps 16-byte
+  // alignment)
+  const int RS = (w + 3) & ~1;
+  double* pre0 = sh2;            // pre-accumulated work of the even rows
+  double* pre1 = sh2 + RS;       // odd rows
+  double* err = sh2 + 2 * RS;    // errors of the row being swept
+  double* nrow = sh2 + 3 * RS;   // w: row j+1 of bm, staged by the helper
+  // bm > 0 per pixel as bits in the row's scan order (32 pixels per word)
+  unsigned int* sup0 = reinterpret_cast<unsigned int*>(sh2 + 3 * RS + w);
+  unsigned int* sup1 = sup0 + (w + 31) / 32 + 1;
+  double* ring = sh2;            // phase A: 3 rows of bm staged for the total
+  __shared__ volatile int progress;   // pixels of the current row swept
+  __shared__ volatile int pre_ready;  // rows whose pre is complete
+  __shared__ volatile int filled, consumed;
+  __shared__ double s_scale;
+  __shared__ int s_stop;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int words = (w + 31) / 32;
+
+  if (tid == 0) {
+    progress = 0;
+    pre_ready = 0;
+    filled = 0;
+    consumed = 0;
+    g_dither_clk[0] = clock64();
+  }
+  __syncthreads();
+  // ---- phase A: total = sequential sum in row-major order (:16-17) -------
+  if (warp == 1) {
+    for (int r = 0; r < h; ++r) {
+      while (r - consumed >= 3) {
+      }
+      double* dst = ring + static_cast<size_t>(r % 3) * w;
+      const double* src = bm + static_cast<size_t>(r) * w;
+      for (int t = lane; t < w; t += 32) dst[t] = src[t];
+      __syncwarp();
+      fence_cta();
+      if (lane == 0) filled = r + 1;
+      __syncwarp();
+    }
+  } else if (tid == 0) {
+    double total = 0.0;
+    for (int r = 0; r < h; ++r) {
+      while (filled <= r) {
+      }
+      fence_cta();
+      const double* row = ring + static_cast<size_t>(r % 3) * w;
+      int t = 0;
+      for (; t + 16 <= w; t += 16) {
+        double x[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) x[k] = row[t + k];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) total += x[k];
+      }
+      for (; t < w; ++t) total += row[t];
+      fence_cta();
+      consumed = r + 1;
+    }
+    *mass_out = total;
+    s_stop = !(total > 0.0);
+    s_scale = budget / total;
+    g_dither_clk[1] = clock64() - g_dither_clk[0];
+  }
+  __syncthreads();
+  if (s_stop) {
+    if (tid == 0) *n_out = 0;
+    return;
+  }
+  const double scale = s_scale;
+  // ---- phase B: row 0's work; the ring is free again ----------------------
+  // pre/err rows are kept in the row's SCAN order at index q + 1, so the
+  // chain's 32-pixel groups (q = 1 + 32m) are 16-byte aligned and addressed
+  // with immediate offsets from one base register
+  for (int t = tid; t < w; t += blockDim.x) pre0[t + 1] = bm[t] * scale;
+  for (int wd = tid; wd <= words; wd += blockDim.x) {
+    unsigned int bits = 0;
+    for (int k = 0; k < 32; ++k) {
+      const int pos = wd * 32 + k;  // row 0 sweeps left to right
+      if (pos < w && bm[pos] > 0.0) bits |= 1u << k;
+    }
+    sup0[wd] = bits;
+  }
+  if (tid == 0) pre_ready = 1;
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane != 0) return;
+    int count = 0;
+    long long waited = 0, waited_end = 0;
+    const long long t_b = clock64();
+    auto record = [&](int i, int j) {
+      if (count < cap) {
+        cells[2 * count] = i;
+        cells[2 * count + 1] = j;
+      }
+      ++count;
+    };
+    for (int j = 0; j < h; ++j) {
+      const int dir = (j % 2 == 0) ? 1 : -1;
+      const double* pre = (j & 1) ? pre1 : pre0;
+      const unsigned int* sup = (j & 1) ? sup1 : sup0;
+      const long long tw = clock64();
+      while (pre_ready < j + 1) {
+      }
+      waited += clock64() - tw;
+      fence_cta();
+      const int start = dir == 1 ? 0 : w - 1;
+      const double c_first = fs_carry_coef(start, j, w, h, dir);
+      const double c_mid = (w > 2) ? fs_carry_coef(start + dir, j, w, h, dir) : 0.0;
+      // q = 0: no in-row carry flows into the first pixel
+      double carry;
+      {
+        const double v = pre[1];
+        double e = v;
+        if (v >= 0.5 && (sup[0] & 1u)) {
+          e = v - 1.0;
+          record(start, j);
+        }
+        err[1] = e;
+        carry = e * c_first;
+      }
+      // exact per-pixel step for pixels 1 .. w-2 (carry coefficient c_mid)
+      auto body = [&](int q, bool s) {
+        const double v = pre[q + 1] + carry;
+        double next;
+        asm("mul.rn.f64 %0, %1, %2;" : "=d"(next) : "d"(v), "d"(c_mid));
+        double e = v;
+        if (__builtin_expect(v >= 0.5 && s, 0)) {
+          e = v - 1.0;
+          next = e * c_mid;
+          record(start + q * dir, j);
+        }
+        err[q + 1] = e;
+        carry = next;
+      };
+      int q = 1;
+      // speculative groups (fs_spec_groups) of 32 pixels, then one each of
+      // 16, 8, 4, 2 for the row tail; a group with an emission is replayed
+      // exactly here, then speculation resumes
+      auto sweep = [&](auto gsize) {
+        constexpr int G = decltype(gsize)::value;
+        while (c_mid == 7.0 / 16.0
+                   ? fs_spec_groups<G, true>(pre, err, sup, q, carry, c_mid, w, &progress)
+                   : fs_spec_groups<G, false>(pre, err, sup, q, carry, c_mid, w, &progress)) {
+#pragma unroll 1
+          for (int k = 0; k < G; ++k) {
+            const int qk = q + k;
+            body(qk, (sup[qk >> 5] >> (qk & 31)) & 1u);
+          }
+          q += G;
+          fence_cta();
+          progress = q;
+        }
+      };
+      sweep(std::integral_constant<int, 32>{});
+      sweep(std::integral_constant<int, 16>{});
+      sweep(std::integral_constant<int, 8>{});
+      sweep(std::integral_constant<int, 4>{});
+      sweep(std::integral_constant<int, 2>{});
+      for (; q < w - 1; ++q) body(q, (sup[q >> 5] >> (q & 31)) & 1u);
+      if (w > 1) {  // last pixel: no in-row target
+        const double v = pre[w] + carry;
+        double e = v;
+        if (v >= 0.5 && ((sup[(w - 1) >> 5] >> ((w - 1) & 31)) & 1u)) {
+          e = v - 1.0;
+          record(start + (w - 1) * dir, j);
+        }
+        err[w] = e;
+      }
+      fence_cta();
+      progress = w;
+      // the helper resets progress once it has consumed row j
+      const long long te = clock64();
+      while (progress != 0 && j + 1 < h) {
+      }
+      waited_end += clock64() - te;
+    }
+    *n_out = count;
+    g_dither_clk[2] = clock64() - t_b;
+    g_dither_clk[3] = waited;
+    g_dither_clk[0] = waited_end;
+    return;
+  }
+
+  // warp 1: pre-accumulate row j+1 from row j's errors, behind the chain
+  for (int j = 0; j + 1 < h; ++j) {
+    const int pd = (j % 2 == 0) ? 1 : -1;  // row j's direction
+    const int jn = j + 1;
+    double* pre = (jn & 1) ? pre1 : pre0;
+    unsigned int* sup = (jn & 1) ? sup1 : sup0;
+    const int dn = -pd;                    // row j+1's direction
+    const int start_n = dn == 1 ? 0 : w - 1;
+    const double* brow = bm + static_cast<size_t>(jn) * w;
+    for (int t = lane; t < w; t += 32) nrow[t] = brow[t];
+    __syncwarp();
+    // support bits of row j+1 in ITS scan order (one ballot per 32 pixels)
+    for (int wd = 0; wd <= words; ++wd) {  // + one zero word of padding
+      const int qn = wd * 32 + lane;
+      const bool s = qn < w && nrow[start_n + qn * dn] > 0.0;
+      const unsigned int bits = __ballot_sync(0xffffffffu, s);
+      if (lane == 0) sup[wd] = bits;
+    }
+    // diffusion weights (t.w / wsum) of row j's sources: interior sources
+    // have wsum == 1 (the quotients are exact); the two scan ends differ
+    auto coef = [&](int s, double wt) {
+      return (s == 0 || s == w - 1) ? wt / fs_wsum(s, j, w, h, pd) : wt;
+    };
+    for (int base = 0; base < w; base += 32) {
+      const int pos = base + lane;  // scan position in row j
+      const int need = min(base + 33, w);  // sources up to pos+1 swept
+      while (progress < need) {
+      }
+      fence_cta();
+      if (pos < w) {
+        // target pixel t of row j+1 receives, in the reference's arrival
+        // order, from row j's pixels t-pd (1/16), t (5/16), t+pd (3/16),
+        // i.e. scan positions pos-1, pos, pos+1
+        const int t = pd == 1 ? pos : w - 1 - pos;
+        double v = nrow[t] * scale;
+        if (pos >= 1) v += err[pos] * coef(t - pd, 1.0 / 16.0);
+        v += err[pos + 1] * coef(t, 5.0 / 16.0);
+        if (pos + 1 < w) v += err[pos + 2] * coef(t + pd, 3.0 / 16.0);
+        pre[w - pos] = v;  // row j+1 scans the other way: position w-1-pos
+      }
+    }
+    __syncwarp();
+    fence_cta();
+    if (lane == 0) {
+      progress = 0;
+      fence_cta();
+      pre_ready = jn + 1;
+    }
+    __syncwarp();
+  }
 }
 
 // dither_samples as a row decomposition that is bit-identical to the
@@ -201,14 +523,27 @@ __global__ void k_observe_finalize(StepState* st, BufState* buf) {
 
 void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
                    int* d_cells, int cap, int* d_n, double* d_mass) {
-  const size_t smem = static_cast<size_t>(2) * w * sizeof(double);
-  if (smem > 48 * 1024) {
+  const size_t rs = (static_cast<size_t>(w) + 3) & ~static_cast<size_t>(1);
+  const size_t smem_pipe = (3 * rs + w) * sizeof(double) + 8 * static_cast<size_t>((w + 31) / 32 + 1) + 16;
+  if (smem_pipe <= 200 * 1024) {
+    if (smem_pipe > 48 * 1024) {
+      cudaFuncSetAttribute(k_dither_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem_pipe));
+    }
+    k_dither_pipe<<<1, 64, smem_pipe, ctx->stream>>>(bm, w, h, budget, d_cells, cap, d_n, d_mass);
+  } else {
+    const size_t smem = static_cast<size_t>(2) * w * sizeof(double);
     cudaFuncSetAttribute(k_dither, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
+    k_dither<<<1, 32, smem, ctx->stream>>>(bm, w, h, budget, d_cells, cap, d_n, d_mass);
   }
-  k_dither<<<1, 32, smem, ctx->stream>>>(bm, w, h, budget, d_cells, cap, d_n,
-                                        d_mass);
   ctx->launches++;
+  if (getenv("GL_DEBUG_DITHER")) {
+    long long clk[4];
+    cudaStreamSynchronize(ctx->stream);
+    cudaMemcpyFromSymbol(clk, g_dither_clk, sizeof(clk));
+    fprintf(stderr, "dither clocks: total-sum %lld, sweep %lld (chain waited %lld at row starts, %lld at row ends) cycles (%d x %d)\n", clk[1], clk[2], clk[3], clk[0], w, h);
+  }
 }
 
 void launch_likelihoods(gl_context* ctx, const uint8_t* occ, const double* score,

@@ -154,6 +154,27 @@ def _doors(occ, rng, span, carve, door):
         carve(a, a + dw)
 
 
+def simple_scan(occ: np.ndarray, x: float, y: float, theta: float, beams: int = 24, max_range: float = 8.0,
+                res: float = 0.1):
+    """A noise-free full-circle scan by fixed-step ray marching (synthetic
+    bench input; the reference's exact grid traversal lives in its
+    simulator, occupancy_map.cpp:273-332)."""
+    import math
+    angles = np.array([-math.pi + b * (2.0 * math.pi / beams) for b in range(beams)])
+    ranges = np.full(beams, max_range)
+    h, w = occ.shape
+    for b, a in enumerate(angles):
+        c, s = math.cos(theta + a), math.sin(theta + a)
+        r = 0.0
+        while r < max_range:
+            i, j = int(math.floor((x + r * c) / res)), int(math.floor((y + r * s) / res))
+            if not (0 <= i < w and 0 <= j < h) or occ[j, i]:
+                ranges[b] = r
+                break
+            r += 0.25 * res
+    return angles, ranges
+
+
 def write_pgm(occ: np.ndarray) -> bytes:
     """Canonical P5 (occupancy_map.cpp:177-185): free 255, occupied 0."""
     h, w = occ.shape
