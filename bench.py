@@ -44,14 +44,18 @@ CONFIGS = {
     "c2": dict(W=1024, H=1024, C=72, workload="1024x1024x72 floor-plan, odometry+map correction, 1 B200 "
                                               "(BASELINE configs[1]); cmd_bench translation stream u=(res,0,0)"),
     "c1": dict(W=256, H=256, C=36, workload="256x256x36 floor-plan, odometry+map only (BASELINE configs[0])"),
-    "c5": dict(W=512, H=512, C=72, workload="512x512x72 floor-plan (BASELINE configs[4], one robot)"),
+    "c5r": dict(W=512, H=512, C=72, workload="512x512x72 floor-plan (BASELINE configs[4], one robot)"),
     "c4s": dict(W=2048, H=2048, C=360, workload="2048x2048x360 floor-plan (config-4 angular width, 1/4 area)"),
     "c5": dict(W=512, H=512, C=72, batch=64, workload="batch of 64 independent robots/maps at 512x512x72 "
                                                       "(BASELINE configs[4])"),
     "c4": dict(W=4096, H=4096, C=360, workload="4096x4096x360 floor-plan on ONE B200 (BASELINE configs[3]; "
                                               "2 x 48.3 GB ping-pong in HBM)"),
 }
-METRIC = "belief updates/sec (Hz) at 1024^2x72"
+METRIC = "belief updates/sec (Hz) at 1024^2x72"  # the headline (configs[1])
+
+
+def metric_for(W, H, C):
+    return f"belief updates/sec (Hz) at {W}^2x{C}" if W == H else f"belief updates/sec (Hz) at {W}x{H}x{C}"
 HBM_FALLBACK = 6650.0
 
 
@@ -227,7 +231,7 @@ def run_reference(args, cfg, world, rank):
     dt = time.perf_counter() - t0
     hz = n / dt
     line = {
-        "impl": "reference", "metric": METRIC, "value": hz, "unit": "Hz", "n_gpus": world, "steps": n,
+        "impl": "reference", "metric": metric_for(cfg["W"], cfg["H"], cfg["C"]), "value": hz, "unit": "Hz", "n_gpus": world, "steps": n,
         "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(n, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["workload"], "W": cfg["W"], "H": cfg["H"], "channels": cfg["C"],
@@ -400,7 +404,7 @@ def run_sharded(args, cfg, world, rank, local):
     if rank != 0:
         return 0
     line = {
-        "metric": METRIC, "value": value, "unit": "Hz", "n_gpus": world, "steps": args.steps,
+        "metric": metric_for(W, H, C), "value": value, "unit": "Hz", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["workload"], "W": W, "H": H, "channels": C,
@@ -493,7 +497,7 @@ def run_ours(args, cfg, world, rank, local):
     if rank != 0:
         return 0
     line = {
-        "metric": METRIC, "value": value, "unit": "Hz", "n_gpus": world, "steps": args.steps,
+        "metric": metric_for(W, H, C), "value": value, "unit": "Hz", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["workload"], "W": W, "H": H, "channels": C,
