@@ -299,6 +299,7 @@ gl_status gl_context_create(int device, gl_context** out) {
     DeviceGuard g(device);
     auto ctx = std::make_unique<gl_context>();
     ctx->device = device;
+    CK(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&ctx->ev_begin));
     CK(cudaEventCreate(&ctx->ev_end));
@@ -933,7 +934,6 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
     // (c_begin - halo + q) mod c_total), carried in the launch parameters
     if (!fused) fail(GL_E_INVALID, "sharded tensors need the fused path (separable/impulse kernels, H <= halo)");
     const int planes = t->c + 2 * t->halo;
-    need(planes <= glb::kParamChannels, "too many planes per shard for the launch-parameter motion table");
     hm.resize(2 * static_cast<size_t>(planes));
     const double dtheta = 2.0 * M_PI / t->c_total;
     for (int q = 0; q < planes; ++q) {
@@ -943,7 +943,7 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
     a.h_motion = hm.data();
     a.motion = nullptr;
     a.halo = t->halo;
-  } else if (fused && t->c <= glb::kParamChannels) {
+  } else if (fused) {
     hm.resize(2 * static_cast<size_t>(t->c));
     glb::motion_table(u, v, 0, t->c, t->theta_t, 2.0 * M_PI / t->c, t->cell, hm.data());
     a.h_motion = hm.data();

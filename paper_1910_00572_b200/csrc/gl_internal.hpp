@@ -42,6 +42,19 @@ struct DeviceBlock {  // one allocation per tensor
   StepState step;
 };
 
+// Per-channel bilinear shift record of one step (belief_tensor.cpp:87-98),
+// computed on the host in the reference's operation order: box origin
+// (floor of the motion vector), the four weights, and whether the shift is
+// integral (the exact-copy branch, :71-86). Fused launches carry the step's
+// table in their parameters.
+struct ChanRec {
+  double w00, w10, w01, w11;
+  int ox, oy;     // floor(dx), floor(dy), clamped to +-2^29
+  int integral;   // round(dx) == dx && round(dy) == dy
+  int pad;
+};
+void chan_rec(double dx, double dy, ChanRec* r);  // host_math.cpp
+
 // Angular taps (belief_tensor.hpp:82): (offset, weight) in list order.
 struct AngTaps {
   int n;
@@ -53,6 +66,7 @@ struct AngTaps {
 
 struct gl_context {
   int device = 0;
+  int sm_count = 0;  // multiprocessors of `device` (fused-step grid sizing)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   int path = GL_PATH_AUTO;

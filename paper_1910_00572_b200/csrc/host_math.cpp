@@ -128,6 +128,27 @@ void motion_table(double u, double v, int c_begin, int count, double theta_t,
   }
 }
 
+// shift_plane's per-channel constants (belief_tensor.cpp:67-98), in the
+// reference's operation order on the host (no FMA contraction).
+void chan_rec(double dx, double dy, ChanRec* r) {
+  const double fx0 = std::floor(dx);
+  const double fy0 = std::floor(dy);
+  const double ax = dx - fx0;
+  const double ay = dy - fy0;
+  r->w00 = (1.0 - ax) * (1.0 - ay);
+  r->w10 = ax * (1.0 - ay);
+  r->w01 = (1.0 - ax) * ay;
+  r->w11 = ax * ay;
+  // far-out shifts only ever read zeros; the clamp keeps the TMA box-origin
+  // arithmetic free of overflow (NaN motion -> origin 0)
+  const double lim = static_cast<double>(1 << 29);
+  auto clamp = [&](double f) { return f == f ? static_cast<int>(std::min(std::max(f, -lim), lim)) : 0; };
+  r->ox = clamp(fx0);
+  r->oy = clamp(fy0);
+  r->integral = (std::round(dx) == dx && std::round(dy) == dy) ? 1 : 0;
+  r->pad = 0;
+}
+
 // ------------------------------------------------------------------ maps
 namespace {
 

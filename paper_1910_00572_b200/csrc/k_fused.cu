@@ -27,6 +27,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <type_traits>
 
@@ -115,8 +116,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map,
 
 struct FusedParams {
   double* dst;
-  const double2* motion;  // per channel (dx, dy), cells (when C > kParamChannels)
-  int param_motion;       // 1: motion vectors are in mv[] below
   const uint8_t* occ;
   const double* inv;
   const double* inv_masked;  // inv with occupied cells set to 0.0 (FAST)
@@ -127,12 +126,16 @@ struct FusedParams {
   int out_off;               // shard: storage plane of output channel 0 (= halo)
   int defer_finalize;        // shard: leave the local max for a cross-rank all-reduce
   int tiles_x, n_tiles;
+  int k_base, k_end;         // this launch's output channels (a window of <= kParamChannels - 2H)
+  int k_chunk, n_chunks;     // output channels per warp, chunks per tile
   const BufState* src_state;
   BufState* dst_state;
   StepState* step_state;
   double sep[2 * kFusedMaxRadius + 1];
   double ang[2 * kFusedMaxHalf + 1];
-  double2 mv[kParamChannels];  // the step's motion table, carried by the launch
+  // the step's shift records (host) for the window's input planes: output
+  // channels k_base-H .. k_end-1+H (shard: storage planes from plane_off + k_base)
+  ChanRec rec[kParamChannels];
 };
 
 template <int R, int ROWS>
@@ -148,34 +151,25 @@ struct Geo {
   static constexpr int STAGE = (B_ELEMS + 15) & ~15;  // 128-B aligned stages
 };
 
-// Per-channel bilinear weights from the motion vector (belief_tensor.cpp:
-// 87-98); integral shifts copy exactly (:71-86).
+// Per-channel bilinear weights (belief_tensor.cpp:87-98) and the integral
+// flag (:71-86), from the host-computed record (glb::chan_rec, the
+// reference's operations in its order): no per-lane weight arithmetic.
 struct ChanShift {
   double w00, w10, w01, w11;
   int sx, sy;
   bool integral;
 };
 
-__device__ __forceinline__ ChanShift chan_shift(double2 mv) {
+__device__ __forceinline__ ChanShift chan_shift(const ChanRec& r) {
   ChanShift s;
-  const double fx = floor(mv.x), fy = floor(mv.y);
-  s.integral = (fx == mv.x) && (fy == mv.y);
-  const double ax = mv.x - fx, ay = mv.y - fy;
-  s.w00 = (1.0 - ax) * (1.0 - ay);
-  s.w10 = ax * (1.0 - ay);
-  s.w01 = (1.0 - ax) * ay;
-  s.w11 = ax * ay;
-  // cvt.rzi.s32.f64 saturates; far-out shifts only ever read zeros, and the
-  // integer clamp keeps the box-origin arithmetic free of overflow
-  s.sx = min(max(static_cast<int>(fx), -(1 << 29)), 1 << 29);
-  s.sy = min(max(static_cast<int>(fy), -(1 << 29)), 1 << 29);
+  s.w00 = r.w00;
+  s.w10 = r.w10;
+  s.w01 = r.w01;
+  s.w11 = r.w11;
+  s.sx = r.ox;
+  s.sy = r.oy;
+  s.integral = r.integral != 0;
   return s;
-}
-
-// integer part only (TMA box origin of a channel)
-__device__ __forceinline__ int2 chan_origin(double2 mv) {
-  return make_int2(min(max(static_cast<int>(floor(mv.x)), -(1 << 29)), 1 << 29),
-                   min(max(static_cast<int>(floor(mv.y)), -(1 << 29)), 1 << 29));
 }
 
 // One S value from the four taps: r0 = row j-sy, r1 = j-sy-1, c0 = i-sx,
@@ -241,27 +235,29 @@ template <int R, int H, int ROWS, int NS, bool FAST>
 __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
                                             const FusedParams& p, double* Bs,
                                             uint64_t* mbar, int lane, int x0,
-                                            int y0, bool active) {
+                                            int y0, int k0, int n_out,
+                                            bool active) {
   using G = Geo<R, ROWS>;
   constexpr int NG = 2 * H + 1;  // ring depth == angular taps
   const int W = p.w, Hh = p.h, C = p.c;
   const size_t plane = static_cast<size_t>(W) * Hh;
-  const int n_iter = C + 2 * H;
+  const int n_iter = n_out + 2 * H;  // this warp's output channels k0 .. k0+n_out-1
   const bool scaled = p.src_state->scaled != 0;  // pending 1/max rescale
   const double sc = p.src_state->scale;
 
-  // storage plane of iteration it. One GPU: circular channel m = it - H in
-  // [-H, C-1+H] (H < C). theta-slab shard: planes are stored with their
-  // neighbours' halo planes, so the walk is linear from plane_off.
+  // storage plane of iteration it. One GPU: circular channel m = k0 + it - H
+  // in [-H, C-1+H] (H < C). theta-slab shard: planes are stored with their
+  // neighbours' halo planes, so the walk is linear from plane_off. The shift
+  // record index is linear in both cases.
   auto chan_of = [&](int it) {
-    if (p.shard) return p.plane_off + it;
-    const int m = it - H;
+    if (p.shard) return p.plane_off + k0 + it;
+    const int m = k0 + it - H;
     return m < 0 ? m + C : (m >= C ? m - C : m);
   };
-  auto motion_of = [&](int kc) { return p.param_motion ? p.mv[kc] : p.motion[kc]; };
+  const int rec0 = k0 - p.k_base;
   auto issue = [&](int it, int stage) {
     const int kc = chan_of(it);
-    const int2 o = chan_origin(motion_of(kc));
+    const int2 o = make_int2(p.rec[rec0 + it].ox, p.rec[rec0 + it].oy);
     mbar_arrive_expect(&mbar[stage], G::B_BYTES);
     tma_load_3d(Bs + stage * G::STAGE, tmap, (x0 - R - o.x - 1) & ~1,
                 y0 - R - o.y - 1, kc, &mbar[stage]);
@@ -314,7 +310,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
     constexpr int u = decltype(Ut)::value;
     constexpr bool emit = decltype(Et)::value;
     const int stage = it % NS;
-    const ChanShift cs = chan_shift(motion_of(chan_of(it)));
+    const ChanShift cs = chan_shift(p.rec[rec0 + it]);
     double* stage_ptr = Bs + stage * G::STAGE;
     mbar_wait(&mbar[stage], static_cast<uint32_t>((it / NS) & 1));
     if (scaled) {
@@ -324,7 +320,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
       __syncwarp();
     }
     const double* Bb = stage_ptr + ((x0 - R - cs.sx - 1) & 1) + lane;
-    double* orow = out_tile + plane * static_cast<size_t>(p.out_off + (emit ? it - 2 * H : 0));  // += W per row
+    double* orow = out_tile + plane * static_cast<size_t>(p.out_off + k0 + (emit ? it - 2 * H : 0));  // += W per row
 
     double lo_c0 = Bb[1], lo_c1 = Bb[0];
     double rw[2 * R + 1];  // rolling window of row-pass results
@@ -423,12 +419,20 @@ __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_
   // Surplus warps of the last CTA redo the last tile with stores disabled,
   // so every warp runs the same control flow (the shuffles then compile to
   // plain SHFL instead of the divergence-safe collective sequence).
-  const int tile_raw = blockIdx.x * NWARP + warp;
+  // Work item = (channel chunk, tile). A CTA's warps share one chunk, so the
+  // chunk (and every shift-record index) derives from blockIdx alone: the
+  // compiler keeps the records in uniform registers. Consecutive warps take
+  // neighbouring tiles, so their halo rows meet in L2.
+  const int cta_per_chunk = (p.n_tiles + NWARP - 1) / NWARP;
+  const int chunk = blockIdx.x / cta_per_chunk;
+  const int tile_raw = (blockIdx.x - chunk * cta_per_chunk) * NWARP + warp;
   const bool active = tile_raw < p.n_tiles;
   const int tile = active ? tile_raw : p.n_tiles - 1;
   const int x0 = (tile % p.tiles_x) * G::OW;
   const int y0 = (tile / p.tiles_x) * ROWS;
-  double vmax = warp_tile<R, H, ROWS, NS, FAST>(&tmap, p, Bs, mbar, lane, x0, y0, active);
+  const int k0 = p.k_base + chunk * p.k_chunk;
+  const int n_out = min(p.k_chunk, p.k_end - k0);
+  double vmax = warp_tile<R, H, ROWS, NS, FAST>(&tmap, p, Bs, mbar, lane, x0, y0, k0, n_out, active);
 
   // global max -> the last CTA finalises status and the pending rescale
 #pragma unroll
@@ -481,6 +485,7 @@ constexpr size_t smem_bytes() {
 
 template <int R, int H, bool FAST>
 void launch_rhf(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp) {
+  const int n_win = fp.k_end - fp.k_base;
   constexpr int ROWS = rows_for<H>();
   using G = Geo<R, ROWS>;
   constexpr size_t smem = smem_bytes<R, ROWS>();
@@ -494,7 +499,19 @@ void launch_rhf(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp) {
   }
   fp.tiles_x = (fp.w + G::OW - 1) / G::OW;
   fp.n_tiles = fp.tiles_x * ((fp.h + ROWS - 1) / ROWS);
-  const int blocks = (fp.n_tiles + kNWARP - 1) / kNWARP;
+  // Small grids leave SMs idle with one warp per tile: split the channels
+  // into chunks (each recomputes its 2H angular neighbours) until about two
+  // waves of warps exist, keeping the recompute below 50%.
+  fp.n_chunks = 1;
+  const long waves2 = 2L * 16 * (ctx->sm_count > 0 ? ctx->sm_count : 148);
+  if (fp.n_tiles < waves2) {
+    const int want = static_cast<int>((waves2 + fp.n_tiles - 1) / fp.n_tiles);
+    const int max_chunks = n_win / (H == 0 ? 2 : 4 * H);
+    fp.n_chunks = std::max(1, std::min(want, max_chunks));
+  }
+  fp.k_chunk = (n_win + fp.n_chunks - 1) / fp.n_chunks;
+  fp.n_chunks = (n_win + fp.k_chunk - 1) / fp.k_chunk;
+  const int blocks = ((fp.n_tiles + kNWARP - 1) / kNWARP) * fp.n_chunks;
   kern<<<blocks, 32 * kNWARP, smem, ctx->stream>>>(*tmap, fp);
   ctx->launches++;
 }
@@ -546,14 +563,10 @@ void fused_box(int r, int H, int* bw, int* bh) {
 void launch_fused_step(gl_context* ctx, const StepArgs& a,
                        const CUtensorMap* tmap, const double* sep, int r,
                        const AngTaps& ang, bool fast) {
-  FusedParams fp{};
+  static thread_local FusedParams fp;  // ~19 KB: keep it off the stack
+  fp = FusedParams{};
+  const int H = ang.n / 2;
   fp.dst = a.dst;
-  fp.motion = a.motion;
-  fp.param_motion = (a.c <= kParamChannels && a.h_motion != nullptr) ? 1 : 0;
-  if (fp.param_motion) {
-    const int planes = a.c + 2 * (a.halo > 0 ? a.halo : 0);  // one vector per storage plane
-    for (int k = 0; k < planes; ++k) fp.mv[k] = make_double2(a.h_motion[2 * k], a.h_motion[2 * k + 1]);
-  }
   fp.occ = a.occ;
   fp.inv = a.inv;
   fp.inv_masked = a.inv_masked;
@@ -562,19 +575,40 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
   fp.h = a.h;
   fp.c = a.c;
   fp.shard = a.halo >= 0 ? 1 : 0;
-  fp.plane_off = a.halo - ang.n / 2;
+  fp.plane_off = a.halo - H;
   fp.out_off = a.halo >= 0 ? a.halo : 0;
-  fp.defer_finalize = a.halo >= 0 ? 1 : 0;
   fp.src_state = a.src_state;
   fp.dst_state = a.dst_state;
   fp.step_state = a.step_state;
   for (int t = 0; t < 2 * r + 1; ++t) fp.sep[t] = sep[t];
   for (int t = 0; t < ang.n; ++t) fp.ang[t] = ang.w[t];
-  const int H = ang.n / 2;
-  switch (r) {
-    case 0: launch_r<0>(ctx, tmap, fp, H, fast); break;
-    case 1: launch_r<1>(ctx, tmap, fp, H, fast); break;
-    default: launch_r<2>(ctx, tmap, fp, H, fast); break;
+  // The shift records ride in the launch parameters; more than
+  // kParamChannels - 2H output channels take several launches over channel
+  // windows. Only the last one finalises the max (a shard never does: its
+  // max goes to the cross-rank all-reduce first).
+  const int win = kParamChannels - 2 * H;
+  for (int kb = 0; kb < a.c; kb += win) {
+    const int ke = std::min(a.c, kb + win);
+    fp.k_base = kb;
+    fp.k_end = ke;
+    fp.defer_finalize = (fp.shard || ke < a.c) ? 1 : 0;
+    for (int q = 0; q < ke - kb + 2 * H; ++q) {
+      // h_motion: one (dx, dy) per channel (whole tensor) or per storage
+      // plane (shard: plane q <-> channel c_begin - halo + q)
+      int src;
+      if (fp.shard) {
+        src = fp.plane_off + kb + q;
+      } else {
+        src = kb - H + q;
+        src = src < 0 ? src + a.c : (src >= a.c ? src - a.c : src);
+      }
+      chan_rec(a.h_motion[2 * src], a.h_motion[2 * src + 1], &fp.rec[q]);
+    }
+    switch (r) {
+      case 0: launch_r<0>(ctx, tmap, fp, H, fast); break;
+      case 1: launch_r<1>(ctx, tmap, fp, H, fast); break;
+      default: launch_r<2>(ctx, tmap, fp, H, fast); break;
+    }
   }
 }
 

@@ -213,3 +213,16 @@ def test_trace_256x256x36_200_steps(ctx, port, ref):
         assert t.hash() == g.tensor_hash_host(B), f"hash mismatch at step {s}"
     assert t.theta_t() == th
     assert_bitwise(t.values(), B, "final")
+
+
+def test_channel_windows_bit_exact(ctx, port):
+    """Theta = 400 (h = 3): the fused launch carries at most kParamChannels
+    shift records, so the step runs as two channel-window launches; the max
+    (and the rescale branch) is finalised once, by the last window. Small
+    grids also split every tile's channels into chunks (each recomputing its
+    2H angular neighbours) — every case here runs chunked."""
+    occ = make_floorplan(64, 48, seed=21)
+    motions = [(0.1, 0.0, 0.0), (0.07, -0.03, 0.05), (0.0, 0.0, 0.02)]
+    _run_pair(ctx, port, occ, 400, (0.03, 0.03, 0.012), motions, GL_PATH_FUSED)
+    B0 = random_tensor(occ, 400, seed=4) * 1e-9  # max < 1e-6: deferred rescale
+    _run_pair(ctx, port, occ, 400, (0.03, 0.03, 0.012), motions, GL_PATH_FUSED, B0=B0)
