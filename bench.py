@@ -372,7 +372,7 @@ def run_sharded(args, cfg, world, rank, local):
     ks = g.build_kernels(g.MotionNoise(), C, m.resolution(), 2.0 * math.pi / C)
     act = g.make_activation(m, ks, C, ctx)
     halo = max(1, len(ks.angular) // 2)
-    shard = ThetaShard(m, C, halo, rank, world, ctx)
+    shard = ThetaShard(m, C, halo, rank, world, ctx, exchange=args.exchange)
     u = g.OdometryDelta(m.resolution(), 0.0, 0.0)
     for _ in range(args.warmup):
         shard.step(u, ks, act)
@@ -409,7 +409,10 @@ def run_sharded(args, cfg, world, rank, local):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["workload"], "W": W, "H": H, "channels": C,
                    "parallelism": f"theta-slab sharding over {world} GPU(s), {n_local} channels + 2x{halo} "
-                                  "halo planes per GPU; NCCL all-reduce (8 B) + halo send/recv per step",
+                                  "halo planes per GPU; NCCL all-reduce (8 B) per step; halo exchange "
+                                  + ("fused into the step kernel (edge planes stored into the neighbours' "
+                                     "halo planes over CUDA IPC / NVLink P2P)" if args.exchange == "peer"
+                                     else "by NCCL send/recv after the step"),
                    "l2": "the per-GPU slab exceeds L2"},
         "e2e": None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -530,6 +533,8 @@ def main():
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--ref-budget-s", type=float, default=90.0)
     ap.add_argument("--no-extras", action="store_true", help="skip the trace-mix / LIDAR-cycle extras")
+    ap.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
+                    help="--shard halo exchange: fused peer-memory stores (default) or NCCL send/recv")
     ap.add_argument("--shard", action="store_true",
                     help="theta-shard ONE belief across the ranks (strong scaling; e.g. --config c4)")
     args = ap.parse_args()

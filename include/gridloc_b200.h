@@ -196,8 +196,12 @@ gl_status gl_tensor_status(gl_context* ctx, gl_tensor* t);
  * argmax, belief_map) are the interior ones. One sharded step is:
  *   gl_step_async                          (fused kernel, local max only)
  *   all-reduce MAX of *gl_tensor_max_ptr   (uint64 bits of a double >= 0)
- *   gl_shard_finalize                      (status + pending 1/max rescale)
- *   halo exchange of storage planes        (gl_tensor_plane_ptr; NCCL)
+ *   gl_shard_finalize                      (status + pending 1/max rescale;
+ *                                           a no-op for a shard holding
+ *                                           every channel: it finalises in
+ *                                           the step kernel)
+ *   halo exchange of storage planes        (gl_tensor_plane_ptr; NCCL) —
+ *                                           or none: gl_shard_set_peers
  * Sharding does not change any per-element operation: results are bitwise
  * those of the unsharded tensor. */
 gl_status gl_shard_init_uniform(gl_context* ctx, const gl_map* map, int c_total,
@@ -210,9 +214,43 @@ gl_status gl_tensor_plane_ptr(gl_context* ctx, gl_tensor* t, int q,
 gl_status gl_tensor_max_ptr(gl_context* ctx, gl_tensor* t,
                             unsigned long long** dptr);
 gl_status gl_shard_finalize(gl_context* ctx, gl_tensor* t);
+/* Fused halo exchange over peer memory (NVLink P2P; no separate exchange
+ * step): with peers set, the shard's step also stores its first `halo`
+ * output planes into the left neighbour's upper halo planes (lo_b = that
+ * neighbour's buffer-b storage plane halo + its channel count) and its last
+ * `halo` output planes into the right neighbour's lower halo (hi_b = the
+ * neighbour's buffer-b storage plane 0). Pointers come from
+ * gl_tensor_buffer_ptr in this process (same device or peer-enabled
+ * devices) or gl_ipc_open across processes. The cross-rank max all-reduce
+ * that follows every step orders these stores before the neighbour's next
+ * step. All NULL: no peer stores (exchange planes yourself). */
+gl_status gl_shard_set_peers(gl_context* ctx, gl_tensor* t, void* lo0,
+                             void* lo1, void* hi0, void* hi1);
+/* storage plane q of ping-pong buffer buf (0/1); the current one is
+ * gl_tensor_current_buffer (all shards of one belief flip together) */
+gl_status gl_tensor_buffer_ptr(gl_context* ctx, gl_tensor* t, int buf, int q,
+                               double** dptr);
+gl_status gl_tensor_current_buffer(const gl_tensor* t, int* buf);
+/* CUDA IPC of a tensor buffer (64-byte cudaIpcMemHandle_t) for peer planes
+ * across processes (one process per GPU) */
+gl_status gl_ipc_get_handle(gl_context* ctx, gl_tensor* t, int buf,
+                            void* handle64);
+gl_status gl_ipc_open(gl_context* ctx, const void* handle64, void** dptr);
+gl_status gl_ipc_close(gl_context* ctx, void* dptr);
 /* device-to-device plane copy (single-device halo exchange) */
 gl_status gl_tensor_copy_planes(gl_context* ctx, gl_tensor* dst, int dst_q,
                                 gl_tensor* src, int src_q, int count);
+
+/* write_belief_snapshot / read_belief_snapshot (belief_tensor.hpp:144-148,
+ * belief_tensor.cpp:543-587): BLF1 = "BLF1", uint32 W/H/Theta, float32
+ * theta_t, W*H*Theta float32 values [k][j][i], little-endian (lossy for the
+ * FP64 belief, as in the reference). I/O failures -> GL_E_RUNTIME with the
+ * reference's messages; bad dimensions -> GL_E_INVALID. */
+gl_status gl_write_belief_snapshot(gl_context* ctx, gl_tensor* t,
+                                   const char* path);
+gl_status gl_read_belief_snapshot(gl_context* ctx, const char* path,
+                                  double cell_size, double origin_x,
+                                  double origin_y, gl_tensor** out);
 
 /* apply_motion (belief_tensor.cpp:340-352): shift only, no mask/diffusion. */
 gl_status gl_apply_motion(gl_context* ctx, gl_tensor* t, double u, double v,

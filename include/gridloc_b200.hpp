@@ -433,6 +433,17 @@ inline PoseEstimate argmax_state(const BeliefTensor& t) {  // :512-541
   return p;
 }
 
+// belief_tensor.hpp:144-148: BLF1 snapshot (float32 payload, lossy)
+inline void write_belief_snapshot(const BeliefTensor& t, const std::string& path) {
+  check(gl_write_belief_snapshot(t.pool().get(), t.get(), path.c_str()));
+}
+inline BeliefTensor read_belief_snapshot(const std::string& path, double cell_size, double origin_x,
+                                         double origin_y, ThreadPool& pool = ThreadPool::default_pool()) {
+  gl_tensor* t = nullptr;
+  check(gl_read_belief_snapshot(pool.get(), path.c_str(), cell_size, origin_x, origin_y, &t));
+  return BeliefTensor(t, pool);
+}
+
 inline SampleSet dither_samples(const Grid2d& bm, int budget,
                                 ThreadPool& pool = ThreadPool::default_pool()) {  // observation.cpp:11-71
   const int cap = static_cast<int>(std::min<size_t>(bm.size(), 4 * static_cast<size_t>(std::max(budget, 1)) + 64));

@@ -295,6 +295,9 @@ class Ref:
         L.ref_tensor_free.argtypes = [_vp]
         L.ref_tensor_set.argtypes = [_vp, _dp, C.c_double]
         L.ref_tensor_get.argtypes = [_vp, _dp, _dp]
+        L.ref_write_snapshot.argtypes = [_vp, C.c_char_p]
+        L.ref_read_snapshot.argtypes = [C.c_char_p, C.c_double, C.c_double, C.c_double, C.POINTER(_vp)]
+        L.ref_tensor_dims.argtypes = [_vp, _ip, _ip, _ip]
         L.ref_scratch_new.restype = _vp
         L.ref_scratch_free.argtypes = [_vp]
         L.ref_scratch_times.argtypes = [_vp, _dp]
@@ -473,6 +476,36 @@ class RefEngine:
             L.ref_pool_free(self.pool)
         except Exception:
             pass
+
+
+def ref_write_snapshot(ref: Ref, values, theta_t: float, path: str, cell=0.1):
+    """The reference's write_belief_snapshot of a (C, H, W) FP64 array."""
+    c, h, w = values.shape
+    t = _vp()
+    assert ref.lib.ref_tensor_new(w, h, c, cell, 0.0, 0.0, C.byref(t)) == 0
+    try:
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        ref.lib.ref_tensor_set(t, v.ctypes.data_as(_dp), theta_t)
+        if ref.lib.ref_write_snapshot(t, os.fsencode(path)) != 0:
+            raise RuntimeError(ref.lib.ref_last_error().decode())
+    finally:
+        ref.lib.ref_tensor_free(t)
+
+
+def ref_read_snapshot(ref: Ref, path: str, cell=0.1):
+    """The reference's read_belief_snapshot -> ((C, H, W) FP64 values, theta_t)."""
+    t = _vp()
+    if ref.lib.ref_read_snapshot(os.fsencode(path), cell, 0.0, 0.0, C.byref(t)) != 0:
+        raise RuntimeError(ref.lib.ref_last_error().decode())
+    try:
+        w, h, c = C.c_int(), C.c_int(), C.c_int()
+        ref.lib.ref_tensor_dims(t, C.byref(w), C.byref(h), C.byref(c))
+        out = np.empty((c.value, h.value, w.value))
+        th = C.c_double()
+        ref.lib.ref_tensor_get(t, out.ctypes.data_as(_dp), C.byref(th))
+        return out, th.value
+    finally:
+        ref.lib.ref_tensor_free(t)
 
 
 def ref_dither(ref: Ref, bm, budget):

@@ -208,6 +208,21 @@ void ref_tensor_get(void* t, double* vals, double* theta_t) {
   if (theta_t) *theta_t = bt->theta_t();
 }
 
+// BLF1 snapshots through the reference's own writer / reader
+int ref_write_snapshot(void* t, const char* path) {
+  return guard([&] { write_belief_snapshot(*static_cast<BeliefTensor*>(t), path); });
+}
+int ref_read_snapshot(const char* path, double cell, double ox, double oy, void** out) {
+  return guard([&] { *out = new BeliefTensor(read_belief_snapshot(path, cell, ox, oy)); });
+}
+int ref_tensor_dims(void* t, int* w, int* h, int* c) {
+  auto* bt = static_cast<BeliefTensor*>(t);
+  *w = bt->width();
+  *h = bt->height();
+  *c = bt->channels();
+  return 0;
+}
+
 // Same order-independent hash as gl_tensor_hash: sum of splitmix64(bits_p +
 // p * golden) over the tensor.
 uint64_t ref_tensor_hash(void* t) {

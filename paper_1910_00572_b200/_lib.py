@@ -72,6 +72,14 @@ SIGNATURES = {
     "gl_tensor_max_ptr": [_vp, _vp, C.POINTER(C.POINTER(C.c_uint64))],
     "gl_shard_finalize": [_vp, _vp],
     "gl_tensor_copy_planes": [_vp, _vp, C.c_int, _vp, C.c_int, C.c_int],
+    "gl_write_belief_snapshot": [_vp, _vp, C.c_char_p],
+    "gl_read_belief_snapshot": [_vp, C.c_char_p, C.c_double, C.c_double, C.c_double, _pvp],
+    "gl_shard_set_peers": [_vp, _vp, _vp, _vp, _vp, _vp],
+    "gl_tensor_buffer_ptr": [_vp, _vp, C.c_int, C.c_int, C.POINTER(_dp)],
+    "gl_tensor_current_buffer": [_vp, _ip],
+    "gl_ipc_get_handle": [_vp, _vp, C.c_int, _vp],
+    "gl_ipc_open": [_vp, _vp, _pvp],
+    "gl_ipc_close": [_vp, _vp],
     "gl_context_launch_count": [_vp, C.POINTER(C.c_uint64)],
     "gl_context_stream": [_vp, _pvp],
     "gl_context_time_steps": [_vp, C.c_int],

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <fstream>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -738,6 +739,76 @@ gl_status gl_init_uniform(gl_context* ctx, const gl_map* map, int channels,
   });
 }
 
+// ------------------------------------------------------------ snapshots
+// BLF1 (belief_tensor.hpp:144-148, belief_tensor.cpp:543-587): "BLF1",
+// uint32 W/H/Theta, float32 theta_t, W*H*Theta float32 values [k][j][i],
+// little-endian. The float32 conversion runs on the device, so half the
+// bytes cross PCIe.
+gl_status gl_write_belief_snapshot(gl_context* ctx, gl_tensor* t, const char* path) {
+  return guard([&] {
+    need(ctx && t && path, "null argument");
+    need(t->halo < 0, "snapshots are written from whole (unsharded) tensors");
+    DeviceGuard g(ctx->device);
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw std::runtime_error(std::string("cannot open for writing: ") + path);
+    materialize(ctx, t);
+    const size_t n = elems_of(t);
+    float* d = static_cast<float*>(ensure_misc(ctx, n * sizeof(float)));
+    glb::launch_to_f32(ctx, interior(t), d, n);
+    std::vector<float> buf(n);
+    CK(cudaMemcpyAsync(buf.data(), d, n * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const char magic[4] = {'B', 'L', 'F', '1'};
+    out.write(magic, 4);
+    const uint32_t dims[3] = {static_cast<uint32_t>(t->w), static_cast<uint32_t>(t->h),
+                              static_cast<uint32_t>(t->c)};
+    out.write(reinterpret_cast<const char*>(dims), sizeof(dims));
+    const float theta = static_cast<float>(t->theta_t);
+    out.write(reinterpret_cast<const char*>(&theta), sizeof(theta));
+    out.write(reinterpret_cast<const char*>(buf.data()), static_cast<std::streamsize>(n * sizeof(float)));
+    if (!out) throw std::runtime_error(std::string("write failed: ") + path);
+  });
+}
+
+gl_status gl_read_belief_snapshot(gl_context* ctx, const char* path, double cell_size,
+                                  double origin_x, double origin_y, gl_tensor** out_t) {
+  return guard([&] {
+    need(ctx && path && out_t, "null argument");
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error(std::string("cannot open snapshot: ") + path);
+    char magic[4];
+    in.read(magic, 4);
+    if (!in || std::memcmp(magic, "BLF1", 4) != 0) {
+      throw std::runtime_error(std::string("bad belief snapshot magic in ") + path);
+    }
+    uint32_t dims[3];
+    float theta;
+    in.read(reinterpret_cast<char*>(dims), sizeof(dims));
+    in.read(reinterpret_cast<char*>(&theta), sizeof(theta));
+    if (!in) throw std::runtime_error(std::string("truncated belief snapshot ") + path);
+    DeviceGuard g(ctx->device);
+    std::unique_ptr<gl_tensor, gl_status (*)(gl_tensor*)> t(
+        new_tensor(ctx, static_cast<int>(dims[0]), static_cast<int>(dims[1]), static_cast<int>(dims[2]),
+                   cell_size, origin_x, origin_y),
+        gl_tensor_destroy);
+    t->theta_t = theta;
+    const size_t n = elems_of(t.get());
+    std::vector<float> buf(n);
+    in.read(reinterpret_cast<char*>(buf.data()), static_cast<std::streamsize>(n * sizeof(float)));
+    if (!in) throw std::runtime_error(std::string("truncated belief snapshot ") + path);
+    float* d = static_cast<float*>(ensure_misc(ctx, n * sizeof(float)));
+    CK(cudaMemcpyAsync(d, buf.data(), n * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+    glb::launch_from_f32(ctx, d, interior(t.get()), n);
+    auto* flag = static_cast<unsigned int*>(ensure_misc(ctx, 64));  // the payload is consumed (stream order)
+    glb::launch_scan_unclean(ctx, interior(t.get()), n, flag);
+    unsigned int unclean = 0;
+    CK(cudaMemcpyAsync(&unclean, flag, sizeof(unclean), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    t->clean[t->cur] = unclean == 0;
+    *out_t = t.release();
+  });
+}
+
 gl_status gl_tensor_destroy(gl_tensor* t) {
   return guard([&] {
     if (!t) return;
@@ -943,6 +1014,9 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
     a.h_motion = hm.data();
     a.motion = nullptr;
     a.halo = t->halo;
+    a.full_shard = t->c == t->c_total;
+    a.peer_lo = t->peer_lo[dst];
+    a.peer_hi = t->peer_hi[dst];
   } else if (fused) {
     hm.resize(2 * static_cast<size_t>(t->c));
     glb::motion_table(u, v, 0, t->c, t->theta_t, 2.0 * M_PI / t->c, t->cell, hm.data());
@@ -1061,12 +1135,73 @@ gl_status gl_shard_finalize(gl_context* ctx, gl_tensor* t) {
   return guard([&] {
     need(ctx && t, "null argument");
     need(t->halo >= 0, "not a sharded tensor");
+    if (t->c == t->c_total) return;  // one rank: the step kernel finalised already
     DeviceGuard g(ctx->device);
     glb::StepArgs a{};
     a.step_state = &t->d_block->step;
     a.dst_state = &t->d_block->buf[t->cur];  // the step already flipped cur
     glb::launch_step_finalize(ctx, a);
     CK(cudaGetLastError());
+  });
+}
+
+gl_status gl_shard_set_peers(gl_context* ctx, gl_tensor* t, void* lo0, void* lo1, void* hi0,
+                             void* hi1) {
+  return guard([&] {
+    need(ctx && t, "null argument");
+    need(t->halo >= 0, "not a sharded tensor");
+    need((lo0 == nullptr) == (lo1 == nullptr) && (hi0 == nullptr) == (hi1 == nullptr),
+         "peer planes must be given for both buffers");
+    t->peer_lo[0] = static_cast<double*>(lo0);
+    t->peer_lo[1] = static_cast<double*>(lo1);
+    t->peer_hi[0] = static_cast<double*>(hi0);
+    t->peer_hi[1] = static_cast<double*>(hi1);
+  });
+}
+
+gl_status gl_tensor_buffer_ptr(gl_context* ctx, gl_tensor* t, int buf, int q, double** dptr) {
+  return guard([&] {
+    need(ctx && t && dptr, "null argument");
+    need(buf == 0 || buf == 1, "buffer index must be 0 or 1");
+    need(q >= 0 && q < t->c + 2 * halo_of(t), "storage plane out of range");
+    *dptr = t->d_buf[buf] + plane_of(t) * q;
+  });
+}
+
+gl_status gl_tensor_current_buffer(const gl_tensor* t, int* buf) {
+  return guard([&] {
+    need(t && buf, "null argument");
+    *buf = t->cur;
+  });
+}
+
+gl_status gl_ipc_get_handle(gl_context* ctx, gl_tensor* t, int buf, void* handle64) {
+  return guard([&] {
+    need(ctx && t && handle64, "null argument");
+    need(buf == 0 || buf == 1, "buffer index must be 0 or 1");
+    DeviceGuard g(ctx->device);
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, t->d_buf[buf]));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle64, &h, sizeof(h));
+  });
+}
+
+gl_status gl_ipc_open(gl_context* ctx, const void* handle64, void** dptr) {
+  return guard([&] {
+    need(ctx && handle64 && dptr, "null argument");
+    DeviceGuard g(ctx->device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    CK(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+gl_status gl_ipc_close(gl_context* ctx, void* dptr) {
+  return guard([&] {
+    need(ctx && dptr, "null argument");
+    DeviceGuard g(ctx->device);
+    CK(cudaIpcCloseMemHandle(dptr));
   });
 }
 

@@ -161,6 +161,9 @@ struct gl_tensor {
   int device = 0;
   CUtensorMap tmap[2];  // 3-D TMA descriptors over d_buf[0/1]
   bool tmap_ok = false;
+  // shard peer planes per destination buffer (gl_shard_set_peers)
+  double* peer_lo[2] = {nullptr, nullptr};
+  double* peer_hi[2] = {nullptr, nullptr};
 };
 
 // ---------------------------------------------------------------- launchers
@@ -185,6 +188,11 @@ struct StepArgs {
   int inv_per_channel;     // 0: one plane for all k
   int w, h, c;             // c = output channels (a shard's interior planes)
   int halo = -1;           // theta-slab shard: halo planes per side; -1 = whole tensor
+  bool full_shard = false; // the shard holds all channels (one rank): no cross-rank max
+  // theta-slab shard with peer planes: the step also stores its first / last
+  // `halo` output planes into the neighbours' halo planes (peer memory)
+  double* peer_lo = nullptr;  // left neighbour's plane for my output channel 0
+  double* peer_hi = nullptr;  // right neighbour's plane for my channel c - halo
 };
 
 // k_generic.cu
@@ -201,6 +209,8 @@ void launch_step_finalize(gl_context* ctx, const StepArgs& a);
 void launch_apply_scale(gl_context* ctx, double* buf, size_t n,
                         BufState* state);
 void launch_fill(gl_context* ctx, double* buf, size_t n, double v);
+void launch_to_f32(gl_context* ctx, const double* in, float* out, size_t n);
+void launch_from_f32(gl_context* ctx, const float* in, double* out, size_t n);
 void launch_init_uniform(gl_context* ctx, double* buf, const uint8_t* occ,
                          int w, int h, int c);
 void launch_make_activation(gl_context* ctx, const uint8_t* occ, int w, int h,

@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "gl_internal.hpp"
@@ -41,6 +42,9 @@
 #endif
 #ifndef GL_FUSED_INVREG_ROWS
 #define GL_FUSED_INVREG_ROWS 8  // tiles up to this height keep inv in registers
+#endif
+#ifndef GL_FUSED_STCS
+#define GL_FUSED_STCS 1         // 1: output stores with the evict-first (.cs) hint
 #endif
 #ifndef GL_FUSED_ROWS_H3
 #define GL_FUSED_ROWS_H3 4      // tile rows for H >= 2 (Theta = 360: H = 3)
@@ -125,6 +129,9 @@ struct FusedParams {
   int plane_off;             // shard: storage plane of iteration 0 (= halo - H)
   int out_off;               // shard: storage plane of output channel 0 (= halo)
   int defer_finalize;        // shard: leave the local max for a cross-rank all-reduce
+  double* peer_lo;           // shard: also store output channels [0, n_edge) here (peer memory)
+  double* peer_hi;           //        and channels [c - n_edge, c) here
+  int n_edge;
   int tiles_x, n_tiles;
   int k_base, k_end;         // this launch's output channels (a window of <= kParamChannels - 2H)
   int k_chunk, n_chunks;     // output channels per warp, chunks per tile
@@ -231,7 +238,7 @@ __device__ __forceinline__ double row_pass(const FusedParams& p, double s) {
   return dot_seq<2 * R + 1, FAST>(p.sep, nb);
 }
 
-template <int R, int H, int ROWS, int NS, bool FAST>
+template <int R, int H, int ROWS, int NS, bool FAST, bool PEER>
 __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
                                             const FusedParams& p, double* Bs,
                                             uint64_t* mbar, int lane, int x0,
@@ -321,6 +328,25 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
     }
     const double* Bb = stage_ptr + ((x0 - R - cs.sx - 1) & 1) + lane;
     double* orow = out_tile + plane * static_cast<size_t>(p.out_off + k0 + (emit ? it - 2 * H : 0));  // += W per row
+    // PEER: shard edge planes also go to the neighbour's halo planes (one
+    // more store per row, over NVLink): the halo exchange is fused into the
+    // step. Non-edge channels aim the second store at their own output, so
+    // the row loop stays branch-free.
+    double* prow = orow;
+    bool pe = false;  // channel-uniform: this output plane is an edge plane
+    if constexpr (PEER) {
+      if (emit) {
+        const int k = k0 + it - 2 * H;
+        const size_t toff = static_cast<size_t>(out_tile - p.dst);
+        if (p.peer_lo != nullptr && k < p.n_edge) {
+          prow = p.peer_lo + plane * static_cast<size_t>(k) + toff;
+          pe = true;
+        } else if (p.peer_hi != nullptr && k >= p.c - p.n_edge) {
+          prow = p.peer_hi + plane * static_cast<size_t>(k - (p.c - p.n_edge)) + toff;
+          pe = true;
+        }
+      }
+    }
 
     double lo_c0 = Bb[1], lo_c1 = Bb[0];
     double rw[2 * R + 1];  // rolling window of row-pass results
@@ -368,8 +394,17 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
           // std::max from 0.0 over free cells (belief_tensor.cpp:464-471);
           // masked cells contribute +0.0, which never raises the max
           vmax = dmax_ref(vmax, o);
-          if ((store_ok >> r) & 1u) *orow = o;
+          const bool ok = (store_ok >> r) & 1u;
+#if GL_FUSED_STCS
+          if (ok) __stcs(orow, o);  // streaming: the output is not re-read this step
+#else
+          if (ok) *orow = o;
+#endif
+          if constexpr (PEER) {
+            if (ok & pe) *prow = o;  // one predicated store, no branch in the row loop
+          }
           orow += W;
+          if constexpr (PEER) prow += W;
         }
       }
     }
@@ -395,7 +430,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
   return vmax;
 }
 
-template <int R, int H, int ROWS, int NS, int NWARP, bool FAST>
+template <int R, int H, int ROWS, int NS, int NWARP, bool FAST, bool PEER>
 __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_MINB_H3)
     k_fused_step(const __grid_constant__ CUtensorMap tmap,
                  const FusedParams p) {
@@ -432,12 +467,15 @@ __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_
   const int y0 = (tile / p.tiles_x) * ROWS;
   const int k0 = p.k_base + chunk * p.k_chunk;
   const int n_out = min(p.k_chunk, p.k_end - k0);
-  double vmax = warp_tile<R, H, ROWS, NS, FAST>(&tmap, p, Bs, mbar, lane, x0, y0, k0, n_out, active);
+  double vmax = warp_tile<R, H, ROWS, NS, FAST, PEER>(&tmap, p, Bs, mbar, lane, x0, y0, k0, n_out, active);
 
   // global max -> the last CTA finalises status and the pending rescale
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) vmax = dmax_ref(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
   if (lane == 0) wmax[warp] = vmax;
+  // peer-plane stores must be visible to the neighbour's next step (which
+  // starts after the cross-rank max all-reduce that follows this kernel)
+  if constexpr (PEER) __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
     double bm = 0.0;
@@ -483,13 +521,13 @@ constexpr size_t smem_bytes() {
   return 128 + static_cast<size_t>(kNWARP) * kNS * G::STAGE * 8 + kNWARP * kNS * 8 + kNWARP * 8;
 }
 
-template <int R, int H, bool FAST>
+template <int R, int H, bool FAST, bool PEER>
 void launch_rhf(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp) {
   const int n_win = fp.k_end - fp.k_base;
   constexpr int ROWS = rows_for<H>();
   using G = Geo<R, ROWS>;
   constexpr size_t smem = smem_bytes<R, ROWS>();
-  auto kern = k_fused_step<R, H, ROWS, kNS, kNWARP, FAST>;
+  auto kern = k_fused_step<R, H, ROWS, kNS, kNWARP, FAST, PEER>;
   static uint64_t configured = 0;  // bit per device: the attribute is per device
   const uint64_t bit = 1ull << (ctx->device & 63);
   if (!(configured & bit)) {
@@ -500,15 +538,22 @@ void launch_rhf(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp) {
   fp.tiles_x = (fp.w + G::OW - 1) / G::OW;
   fp.n_tiles = fp.tiles_x * ((fp.h + ROWS - 1) / ROWS);
   // Small grids leave SMs idle with one warp per tile: split the channels
-  // into chunks (each recomputes its 2H angular neighbours) until about two
-  // waves of warps exist, keeping the recompute below 50%.
+  // into chunks (each recomputes its 2H angular neighbours) until one full
+  // wave of resident warps (16 per SM) exists, keeping the recompute below
+  // 50%. Measured at 1024^2 x 72 (4480 tiles): 1 chunk 0.265 ms, 2 chunks
+  // 0.274 ms — chunking only pays when the tiles cannot fill the GPU.
   fp.n_chunks = 1;
-  const long waves2 = 2L * 16 * (ctx->sm_count > 0 ? ctx->sm_count : 148);
-  if (fp.n_tiles < waves2) {
-    const int want = static_cast<int>((waves2 + fp.n_tiles - 1) / fp.n_tiles);
+  const long wave = 16L * (ctx->sm_count > 0 ? ctx->sm_count : 148);
+  if (fp.n_tiles < wave) {
+    const int want = static_cast<int>((wave + fp.n_tiles - 1) / fp.n_tiles);
     const int max_chunks = n_win / (H == 0 ? 2 : 4 * H);
     fp.n_chunks = std::max(1, std::min(want, max_chunks));
   }
+  static const int chunk_override = [] {
+    const char* e = std::getenv("GRIDLOC_B200_CHUNKS");  // tuning experiments only
+    return e ? std::atoi(e) : 0;
+  }();
+  if (chunk_override > 0) fp.n_chunks = std::min(chunk_override, n_win);
   fp.k_chunk = (n_win + fp.n_chunks - 1) / fp.n_chunks;
   fp.n_chunks = (n_win + fp.k_chunk - 1) / fp.k_chunk;
   const int blocks = ((fp.n_tiles + kNWARP - 1) / kNWARP) * fp.n_chunks;
@@ -518,10 +563,11 @@ void launch_rhf(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp) {
 
 template <int R, int H>
 void launch_rh(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp, bool fast) {
+  const bool peer = fp.peer_lo != nullptr || fp.peer_hi != nullptr;
   if (fast) {
-    launch_rhf<R, H, true>(ctx, tmap, fp);
+    peer ? launch_rhf<R, H, true, true>(ctx, tmap, fp) : launch_rhf<R, H, true, false>(ctx, tmap, fp);
   } else {
-    launch_rhf<R, H, false>(ctx, tmap, fp);
+    peer ? launch_rhf<R, H, false, true>(ctx, tmap, fp) : launch_rhf<R, H, false, false>(ctx, tmap, fp);
   }
 }
 
@@ -580,6 +626,9 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
   fp.src_state = a.src_state;
   fp.dst_state = a.dst_state;
   fp.step_state = a.step_state;
+  fp.peer_lo = a.peer_lo;
+  fp.peer_hi = a.peer_hi;
+  fp.n_edge = a.halo > 0 ? a.halo : 0;
   for (int t = 0; t < 2 * r + 1; ++t) fp.sep[t] = sep[t];
   for (int t = 0; t < ang.n; ++t) fp.ang[t] = ang.w[t];
   // The shift records ride in the launch parameters; more than
@@ -591,7 +640,8 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
     const int ke = std::min(a.c, kb + win);
     fp.k_base = kb;
     fp.k_end = ke;
-    fp.defer_finalize = (fp.shard || ke < a.c) ? 1 : 0;
+    // a shard holding every channel (one rank) finalises in the kernel too
+    fp.defer_finalize = ((fp.shard && !a.full_shard) || ke < a.c) ? 1 : 0;
     for (int q = 0; q < ke - kb + 2 * H; ++q) {
       // h_motion: one (dx, dy) per channel (whole tensor) or per storage
       // plane (shard: plane q <-> channel c_begin - halo + q)

@@ -479,6 +479,32 @@ void launch_apply_scale(gl_context* ctx, double* buf, size_t n,
   ctx->launches += 2;
 }
 
+// BLF1 snapshot payload (belief_tensor.cpp:555-559, 579-584): float32 <->
+// float64, round-to-nearest like static_cast<float>; float -> double exact.
+__global__ void k_to_f32(const double* __restrict__ in, float* __restrict__ out, size_t n) {
+  for (size_t q = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+       q < n; q += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    out[q] = __double2float_rn(in[q]);
+  }
+}
+
+__global__ void k_from_f32(const float* __restrict__ in, double* __restrict__ out, size_t n) {
+  for (size_t q = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+       q < n; q += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    out[q] = static_cast<double>(in[q]);
+  }
+}
+
+void launch_to_f32(gl_context* ctx, const double* in, float* out, size_t n) {
+  k_to_f32<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(in, out, n);
+  ctx->launches++;
+}
+
+void launch_from_f32(gl_context* ctx, const float* in, double* out, size_t n) {
+  k_from_f32<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(in, out, n);
+  ctx->launches++;
+}
+
 void launch_fill(gl_context* ctx, double* buf, size_t n, double v) {
   k_fill<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(buf, n, v);
   ctx->launches++;

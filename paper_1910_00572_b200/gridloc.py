@@ -9,6 +9,7 @@ reference's ``ThreadPool&`` / ``StepScratch&`` parameters become an optional
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from dataclasses import dataclass, field as dc_field
 
@@ -545,6 +546,19 @@ def belief_map(tensor: BeliefTensor) -> np.ndarray:
     out = np.empty((tensor.height(), tensor.width()))
     check(tensor.ctx.lib.gl_belief_map(tensor.ctx.h, tensor.h, _d(out)))
     return out
+
+
+def write_belief_snapshot(tensor: BeliefTensor, path: str):
+    """belief_tensor.cpp:543-563: BLF1, float32 payload (lossy)."""
+    check(tensor.ctx.lib.gl_write_belief_snapshot(tensor.ctx.h, tensor.h, os.fsencode(path)))
+
+
+def read_belief_snapshot(path: str, cell_size: float, origin_x: float, origin_y: float, ctx=None) -> BeliefTensor:
+    """belief_tensor.cpp:565-587."""
+    ctx = _ctx(ctx)
+    h = C.c_void_p()
+    check(ctx.lib.gl_read_belief_snapshot(ctx.h, os.fsencode(path), cell_size, origin_x, origin_y, C.byref(h)))
+    return BeliefTensor(ctx=ctx, _handle=h)
 
 
 def argmax_state(tensor: BeliefTensor) -> PoseEstimate:

@@ -12,7 +12,15 @@ side and a step is
   3. finalize (extinguish status, pending 1/max rescale — global, so every
      rank scales identically),
   4. the halo exchange: my first/last `halo` interior planes go to the
-     left/right neighbour's upper/lower halo (NCCL send/recv over NVLink).
+     left/right neighbour's upper/lower halo.
+
+The exchange has two forms. "peer" (default): the fused step kernel itself
+stores its edge planes into the neighbours' halo planes through peer memory
+(CUDA IPC + NVLink P2P, gl_shard_set_peers), so the transfer overlaps the
+compute tile by tile and there is no exchange step at all; the MAX
+all-reduce that follows every step is the barrier that orders those stores
+before the neighbour's next step. "nccl": NCCL send/recv of the planes after
+the step (the north star's form; kept for fabrics without P2P).
 
 No per-element operation changes, so the sharded belief is bitwise the
 unsharded one. The exchange plan and the argmax combine are pure functions
@@ -61,6 +69,32 @@ def halo_plan(c_total: int, world: int, rank: int, halo: int) -> HaloPlan:
                     recv_left=(0, halo), recv_right=(halo + n, halo))
 
 
+@dataclass(frozen=True)
+class PeerPlan:
+    """Where the fused step stores this rank's edge planes (peer mode):
+    output channels [0, halo) -> rank lo_rank's storage planes from lo_q (its
+    upper halo); channels [n - halo, n) -> rank hi_rank's planes from hi_q
+    (its lower halo)."""
+    lo_rank: int
+    lo_q: int
+    hi_rank: int
+    hi_q: int
+
+
+def peer_plan(c_total: int, world: int, rank: int, halo: int) -> PeerPlan:
+    left, right = (rank - 1) % world, (rank + 1) % world
+    lc0, lc1 = partition(c_total, world, left)
+    halo_plan(c_total, world, rank, halo)  # validates halo against the shard sizes
+    return PeerPlan(left, halo + (lc1 - lc0), right, 0)
+
+
+def exchange_ipc_handles(dist, mine, group=None):
+    """All-gather every rank's (buffer-0, buffer-1) IPC handles (bytes)."""
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, tuple(bytes(h) for h in mine), group=group)
+    return out
+
+
 def combine_argmax(cands):
     """cands: per-rank (value, global flat index); the reference keeps the
     first strict maximum in (k, j, i) order (belief_tensor.cpp:518-527), i.e.
@@ -105,7 +139,8 @@ class ThetaShard:
     """This rank's slab. Collectives go through torch.distributed (NCCL) on
     the library's stream; one process per GPU."""
 
-    def __init__(self, m, c_total: int, halo: int, rank: int, world: int, ctx, group=None):
+    def __init__(self, m, c_total: int, halo: int, rank: int, world: int, ctx, group=None,
+                 exchange: str = "peer"):
         import torch
         import torch.distributed as dist
         from .gridloc import BeliefTensor
@@ -119,6 +154,52 @@ class ThetaShard:
         self.t = BeliefTensor(ctx=ctx, _handle=h)
         self.stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", ctx.device))
         self.plane_elems = m.width() * m.height()
+        if exchange not in ("peer", "nccl"):
+            raise ValueError("exchange must be 'peer' or 'nccl'")
+        self.exchange = exchange
+        self._ipc_open = []
+        if exchange == "peer":
+            self._set_peers()
+
+    def _buffer_base(self, t_handle, buf):
+        p = C.POINTER(C.c_double)()
+        check(self.ctx.lib.gl_tensor_buffer_ptr(self.ctx.h, t_handle, buf, 0, C.byref(p)))
+        return C.cast(p, C.c_void_p).value
+
+    def _set_peers(self):
+        """Point the fused step's edge-plane stores at the neighbours' halo
+        planes: this process's own buffers when world == 1, CUDA IPC
+        mappings of the neighbours' buffers otherwise."""
+        lib, pp = self.ctx.lib, peer_plan(self.c_total, self.world, self.rank, self.halo)
+        bytes_per_plane = 8 * self.plane_elems
+        if self.world == 1:
+            bases = {self.rank: [self._buffer_base(self.t.h, b) for b in (0, 1)]}
+        else:
+            mine = []
+            for b in (0, 1):
+                h = (C.c_ubyte * 64)()
+                check(lib.gl_ipc_get_handle(self.ctx.h, self.t.h, b, h))
+                mine.append(bytes(h))
+            allh = exchange_ipc_handles(self.dist, mine, self.group)
+            bases = {}
+            for r in {pp.lo_rank, pp.hi_rank}:
+                bases[r] = []
+                for b in (0, 1):
+                    buf = (C.c_ubyte * 64).from_buffer_copy(allh[r][b])
+                    ptr = C.c_void_p()
+                    check(lib.gl_ipc_open(self.ctx.h, buf, C.byref(ptr)))
+                    self._ipc_open.append(ptr.value)
+                    bases[r].append(ptr.value)
+        lo = [bases[pp.lo_rank][b] + pp.lo_q * bytes_per_plane for b in (0, 1)]
+        hi = [bases[pp.hi_rank][b] + pp.hi_q * bytes_per_plane for b in (0, 1)]
+        check(lib.gl_shard_set_peers(self.ctx.h, self.t.h, C.c_void_p(lo[0]), C.c_void_p(lo[1]),
+                                     C.c_void_p(hi[0]), C.c_void_p(hi[1])))
+
+    def close(self):
+        """Unmap the neighbours' IPC buffers (peer mode, world > 1)."""
+        for ptr in self._ipc_open:
+            check(self.ctx.lib.gl_ipc_close(self.ctx.h, C.c_void_p(ptr)))
+        self._ipc_open = []
 
     def _planes(self, q0: int, count: int):
         p = C.POINTER(C.c_double)()
@@ -140,9 +221,13 @@ class ThetaShard:
             if self.world > 1:
                 self.dist.all_reduce(self._max_tensor(), op=self.dist.ReduceOp.MAX, group=self.group)
             check(self.ctx.lib.gl_shard_finalize(self.ctx.h, self.t.h))
-            self.exchange_halos()
+            if self.exchange == "nccl":
+                self.exchange_halos()
 
     def exchange_halos(self):
+        """Explicit exchange of the current buffer's edge planes (the "nccl"
+        mode's per-step exchange; in peer mode only needed after uploading
+        values with set_values)."""
         pl = self.plan
         if self.world == 1:
             lib = self.ctx.lib

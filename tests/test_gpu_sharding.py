@@ -80,3 +80,53 @@ def _cai(ptr):
         __cuda_array_interface__ = {"shape": (1,), "typestr": "<i8", "data": (ptr, False), "version": 3,
                                     "strides": None, "stream": None}
     return _V()
+
+
+@pytest.mark.parametrize("G,c_total,noise", [(1, 72, (0.03, 0.03, 0.012)), (2, 72, (0.03, 0.03, 0.012)),
+                                             (3, 36, (1e-4, 1e-4, 0.012)), (8, 360, (0.03, 0.03, 0.012))])
+def test_fused_peer_halo_stores_bitwise_equal_unsharded(ctx, G, c_total, noise):
+    """Peer mode: each shard's fused step stores its edge planes straight
+    into the neighbours' halo planes (gl_shard_set_peers; here the
+    neighbours' buffers on the same device stand in for CUDA-IPC mappings of
+    other GPUs' buffers, the kernel code is the same). No exchange step runs,
+    yet every step must equal the unsharded belief bit for bit."""
+    import torch
+    from paper_1910_00572_b200.sharding import peer_plan
+    occ = make_floorplan(128, 96, seed=22)
+    m = g.OccupancyMap(128, 96, 0.1, occ, ctx=ctx)
+    ks = g.build_kernels(g.MotionNoise(*noise), c_total, 0.1, 2 * math.pi / c_total)
+    act = g.make_activation(m, ks, c_total, ctx)
+    halo = max(len(ks.angular) // 2, 1)
+    full = g.init_uniform(m, c_total, ctx)
+    shards = [_shard(ctx, m, c_total, *partition(c_total, G, r), halo) for r in range(G)]
+
+    def plane(t, b, q):
+        p = C.POINTER(C.c_double)()
+        check(ctx.lib.gl_tensor_buffer_ptr(ctx.h, t.h, b, q, C.byref(p)))
+        return C.cast(p, C.c_void_p)
+
+    for r, t in enumerate(shards):
+        pp = peer_plan(c_total, G, r, halo)
+        lo, hi = shards[pp.lo_rank], shards[pp.hi_rank]
+        check(ctx.lib.gl_shard_set_peers(ctx.h, t.h, plane(lo, 0, pp.lo_q), plane(lo, 1, pp.lo_q),
+                                         plane(hi, 0, pp.hi_q), plane(hi, 1, pp.hi_q)))
+    rng = Rng(G * 7 + c_total)
+    motions = [random_motion(rng) for _ in range(5)] + [(0.1, 0.0, 0.0), (0.0, 0.0, 0.2)]
+    for (u, v, w) in motions:
+        g.step(full, g.OdometryDelta(u, v, w), m, ks, act, ctx)
+        for t in shards:
+            g.step_async(t, g.OdometryDelta(u, v, w), m, ks, act, ctx)
+        ctx.synchronize()
+        dev = [torch.as_tensor(_cai(C.cast(_max_bits(ctx, t), C.c_void_p).value), device="cuda")
+               for t in shards]
+        gmax = torch.stack(dev).max()
+        for d in dev:
+            d.copy_(gmax.reshape(1))
+        torch.cuda.synchronize()
+        for t in shards:
+            check(ctx.lib.gl_shard_finalize(ctx.h, t.h))
+        ctx.synchronize()
+        for t in shards:
+            g.tensor_status(t)
+        got = np.concatenate([t.values() for t in shards], axis=0)
+        assert_bitwise(got, full.values(), f"G={G} peer-store shards vs unsharded")

@@ -12,7 +12,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1910_00572_b200.sharding import combine_argmax, exchange_planes, halo_plan, partition
+from paper_1910_00572_b200.sharding import (combine_argmax, exchange_ipc_handles, exchange_planes, halo_plan,
+                                            partition, peer_plan)
 
 PLANE = 12  # elements per plane in these host-only tests
 
@@ -51,7 +52,11 @@ def _worker(rank, world, port, c_total, halo, q):
         outs = [torch.zeros_like(cand) for _ in range(world)]
         dist.all_gather(outs, cand)
         best = combine_argmax([(float(o[0]), int(o[1])) for o in outs])
-        q.put((rank, got == want, got, want, gmax, best))
+        # peer mode: every rank learns every rank's two IPC handles
+        mine = (bytes([rank]) * 64, bytes([rank + 100]) * 64)
+        allh = exchange_ipc_handles(dist, mine)
+        ipc_ok = all(allh[r] == (bytes([r]) * 64, bytes([r + 100]) * 64) for r in range(world))
+        q.put((rank, got == want and ipc_ok, got, want, gmax, best))
     finally:
         dist.destroy_process_group()
 
@@ -89,3 +94,25 @@ def test_combine_argmax_rules():
     assert combine_argmax([(0.5, 10), (0.7, 99), (0.7, 3)]) == (0.7, 3)
     assert combine_argmax([(-1.0, 0), (-1.0, 5)]) is None
     assert combine_argmax([(float("nan"), 0), (0.1, 4)]) == (0.1, 4)
+
+
+@pytest.mark.parametrize("world,c_total,halo", [(1, 72, 1), (2, 8, 1), (3, 36, 1), (8, 360, 3), (3, 16, 2),
+                                                (5, 72, 1)])
+def test_peer_plan_targets_the_halo_planes_the_exchange_fills(world, c_total, halo):
+    """The fused peer stores must land exactly where the explicit exchange
+    would put them: my first `halo` planes -> the left neighbour's upper halo
+    (its recv_right), my last -> the right neighbour's lower halo (its
+    recv_left); channel identities match the storage-plane rule."""
+    for r in range(world):
+        pp = peer_plan(c_total, world, r, halo)
+        pl = halo_plan(c_total, world, r, halo)
+        assert (pp.lo_rank, pp.hi_rank) == (pl.left, pl.right)
+        assert (pp.lo_q, halo) == halo_plan(c_total, world, pl.left, halo).recv_right
+        assert (pp.hi_q, halo) == halo_plan(c_total, world, pl.right, halo).recv_left
+        c0, c1 = partition(c_total, world, r)
+        lc0, _ = partition(c_total, world, pl.left)
+        rc0, _ = partition(c_total, world, pl.right)
+        for e in range(halo):
+            # storage plane q of rank s holds channel (c_begin_s - halo + q) mod C
+            assert (lc0 - halo + pp.lo_q + e) % c_total == (c0 + e) % c_total
+            assert (rc0 - halo + pp.hi_q + e) % c_total == (c1 - halo + e) % c_total
