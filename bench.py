@@ -410,8 +410,8 @@ def run_sharded(args, cfg, world, rank, local):
         "config": {"workload": cfg["workload"], "W": W, "H": H, "channels": C,
                    "parallelism": f"theta-slab sharding over {world} GPU(s), {n_local} channels + 2x{halo} "
                                   "halo planes per GPU; NCCL all-reduce (8 B) per step; halo exchange "
-                                  + ("fused into the step kernel (edge planes stored into the neighbours' "
-                                     "halo planes over CUDA IPC / NVLink P2P)" if args.exchange == "peer"
+                                  + ("fused into the step kernel (TMA reads of the neighbours' planes "
+                                     "over CUDA IPC / NVLink P2P)" if args.exchange == "peer"
                                      else "by NCCL send/recv after the step"),
                    "l2": "the per-GPU slab exceeds L2"},
         "e2e": None,

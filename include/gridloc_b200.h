@@ -214,18 +214,20 @@ gl_status gl_tensor_plane_ptr(gl_context* ctx, gl_tensor* t, int q,
 gl_status gl_tensor_max_ptr(gl_context* ctx, gl_tensor* t,
                             unsigned long long** dptr);
 gl_status gl_shard_finalize(gl_context* ctx, gl_tensor* t);
-/* Fused halo exchange over peer memory (NVLink P2P; no separate exchange
- * step): with peers set, the shard's step also stores its first `halo`
- * output planes into the left neighbour's upper halo planes (lo_b = that
- * neighbour's buffer-b storage plane halo + its channel count) and its last
- * `halo` output planes into the right neighbour's lower halo (hi_b = the
- * neighbour's buffer-b storage plane 0). Pointers come from
+/* Halo exchange fused into the step over peer memory (NVLink P2P): with
+ * peers set, the step's TMA reads its lower halo input planes straight from
+ * the left neighbour's buffer and its upper ones from the right neighbour's
+ * (lo_b / hi_b = the neighbour's buffer b at storage plane 0, lo_count /
+ * hi_count = their interior channel counts; same W, H and halo on every
+ * shard), so no exchange step exists. Pointers come from
  * gl_tensor_buffer_ptr in this process (same device or peer-enabled
  * devices) or gl_ipc_open across processes. The cross-rank max all-reduce
- * that follows every step orders these stores before the neighbour's next
- * step. All NULL: no peer stores (exchange planes yourself). */
+ * after every step orders the neighbours' writes of a buffer before these
+ * reads, and these reads before the neighbours overwrite it. All NULL:
+ * read the shard's own halo planes (exchange them yourself). */
 gl_status gl_shard_set_peers(gl_context* ctx, gl_tensor* t, void* lo0,
-                             void* lo1, void* hi0, void* hi1);
+                             void* lo1, int lo_count, void* hi0, void* hi1,
+                             int hi_count);
 /* storage plane q of ping-pong buffer buf (0/1); the current one is
  * gl_tensor_current_buffer (all shards of one belief flip together) */
 gl_status gl_tensor_buffer_ptr(gl_context* ctx, gl_tensor* t, int buf, int q,

@@ -74,7 +74,7 @@ SIGNATURES = {
     "gl_tensor_copy_planes": [_vp, _vp, C.c_int, _vp, C.c_int, C.c_int],
     "gl_write_belief_snapshot": [_vp, _vp, C.c_char_p],
     "gl_read_belief_snapshot": [_vp, C.c_char_p, C.c_double, C.c_double, C.c_double, _pvp],
-    "gl_shard_set_peers": [_vp, _vp, _vp, _vp, _vp, _vp],
+    "gl_shard_set_peers": [_vp, _vp, _vp, _vp, C.c_int, _vp, _vp, C.c_int],
     "gl_tensor_buffer_ptr": [_vp, _vp, C.c_int, C.c_int, C.POINTER(_dp)],
     "gl_tensor_current_buffer": [_vp, _ip],
     "gl_ipc_get_handle": [_vp, _vp, C.c_int, _vp],

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <deque>
 #include <fstream>
 #include <memory>
 #include <mutex>
@@ -127,6 +128,7 @@ bool make_tmap(CUtensorMap* m, double* base, int w, int h, int c, int bw,
 // Tensor-map cache per (tensor buffer, box) lives on the tensor.
 struct TmapCache {
   double* base = nullptr;
+  int planes = 0;
   int bw = 0, bh = 0;
   CUtensorMap map;
 };
@@ -250,7 +252,7 @@ gl_status read_status(gl_context* ctx, gl_tensor* t) {
 // Per-tensor TMA map cache (stored out of line to keep gl_tensor POD-ish).
 namespace {
 struct TensorExtra {
-  std::vector<TmapCache> maps;
+  std::deque<TmapCache> maps;  // stable addresses
 };
 std::mutex g_extra_mu;
 std::vector<std::pair<const gl_tensor*, std::unique_ptr<TensorExtra>>> g_extra;
@@ -270,17 +272,24 @@ void drop_extra(const gl_tensor* t) {
                 g_extra.end());
 }
 
-const CUtensorMap* tensor_tmap(gl_tensor* t, int buf, int bw, int bh) {
+// map over `planes` storage planes at `base` (the tensor's own buffer, or a
+// theta-shard neighbour's), cached on the tensor
+const CUtensorMap* tensor_tmap_at(gl_tensor* t, double* base, int planes, int bw, int bh) {
   TensorExtra* x = extra_of(t);
   for (auto& m : x->maps)
-    if (m.base == t->d_buf[buf] && m.bw == bw && m.bh == bh) return &m.map;
+    if (m.base == base && m.planes == planes && m.bw == bw && m.bh == bh) return &m.map;
   TmapCache c;
-  c.base = t->d_buf[buf];
+  c.base = base;
+  c.planes = planes;
   c.bw = bw;
   c.bh = bh;
-  if (!make_tmap(&c.map, c.base, t->w, t->h, t->c + 2 * halo_of(t), bw, bh)) return nullptr;
+  if (!make_tmap(&c.map, c.base, t->w, t->h, planes, bw, bh)) return nullptr;
   x->maps.push_back(c);
   return &x->maps.back().map;
+}
+
+const CUtensorMap* tensor_tmap(gl_tensor* t, int buf, int bw, int bh) {
+  return tensor_tmap_at(t, t->d_buf[buf], t->c + 2 * halo_of(t), bw, bh);
 }
 }  // namespace
 
@@ -1015,8 +1024,14 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
     a.motion = nullptr;
     a.halo = t->halo;
     a.full_shard = t->c == t->c_total;
-    a.peer_lo = t->peer_lo[dst];
-    a.peer_hi = t->peer_hi[dst];
+    if (fused && t->peer_lo_buf[src] != nullptr) {
+      int bw = 0, bh = 0;
+      glb::fused_box(r, ang.n / 2, &bw, &bh);
+      a.tmap_lo = tensor_tmap_at(t, t->peer_lo_buf[src], t->peer_lo_count + 2 * t->halo, bw, bh);
+      a.tmap_hi = tensor_tmap_at(t, t->peer_hi_buf[src], t->peer_hi_count + 2 * t->halo, bw, bh);
+      if (a.tmap_lo == nullptr || a.tmap_hi == nullptr) fail(GL_E_CUDA, "tensor map over a peer buffer failed");
+      a.lo_add = t->peer_lo_count;
+    }
   } else if (fused) {
     hm.resize(2 * static_cast<size_t>(t->c));
     glb::motion_table(u, v, 0, t->c, t->theta_t, 2.0 * M_PI / t->c, t->cell, hm.data());
@@ -1145,17 +1160,20 @@ gl_status gl_shard_finalize(gl_context* ctx, gl_tensor* t) {
   });
 }
 
-gl_status gl_shard_set_peers(gl_context* ctx, gl_tensor* t, void* lo0, void* lo1, void* hi0,
-                             void* hi1) {
+gl_status gl_shard_set_peers(gl_context* ctx, gl_tensor* t, void* lo0, void* lo1, int lo_count,
+                             void* hi0, void* hi1, int hi_count) {
   return guard([&] {
     need(ctx && t, "null argument");
     need(t->halo >= 0, "not a sharded tensor");
-    need((lo0 == nullptr) == (lo1 == nullptr) && (hi0 == nullptr) == (hi1 == nullptr),
-         "peer planes must be given for both buffers");
-    t->peer_lo[0] = static_cast<double*>(lo0);
-    t->peer_lo[1] = static_cast<double*>(lo1);
-    t->peer_hi[0] = static_cast<double*>(hi0);
-    t->peer_hi[1] = static_cast<double*>(hi1);
+    const bool none = !lo0 && !lo1 && !hi0 && !hi1;
+    need(none || (lo0 && lo1 && hi0 && hi1), "peer buffers must be given for both neighbours and buffers");
+    need(none || (lo_count >= t->halo && hi_count >= t->halo), "a neighbour holds fewer channels than the halo");
+    for (int b = 0; b < 2; ++b) {
+      t->peer_lo_buf[b] = static_cast<double*>(b ? lo1 : lo0);
+      t->peer_hi_buf[b] = static_cast<double*>(b ? hi1 : hi0);
+    }
+    t->peer_lo_count = none ? 0 : lo_count;
+    t->peer_hi_count = none ? 0 : hi_count;
   });
 }
 

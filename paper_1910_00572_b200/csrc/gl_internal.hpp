@@ -161,9 +161,11 @@ struct gl_tensor {
   int device = 0;
   CUtensorMap tmap[2];  // 3-D TMA descriptors over d_buf[0/1]
   bool tmap_ok = false;
-  // shard peer planes per destination buffer (gl_shard_set_peers)
-  double* peer_lo[2] = {nullptr, nullptr};
-  double* peer_hi[2] = {nullptr, nullptr};
+  // shard peers (gl_shard_set_peers): the neighbours' ping-pong buffers
+  // (storage plane 0) and their interior channel counts
+  double* peer_lo_buf[2] = {nullptr, nullptr};
+  double* peer_hi_buf[2] = {nullptr, nullptr};
+  int peer_lo_count = 0, peer_hi_count = 0;
 };
 
 // ---------------------------------------------------------------- launchers
@@ -189,10 +191,11 @@ struct StepArgs {
   int w, h, c;             // c = output channels (a shard's interior planes)
   int halo = -1;           // theta-slab shard: halo planes per side; -1 = whole tensor
   bool full_shard = false; // the shard holds all channels (one rank): no cross-rank max
-  // theta-slab shard with peer planes: the step also stores its first / last
-  // `halo` output planes into the neighbours' halo planes (peer memory)
-  double* peer_lo = nullptr;  // left neighbour's plane for my output channel 0
-  double* peer_hi = nullptr;  // right neighbour's plane for my channel c - halo
+  // theta-slab shard with peers: the step reads its halo input planes
+  // straight from the neighbours' buffers (TMA over peer memory)
+  const CUtensorMap* tmap_lo = nullptr;  // left neighbour's source buffer
+  const CUtensorMap* tmap_hi = nullptr;  // right neighbour's source buffer
+  int lo_add = 0;                        // left neighbour's interior channel count
 };
 
 // k_generic.cu

@@ -129,9 +129,10 @@ struct FusedParams {
   int plane_off;             // shard: storage plane of iteration 0 (= halo - H)
   int out_off;               // shard: storage plane of output channel 0 (= halo)
   int defer_finalize;        // shard: leave the local max for a cross-rank all-reduce
-  double* peer_lo;           // shard: also store output channels [0, n_edge) here (peer memory)
-  double* peer_hi;           //        and channels [c - n_edge, c) here
-  int n_edge;
+  // shard with peers: storage planes s < halo are read from the left
+  // neighbour's buffer (its plane s + lo_add), planes s >= halo + c from the
+  // right neighbour's (plane s - c), through their own tensor maps
+  int peer_read, halo, lo_add;
   int tiles_x, n_tiles;
   int k_base, k_end;         // this launch's output channels (a window of <= kParamChannels - 2H)
   int k_chunk, n_chunks;     // output channels per warp, chunks per tile
@@ -238,8 +239,10 @@ __device__ __forceinline__ double row_pass(const FusedParams& p, double s) {
   return dot_seq<2 * R + 1, FAST>(p.sep, nb);
 }
 
-template <int R, int H, int ROWS, int NS, bool FAST, bool PEER>
+template <int R, int H, int ROWS, int NS, bool FAST>
 __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
+                                            const CUtensorMap* tmap_lo,
+                                            const CUtensorMap* tmap_hi,
                                             const FusedParams& p, double* Bs,
                                             uint64_t* mbar, int lane, int x0,
                                             int y0, int k0, int n_out,
@@ -263,10 +266,22 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
   };
   const int rec0 = k0 - p.k_base;
   auto issue = [&](int it, int stage) {
-    const int kc = chan_of(it);
+    int kc = chan_of(it);
+    const CUtensorMap* m = tmap;
+    if (p.peer_read) {
+      // theta-slab halo planes come straight from the neighbours' buffers
+      // (peer memory over NVLink): no halo exchange step exists
+      if (kc < p.halo) {
+        m = tmap_lo;
+        kc += p.lo_add;
+      } else if (kc >= p.halo + C) {
+        m = tmap_hi;
+        kc -= C;
+      }
+    }
     const int2 o = make_int2(p.rec[rec0 + it].ox, p.rec[rec0 + it].oy);
     mbar_arrive_expect(&mbar[stage], G::B_BYTES);
-    tma_load_3d(Bs + stage * G::STAGE, tmap, (x0 - R - o.x - 1) & ~1,
+    tma_load_3d(Bs + stage * G::STAGE, m, (x0 - R - o.x - 1) & ~1,
                 y0 - R - o.y - 1, kc, &mbar[stage]);
   };
 
@@ -328,25 +343,6 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
     }
     const double* Bb = stage_ptr + ((x0 - R - cs.sx - 1) & 1) + lane;
     double* orow = out_tile + plane * static_cast<size_t>(p.out_off + k0 + (emit ? it - 2 * H : 0));  // += W per row
-    // PEER: shard edge planes also go to the neighbour's halo planes (one
-    // more store per row, over NVLink): the halo exchange is fused into the
-    // step. Non-edge channels aim the second store at their own output, so
-    // the row loop stays branch-free.
-    double* prow = orow;
-    bool pe = false;  // channel-uniform: this output plane is an edge plane
-    if constexpr (PEER) {
-      if (emit) {
-        const int k = k0 + it - 2 * H;
-        const size_t toff = static_cast<size_t>(out_tile - p.dst);
-        if (p.peer_lo != nullptr && k < p.n_edge) {
-          prow = p.peer_lo + plane * static_cast<size_t>(k) + toff;
-          pe = true;
-        } else if (p.peer_hi != nullptr && k >= p.c - p.n_edge) {
-          prow = p.peer_hi + plane * static_cast<size_t>(k - (p.c - p.n_edge)) + toff;
-          pe = true;
-        }
-      }
-    }
 
     double lo_c0 = Bb[1], lo_c1 = Bb[0];
     double rw[2 * R + 1];  // rolling window of row-pass results
@@ -400,11 +396,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
 #else
           if (ok) *orow = o;
 #endif
-          if constexpr (PEER) {
-            if (ok & pe) *prow = o;  // one predicated store, no branch in the row loop
-          }
           orow += W;
-          if constexpr (PEER) prow += W;
         }
       }
     }
@@ -430,9 +422,11 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
   return vmax;
 }
 
-template <int R, int H, int ROWS, int NS, int NWARP, bool FAST, bool PEER>
+template <int R, int H, int ROWS, int NS, int NWARP, bool FAST>
 __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_MINB_H3)
     k_fused_step(const __grid_constant__ CUtensorMap tmap,
+                 const __grid_constant__ CUtensorMap tmap_lo,
+                 const __grid_constant__ CUtensorMap tmap_hi,
                  const FusedParams p) {
   using G = Geo<R, ROWS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -467,15 +461,13 @@ __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_
   const int y0 = (tile / p.tiles_x) * ROWS;
   const int k0 = p.k_base + chunk * p.k_chunk;
   const int n_out = min(p.k_chunk, p.k_end - k0);
-  double vmax = warp_tile<R, H, ROWS, NS, FAST, PEER>(&tmap, p, Bs, mbar, lane, x0, y0, k0, n_out, active);
+  double vmax = warp_tile<R, H, ROWS, NS, FAST>(&tmap, &tmap_lo, &tmap_hi, p, Bs, mbar, lane, x0, y0, k0, n_out,
+                                                active);
 
   // global max -> the last CTA finalises status and the pending rescale
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) vmax = dmax_ref(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
   if (lane == 0) wmax[warp] = vmax;
-  // peer-plane stores must be visible to the neighbour's next step (which
-  // starts after the cross-rank max all-reduce that follows this kernel)
-  if constexpr (PEER) __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
     double bm = 0.0;
@@ -521,13 +513,13 @@ constexpr size_t smem_bytes() {
   return 128 + static_cast<size_t>(kNWARP) * kNS * G::STAGE * 8 + kNWARP * kNS * 8 + kNWARP * 8;
 }
 
-template <int R, int H, bool FAST, bool PEER>
-void launch_rhf(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp) {
+template <int R, int H, bool FAST>
+void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& fp) {
   const int n_win = fp.k_end - fp.k_base;
   constexpr int ROWS = rows_for<H>();
   using G = Geo<R, ROWS>;
   constexpr size_t smem = smem_bytes<R, ROWS>();
-  auto kern = k_fused_step<R, H, ROWS, kNS, kNWARP, FAST, PEER>;
+  auto kern = k_fused_step<R, H, ROWS, kNS, kNWARP, FAST>;
   static uint64_t configured = 0;  // bit per device: the attribute is per device
   const uint64_t bit = 1ull << (ctx->device & 63);
   if (!(configured & bit)) {
@@ -557,22 +549,21 @@ void launch_rhf(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp) {
   fp.k_chunk = (n_win + fp.n_chunks - 1) / fp.n_chunks;
   fp.n_chunks = (n_win + fp.k_chunk - 1) / fp.k_chunk;
   const int blocks = ((fp.n_tiles + kNWARP - 1) / kNWARP) * fp.n_chunks;
-  kern<<<blocks, 32 * kNWARP, smem, ctx->stream>>>(*tmap, fp);
+  kern<<<blocks, 32 * kNWARP, smem, ctx->stream>>>(*tmaps[0], *tmaps[1], *tmaps[2], fp);
   ctx->launches++;
 }
 
 template <int R, int H>
-void launch_rh(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp, bool fast) {
-  const bool peer = fp.peer_lo != nullptr || fp.peer_hi != nullptr;
+void launch_rh(gl_context* ctx, const CUtensorMap* const* tmap, FusedParams& fp, bool fast) {
   if (fast) {
-    peer ? launch_rhf<R, H, true, true>(ctx, tmap, fp) : launch_rhf<R, H, true, false>(ctx, tmap, fp);
+    launch_rhf<R, H, true>(ctx, tmap, fp);
   } else {
-    peer ? launch_rhf<R, H, false, true>(ctx, tmap, fp) : launch_rhf<R, H, false, false>(ctx, tmap, fp);
+    launch_rhf<R, H, false>(ctx, tmap, fp);
   }
 }
 
 template <int R>
-void launch_r(gl_context* ctx, const CUtensorMap* tmap, FusedParams& fp, int H,
+void launch_r(gl_context* ctx, const CUtensorMap* const* tmap, FusedParams& fp, int H,
               bool fast) {
   switch (H) {
     case 0: launch_rh<R, 0>(ctx, tmap, fp, fast); break;
@@ -626,9 +617,10 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
   fp.src_state = a.src_state;
   fp.dst_state = a.dst_state;
   fp.step_state = a.step_state;
-  fp.peer_lo = a.peer_lo;
-  fp.peer_hi = a.peer_hi;
-  fp.n_edge = a.halo > 0 ? a.halo : 0;
+  fp.peer_read = (a.tmap_lo != nullptr && a.tmap_hi != nullptr) ? 1 : 0;
+  fp.halo = a.halo > 0 ? a.halo : 0;
+  fp.lo_add = a.lo_add;
+  const CUtensorMap* maps[3] = {tmap, fp.peer_read ? a.tmap_lo : tmap, fp.peer_read ? a.tmap_hi : tmap};
   for (int t = 0; t < 2 * r + 1; ++t) fp.sep[t] = sep[t];
   for (int t = 0; t < ang.n; ++t) fp.ang[t] = ang.w[t];
   // The shift records ride in the launch parameters; more than
@@ -655,9 +647,9 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
       chan_rec(a.h_motion[2 * src], a.h_motion[2 * src + 1], &fp.rec[q]);
     }
     switch (r) {
-      case 0: launch_r<0>(ctx, tmap, fp, H, fast); break;
-      case 1: launch_r<1>(ctx, tmap, fp, H, fast); break;
-      default: launch_r<2>(ctx, tmap, fp, H, fast); break;
+      case 0: launch_r<0>(ctx, maps, fp, H, fast); break;
+      case 1: launch_r<1>(ctx, maps, fp, H, fast); break;
+      default: launch_r<2>(ctx, maps, fp, H, fast); break;
     }
   }
 }

@@ -25,6 +25,7 @@ __all__ = [
     "load_map", "init_uniform", "motion_vector", "build_kernels", "make_activation", "step", "step_async",
     "apply_motion", "belief_map", "argmax_state", "dither_samples", "scan_likelihood", "observation_update",
     "distance_field", "wrap_angle", "compose_delta", "Localizer", "LocalizerConfig",
+    "write_belief_snapshot", "read_belief_snapshot",
     "BeliefExtinguishedError", "MapParseError", "CudaError", "GridlocError",
 ]
 

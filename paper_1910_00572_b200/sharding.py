@@ -14,13 +14,14 @@ side and a step is
   4. the halo exchange: my first/last `halo` interior planes go to the
      left/right neighbour's upper/lower halo.
 
-The exchange has two forms. "peer" (default): the fused step kernel itself
-stores its edge planes into the neighbours' halo planes through peer memory
-(CUDA IPC + NVLink P2P, gl_shard_set_peers), so the transfer overlaps the
-compute tile by tile and there is no exchange step at all; the MAX
-all-reduce that follows every step is the barrier that orders those stores
-before the neighbour's next step. "nccl": NCCL send/recv of the planes after
-the step (the north star's form; kept for fabrics without P2P).
+The exchange has two forms. "peer" (default): the fused step kernel reads
+its halo input planes straight from the neighbours' buffers through peer
+memory (CUDA IPC mappings, TMA over NVLink P2P; gl_shard_set_peers), so the
+transfer overlaps the compute tile by tile and there is no exchange step at
+all; the MAX all-reduce that follows every step is the barrier that orders
+a neighbour's writes of a buffer before these reads, and these reads before
+the neighbour overwrites it. "nccl": NCCL send/recv of the planes after the
+step (the north star's form; kept for fabrics without P2P).
 
 No per-element operation changes, so the sharded belief is bitwise the
 unsharded one. The exchange plan and the argmax combine are pure functions
@@ -71,21 +72,22 @@ def halo_plan(c_total: int, world: int, rank: int, halo: int) -> HaloPlan:
 
 @dataclass(frozen=True)
 class PeerPlan:
-    """Where the fused step stores this rank's edge planes (peer mode):
-    output channels [0, halo) -> rank lo_rank's storage planes from lo_q (its
-    upper halo); channels [n - halo, n) -> rank hi_rank's planes from hi_q
-    (its lower halo)."""
+    """Where the fused step reads this rank's halo input planes (peer mode):
+    storage plane s < halo comes from rank lo_rank's storage plane
+    s + lo_count (lo_count = its interior channel count), plane s >= halo + n
+    from rank hi_rank's plane s - n."""
     lo_rank: int
-    lo_q: int
+    lo_count: int
     hi_rank: int
-    hi_q: int
+    hi_count: int
 
 
 def peer_plan(c_total: int, world: int, rank: int, halo: int) -> PeerPlan:
     left, right = (rank - 1) % world, (rank + 1) % world
     lc0, lc1 = partition(c_total, world, left)
+    rc0, rc1 = partition(c_total, world, right)
     halo_plan(c_total, world, rank, halo)  # validates halo against the shard sizes
-    return PeerPlan(left, halo + (lc1 - lc0), right, 0)
+    return PeerPlan(left, lc1 - lc0, right, rc1 - rc0)
 
 
 def exchange_ipc_handles(dist, mine, group=None):
@@ -167,11 +169,10 @@ class ThetaShard:
         return C.cast(p, C.c_void_p).value
 
     def _set_peers(self):
-        """Point the fused step's edge-plane stores at the neighbours' halo
-        planes: this process's own buffers when world == 1, CUDA IPC
-        mappings of the neighbours' buffers otherwise."""
+        """Point the fused step's halo reads at the neighbours' buffers: this
+        process's own buffers when world == 1, CUDA IPC mappings of the
+        neighbours' buffers otherwise."""
         lib, pp = self.ctx.lib, peer_plan(self.c_total, self.world, self.rank, self.halo)
-        bytes_per_plane = 8 * self.plane_elems
         if self.world == 1:
             bases = {self.rank: [self._buffer_base(self.t.h, b) for b in (0, 1)]}
         else:
@@ -190,10 +191,9 @@ class ThetaShard:
                     check(lib.gl_ipc_open(self.ctx.h, buf, C.byref(ptr)))
                     self._ipc_open.append(ptr.value)
                     bases[r].append(ptr.value)
-        lo = [bases[pp.lo_rank][b] + pp.lo_q * bytes_per_plane for b in (0, 1)]
-        hi = [bases[pp.hi_rank][b] + pp.hi_q * bytes_per_plane for b in (0, 1)]
-        check(lib.gl_shard_set_peers(self.ctx.h, self.t.h, C.c_void_p(lo[0]), C.c_void_p(lo[1]),
-                                     C.c_void_p(hi[0]), C.c_void_p(hi[1])))
+        lo, hi = bases[pp.lo_rank], bases[pp.hi_rank]
+        check(lib.gl_shard_set_peers(self.ctx.h, self.t.h, C.c_void_p(lo[0]), C.c_void_p(lo[1]), pp.lo_count,
+                                     C.c_void_p(hi[0]), C.c_void_p(hi[1]), pp.hi_count))
 
     def close(self):
         """Unmap the neighbours' IPC buffers (peer mode, world > 1)."""
@@ -226,8 +226,7 @@ class ThetaShard:
 
     def exchange_halos(self):
         """Explicit exchange of the current buffer's edge planes (the "nccl"
-        mode's per-step exchange; in peer mode only needed after uploading
-        values with set_values)."""
+        mode's per-step exchange; peer mode never needs it)."""
         pl = self.plan
         if self.world == 1:
             lib = self.ctx.lib

@@ -84,12 +84,14 @@ def _cai(ptr):
 
 @pytest.mark.parametrize("G,c_total,noise", [(1, 72, (0.03, 0.03, 0.012)), (2, 72, (0.03, 0.03, 0.012)),
                                              (3, 36, (1e-4, 1e-4, 0.012)), (8, 360, (0.03, 0.03, 0.012))])
-def test_fused_peer_halo_stores_bitwise_equal_unsharded(ctx, G, c_total, noise):
-    """Peer mode: each shard's fused step stores its edge planes straight
-    into the neighbours' halo planes (gl_shard_set_peers; here the
+def test_fused_peer_halo_reads_bitwise_equal_unsharded(ctx, G, c_total, noise):
+    """Peer mode: each shard's fused step TMA-reads its halo input planes
+    straight from the neighbours' buffers (gl_shard_set_peers; here the
     neighbours' buffers on the same device stand in for CUDA-IPC mappings of
-    other GPUs' buffers, the kernel code is the same). No exchange step runs,
-    yet every step must equal the unsharded belief bit for bit."""
+    other GPUs' buffers — the kernel code is the same). No exchange step
+    runs and the shards' own halo planes are never written, yet every step
+    must equal the unsharded belief bit for bit. G = 1 reads its own
+    interior planes circularly."""
     import torch
     from paper_1910_00572_b200.sharding import peer_plan
     occ = make_floorplan(128, 96, seed=22)
@@ -100,16 +102,23 @@ def test_fused_peer_halo_stores_bitwise_equal_unsharded(ctx, G, c_total, noise):
     full = g.init_uniform(m, c_total, ctx)
     shards = [_shard(ctx, m, c_total, *partition(c_total, G, r), halo) for r in range(G)]
 
-    def plane(t, b, q):
+    def base(t, b):
         p = C.POINTER(C.c_double)()
-        check(ctx.lib.gl_tensor_buffer_ptr(ctx.h, t.h, b, q, C.byref(p)))
+        check(ctx.lib.gl_tensor_buffer_ptr(ctx.h, t.h, b, 0, C.byref(p)))
         return C.cast(p, C.c_void_p)
 
     for r, t in enumerate(shards):
         pp = peer_plan(c_total, G, r, halo)
         lo, hi = shards[pp.lo_rank], shards[pp.hi_rank]
-        check(ctx.lib.gl_shard_set_peers(ctx.h, t.h, plane(lo, 0, pp.lo_q), plane(lo, 1, pp.lo_q),
-                                         plane(hi, 0, pp.hi_q), plane(hi, 1, pp.hi_q)))
+        check(ctx.lib.gl_shard_set_peers(ctx.h, t.h, base(lo, 0), base(lo, 1), pp.lo_count,
+                                         base(hi, 0), base(hi, 1), pp.hi_count))
+        # poison the own halo planes: peer mode must never read them
+        for b in (0, 1):
+            for q in list(range(halo)) + list(range(halo + t.channels(), 2 * halo + t.channels())):
+                p = C.POINTER(C.c_double)()
+                check(ctx.lib.gl_tensor_buffer_ptr(ctx.h, t.h, b, q, C.byref(p)))
+                torch.as_tensor(_cai_f64(C.cast(p, C.c_void_p).value, 128 * 96), device="cuda").fill_(float("nan"))
+    torch.cuda.synchronize()
     rng = Rng(G * 7 + c_total)
     motions = [random_motion(rng) for _ in range(5)] + [(0.1, 0.0, 0.0), (0.0, 0.0, 0.2)]
     for (u, v, w) in motions:
@@ -129,4 +138,11 @@ def test_fused_peer_halo_stores_bitwise_equal_unsharded(ctx, G, c_total, noise):
         for t in shards:
             g.tensor_status(t)
         got = np.concatenate([t.values() for t in shards], axis=0)
-        assert_bitwise(got, full.values(), f"G={G} peer-store shards vs unsharded")
+        assert_bitwise(got, full.values(), f"G={G} peer-read shards vs unsharded")
+
+
+def _cai_f64(ptr, n):
+    class _V:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3,
+                                    "strides": None, "stream": None}
+    return _V()

@@ -98,21 +98,27 @@ def test_combine_argmax_rules():
 
 @pytest.mark.parametrize("world,c_total,halo", [(1, 72, 1), (2, 8, 1), (3, 36, 1), (8, 360, 3), (3, 16, 2),
                                                 (5, 72, 1)])
-def test_peer_plan_targets_the_halo_planes_the_exchange_fills(world, c_total, halo):
-    """The fused peer stores must land exactly where the explicit exchange
-    would put them: my first `halo` planes -> the left neighbour's upper halo
-    (its recv_right), my last -> the right neighbour's lower halo (its
-    recv_left); channel identities match the storage-plane rule."""
+def test_peer_plan_reads_the_channels_the_halo_holds(world, c_total, halo):
+    """Peer mode reads halo input planes from the neighbours' buffers: own
+    storage plane s < halo from the left neighbour's plane s + lo_count,
+    s >= halo + n from the right neighbour's plane s - n. Those planes must
+    hold exactly the channels the own halo planes stand for (storage plane q
+    of rank r holds channel (c_begin_r - halo + q) mod C), and must be
+    interior planes of the neighbour (it wrote them in the last step)."""
     for r in range(world):
         pp = peer_plan(c_total, world, r, halo)
         pl = halo_plan(c_total, world, r, halo)
         assert (pp.lo_rank, pp.hi_rank) == (pl.left, pl.right)
-        assert (pp.lo_q, halo) == halo_plan(c_total, world, pl.left, halo).recv_right
-        assert (pp.hi_q, halo) == halo_plan(c_total, world, pl.right, halo).recv_left
         c0, c1 = partition(c_total, world, r)
-        lc0, _ = partition(c_total, world, pl.left)
-        rc0, _ = partition(c_total, world, pl.right)
-        for e in range(halo):
-            # storage plane q of rank s holds channel (c_begin_s - halo + q) mod C
-            assert (lc0 - halo + pp.lo_q + e) % c_total == (c0 + e) % c_total
-            assert (rc0 - halo + pp.hi_q + e) % c_total == (c1 - halo + e) % c_total
+        n = c1 - c0
+        lc0, lc1 = partition(c_total, world, pl.left)
+        rc0, rc1 = partition(c_total, world, pl.right)
+        assert (pp.lo_count, pp.hi_count) == (lc1 - lc0, rc1 - rc0)
+        for s in range(halo):
+            q = s + pp.lo_count
+            assert halo <= q < halo + pp.lo_count
+            assert (lc0 - halo + q) % c_total == (c0 - halo + s) % c_total
+        for s in range(halo + n, 2 * halo + n):
+            q = s - n
+            assert halo <= q < halo + pp.hi_count
+            assert (rc0 - halo + q) % c_total == (c0 - halo + s) % c_total
