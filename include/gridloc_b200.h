@@ -68,6 +68,11 @@ gl_status gl_context_set_path(gl_context* ctx, int path);
  * 1 (default) drops the bitwise no-op 0.0 seeds / copy selects; 0 always
  * runs the literal reference operation sequence. Results are identical. */
 gl_status gl_context_set_fast(gl_context* ctx, int enable);
+/* Step max in the fused FAST kernel: 0 = auto (high-word max on tensors of
+ * >= 2^27 states, with an exact full-grid epilogue when it cannot decide
+ * max >= 1e-6), 1 = always, 2 = never (exact max in the kernel). Results are
+ * bit-identical in every mode. */
+gl_status gl_context_set_himax(gl_context* ctx, int mode);
 /* scan_likelihood's final exp (the per-pose geometric mean,
  * observation.cpp:110): 1 (default) evaluates it with the host's libm like the
  * reference (bit-exact; one D2H/H2D of <= 512*Theta doubles per observation),
@@ -298,6 +303,28 @@ gl_status gl_observation_update(gl_context* ctx, gl_tensor* t,
                                 int n_beams, double max_range,
                                 const gl_map* map, const gl_field* field,
                                 gl_likelihood params);
+
+/* diagnostics: out4[0] = step epilogues that took the exact max */
+gl_status gl_debug_counters(gl_context* ctx, unsigned long long* out4);
+
+/* map_difficulty (evaluation.cpp:25-72; DifficultyConfig evaluation.hpp:
+ * 21-29): the fraction of free cells (interior, every `stride`-th) whose
+ * noise-free scan is best matched (first maximum over candidate cells x
+ * theta_bins headings, scan_likelihood) more than error_threshold meters
+ * away. Bit-exact: host-libm tables, device FP64 in reference order, near
+ * ties re-decided with glibc exp. beam_count <= 256. */
+typedef struct {
+  double error_threshold; /* C, meters (1.0) */
+  int beam_count;         /* 8 */
+  double fov;             /* 2 pi */
+  double max_range;       /* 8 m */
+  int stride;             /* 1 */
+  int theta_bins;         /* 8 */
+  gl_likelihood likelihood; /* {0.2, 0.05, 1} */
+} gl_difficulty_config;
+gl_status gl_map_difficulty(gl_context* ctx, const gl_map* map,
+                            const gl_field* field,
+                            const gl_difficulty_config* cfg, double* out);
 
 #ifdef __cplusplus
 }

@@ -298,6 +298,9 @@ class Ref:
         L.ref_write_snapshot.argtypes = [_vp, C.c_char_p]
         L.ref_read_snapshot.argtypes = [C.c_char_p, C.c_double, C.c_double, C.c_double, C.POINTER(_vp)]
         L.ref_tensor_dims.argtypes = [_vp, _ip, _ip, _ip]
+        L.ref_map_difficulty.argtypes = [_vp, _vp, C.c_double, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                         C.c_double, C.c_double, C.c_int, _vp, _dp]
+        L.ref_world.argtypes = [C.c_int, C.POINTER(_vp)]
         L.ref_scratch_new.restype = _vp
         L.ref_scratch_free.argtypes = [_vp]
         L.ref_scratch_times.argtypes = [_vp, _dp]
@@ -476,6 +479,36 @@ class RefEngine:
             L.ref_pool_free(self.pool)
         except Exception:
             pass
+
+
+def ref_map_difficulty(ref: Ref, rmap: "RefMap", cfg: dict, threads: int = 0) -> float:
+    """The reference's map_difficulty (evaluation.cpp:25-72) on its own pool."""
+    pool = ref.lib.ref_pool_new(threads)
+    try:
+        out = C.c_double()
+        sh, fl, bs = cfg["lik"]
+        rc = ref.lib.ref_map_difficulty(rmap.h, rmap.field, cfg["thr"], cfg["beams"], cfg["fov"], cfg["max_range"],
+                                        cfg["stride"], cfg["bins"], sh, fl, bs, pool, C.byref(out))
+        if rc != 0:
+            raise RuntimeError(ref.lib.ref_last_error().decode())
+        return out.value
+    finally:
+        ref.lib.ref_pool_free(pool)
+
+
+def ref_world_cells(ref: Ref, which: int):
+    """Occupancy of one of the reference's fixed worlds (worlds.cpp)."""
+    h = _vp()
+    if ref.lib.ref_world(which, C.byref(h)) != 0:
+        raise RuntimeError(ref.lib.ref_last_error().decode())
+    try:
+        w, hh, fc = C.c_int(), C.c_int(), C.c_int()
+        ref.lib.ref_map_dims(h, C.byref(w), C.byref(hh), C.byref(fc))
+        out = np.empty((hh.value, w.value), np.uint8)
+        ref.lib.ref_map_cells(h, _u8(out))
+        return out
+    finally:
+        ref.lib.ref_map_free(h)
 
 
 def ref_write_snapshot(ref: Ref, values, theta_t: float, path: str, cell=0.1):

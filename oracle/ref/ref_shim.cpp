@@ -24,6 +24,8 @@
 #include <vector>
 
 #include "gridloc/belief_tensor.hpp"
+#include "gridloc/evaluation.hpp"
+#include "gridloc/worlds.hpp"
 #include "gridloc/geometry.hpp"
 #include "gridloc/localizer.hpp"
 #include "gridloc/observation.hpp"
@@ -206,6 +208,35 @@ void ref_tensor_get(void* t, double* vals, double* theta_t) {
   auto* bt = static_cast<BeliefTensor*>(t);
   if (vals) std::memcpy(vals, bt->values().data(), bt->size() * sizeof(double));
   if (theta_t) *theta_t = bt->theta_t();
+}
+
+// map_difficulty (evaluation.cpp:25-72) and the fixed synthetic worlds
+int ref_map_difficulty(void* map, void* field, double thr, int beams, double fov, double max_range,
+                       int stride, int bins, double sigma_hit, double weight_floor, int beam_stride,
+                       void* pool, double* out) {
+  return guard([&] {
+    DifficultyConfig c;
+    c.error_threshold = thr;
+    c.beam_count = beams;
+    c.fov = fov;
+    c.max_range = max_range;
+    c.stride = stride;
+    c.theta_bins = bins;
+    c.likelihood = LikelihoodParams{sigma_hit, weight_floor, beam_stride};
+    *out = map_difficulty(*static_cast<OccupancyMap*>(map), static_cast<Field*>(field)->df, c,
+                          *static_cast<ThreadPool*>(pool));
+  });
+}
+int ref_world(int which, void** out) {
+  return guard([&] {
+    switch (which) {
+      case 0: *out = new OccupancyMap(make_twin_room_map()); break;
+      case 1: *out = new OccupancyMap(make_disconnected_twin_rooms()); break;
+      case 2: *out = new OccupancyMap(make_asymmetric_office_map()); break;
+      case 3: *out = new OccupancyMap(make_loop_corridor_map()); break;
+      default: throw std::invalid_argument("no such world");
+    }
+  });
 }
 
 // BLF1 snapshots through the reference's own writer / reader

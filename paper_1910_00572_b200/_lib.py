@@ -48,6 +48,12 @@ class LikelihoodC(C.Structure):
     _fields_ = [("sigma_hit", C.c_double), ("weight_floor", C.c_double), ("beam_stride", C.c_int)]
 
 
+class DifficultyC(C.Structure):
+    _fields_ = [("error_threshold", C.c_double), ("beam_count", C.c_int), ("fov", C.c_double),
+                ("max_range", C.c_double), ("stride", C.c_int), ("theta_bins", C.c_int),
+                ("likelihood", LikelihoodC)]
+
+
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int)
 _u8p = C.POINTER(C.c_uint8)
@@ -65,6 +71,7 @@ SIGNATURES = {
     "gl_context_last_step_ms": [_vp, _dp],
     "gl_context_set_path": [_vp, C.c_int],
     "gl_context_set_fast": [_vp, C.c_int],
+    "gl_context_set_himax": [_vp, C.c_int],
     "gl_context_set_host_exp": [_vp, C.c_int],
     "gl_shard_init_uniform": [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _pvp],
     "gl_shard_info": [_vp, _ip, _ip, _ip, _ip],
@@ -74,6 +81,8 @@ SIGNATURES = {
     "gl_tensor_copy_planes": [_vp, _vp, C.c_int, _vp, C.c_int, C.c_int],
     "gl_write_belief_snapshot": [_vp, _vp, C.c_char_p],
     "gl_read_belief_snapshot": [_vp, C.c_char_p, C.c_double, C.c_double, C.c_double, _pvp],
+    "gl_debug_counters": [_vp, C.POINTER(C.c_uint64)],
+    "gl_map_difficulty": [_vp, _vp, _vp, C.POINTER(DifficultyC), _dp],
     "gl_shard_set_peers": [_vp, _vp, _vp, _vp, C.c_int, _vp, _vp, C.c_int],
     "gl_tensor_buffer_ptr": [_vp, _vp, C.c_int, C.c_int, C.POINTER(_dp)],
     "gl_tensor_current_buffer": [_vp, _ip],
@@ -142,7 +151,12 @@ def load():
             f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
             "(the gridloc_b200 product has no CPU fallback)")
     lib = C.CDLL(LIB_PATH)
+    # a library built from an older tree (GRIDLOC_B200_LIB, tuning
+    # experiments only) may lack newer entry points; the product must not
+    experimental = "GRIDLOC_B200_LIB" in os.environ
     for name, args in SIGNATURES.items():
+        if experimental and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = C.c_int

@@ -440,6 +440,14 @@ gl_status gl_context_set_fast(gl_context* ctx, int enable) {
   });
 }
 
+gl_status gl_context_set_himax(gl_context* ctx, int mode) {
+  return guard([&] {
+    need(ctx, "null context");
+    need(mode >= 0 && mode <= 2, "himax mode must be 0 (auto), 1 (always) or 2 (never)");
+    ctx->himax_mode = mode;
+  });
+}
+
 gl_status gl_context_launch_count(gl_context* ctx, uint64_t* n) {
   return guard([&] {
     need(ctx && n, "null argument");
@@ -1551,6 +1559,192 @@ gl_status gl_observation_update(gl_context* ctx, gl_tensor* t,
     if (read_status(ctx, t) == GL_E_EXTINGUISHED) {
       fail(GL_E_EXTINGUISHED, "observation update zeroed the tensor");
     }
+  });
+}
+
+// diagnostics: [0] step epilogues that took the exact max (HIMAX fallback)
+gl_status gl_debug_counters(gl_context* ctx, unsigned long long* out4) {
+  return guard([&] {
+    need(ctx && out4, "null argument");
+    DeviceGuard g(ctx->device);
+    CK(cudaStreamSynchronize(ctx->stream));
+    glb::fused_counters(out4);
+  });
+}
+
+// -------------------------------------------------------- map difficulty
+gl_status gl_map_difficulty(gl_context* ctx, const gl_map* map, const gl_field* field,
+                            const gl_difficulty_config* cfg, double* out) {
+  return guard([&] {
+    need(ctx && map && field && cfg && out, "null argument");
+    need(field->w == map->w && field->h == map->h, "field and map sizes differ");
+    // simulate_scan / raycast / scan_likelihood argument checks
+    need(cfg->beam_count >= 1, "beam_count must be >= 1");
+    need(cfg->max_range > 0.0, "max_range must be > 0");
+    need(cfg->beam_count <= glb::kMaxDifficultyBeams, "beam_count above 256 is not supported");
+    need(cfg->theta_bins >= 0, "theta_bins must be >= 0");
+    DeviceGuard g(ctx->device);
+    const int W = map->w, H = map->h;
+    const double res = map->res, ox = map->ox, oy = map->oy;
+    const int stride = std::max(1, cfg->stride);
+    std::vector<int> cells;  // (i, j) pairs, evaluation.cpp:28-33 order
+    for (int j = 1; j < H - 1; j += stride)
+      for (int i = 1; i < W - 1; i += stride)
+        if (!map->occ[static_cast<size_t>(j) * W + i]) {
+          cells.push_back(i);
+          cells.push_back(j);
+        }
+    const int n = static_cast<int>(cells.size() / 2);
+    if (n == 0) {
+      *out = 0.0;
+      return;
+    }
+    const int beams = cfg->beam_count, bins = cfg->theta_bins;
+    auto cx_of = [&](int i) { return ox + (i + 0.5) * res; };
+    auto cy_of = [&](int j) { return oy + (j + 0.5) * res; };
+    std::vector<int> winner(n, 0);
+    std::vector<double> ranges;
+    if (bins > 0) {
+      // beam angles (simulator.cpp:75-84) and host-libm direction tables
+      std::vector<double> angles(beams);
+      const bool full_circle = cfg->fov >= 2.0 * M_PI - 1e-9;
+      for (int b = 0; b < beams; ++b) {
+        if (beams == 1) {
+          angles[b] = 0.0;
+        } else if (full_circle) {
+          angles[b] = -M_PI + b * (2.0 * M_PI / beams);
+        } else {
+          angles[b] = -cfg->fov / 2.0 + b * (cfg->fov / (beams - 1));
+        }
+      }
+      std::vector<double> ray(2 * beams), dir(2 * static_cast<size_t>(bins) * beams);
+      for (int b = 0; b < beams; ++b) {
+        const double a = 0.0 + angles[b];  // query pose theta = 0
+        ray[2 * b] = std::cos(a);
+        ray[2 * b + 1] = std::sin(a);
+      }
+      for (int t = 0; t < bins; ++t) {
+        const double ta = wrap_angle(2.0 * M_PI * t / bins);  // evaluation.cpp:37-39
+        for (int b = 0; b < beams; ++b) {
+          const double a = ta + angles[b];
+          dir[2 * (static_cast<size_t>(t) * beams + b)] = std::cos(a);
+          dir[2 * (static_cast<size_t>(t) * beams + b) + 1] = std::sin(a);
+        }
+      }
+      const ObsTables tb = obs_tables(ctx, field, cfg->likelihood);
+      // device buffers (one allocation)
+      size_t off = 0;
+      auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = (off + bytes + 255) & ~size_t(255);
+        return o;
+      };
+      const size_t o_cells = take(sizeof(int) * cells.size()), o_ray = take(sizeof(double) * ray.size()),
+                   o_dir = take(sizeof(double) * dir.size()),
+                   o_rng = take(sizeof(double) * static_cast<size_t>(n) * beams),
+                   o_bls = take(sizeof(double) * n), o_bix = take(sizeof(int) * n), o_cnt = take(sizeof(int) * n),
+                   o_near = take(sizeof(int) * n), o_bad = take(sizeof(int));
+      char* d = nullptr;
+      CK(cudaMalloc(&d, off));
+      std::unique_ptr<char, decltype(&cudaFree)> hold(d, &cudaFree);
+      CK(cudaMemcpyAsync(d + o_cells, cells.data(), sizeof(int) * cells.size(), cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(d + o_ray, ray.data(), sizeof(double) * ray.size(), cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(d + o_dir, dir.data(), sizeof(double) * dir.size(), cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemsetAsync(d + o_near, 0, sizeof(int) * n, ctx->stream));
+      CK(cudaMemsetAsync(d + o_bad, 0, sizeof(int), ctx->stream));
+      glb::DifficultyArgs a{};
+      a.occ = map->d_occ;
+      a.score = tb.d_score;
+      a.oob = tb.oob;
+      a.w = W;
+      a.h = H;
+      a.res = res;
+      a.ox = ox;
+      a.oy = oy;
+      a.cells = reinterpret_cast<const int2*>(d + o_cells);
+      a.n = n;
+      a.ray = reinterpret_cast<const double2*>(d + o_ray);
+      a.dir = reinterpret_cast<const double2*>(d + o_dir);
+      a.beams = beams;
+      a.bins = bins;
+      a.stride = std::max(1, cfg->likelihood.beam_stride);
+      a.max_range = cfg->max_range;
+      a.half_cell = 0.5 * res;
+      a.ranges = reinterpret_cast<double*>(d + o_rng);
+      a.best_ls = reinterpret_cast<double*>(d + o_bls);
+      a.best_idx = reinterpret_cast<int*>(d + o_bix);
+      a.counted = reinterpret_cast<int*>(d + o_cnt);
+      a.near = reinterpret_cast<int*>(d + o_near);
+      a.bad = reinterpret_cast<int*>(d + o_bad);
+      glb::launch_difficulty(ctx, a);
+      CK(cudaGetLastError());
+      ranges.resize(static_cast<size_t>(n) * beams);
+      std::vector<double> bls(n);
+      std::vector<int> bix(n), cnt(n), nearc(n);
+      int bad = 0;
+      CK(cudaMemcpyAsync(ranges.data(), a.ranges, sizeof(double) * ranges.size(), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpyAsync(bls.data(), a.best_ls, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpyAsync(bix.data(), a.best_idx, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpyAsync(cnt.data(), a.counted, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpyAsync(nearc.data(), a.near, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpyAsync(&bad, a.bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      if (bad == 1) fail(GL_E_MAP_PARSE, "raycast origin not in a free cell");
+      if (bad == 2) fail(GL_E_RUNTIME, "map_difficulty: a candidate cell centre is not world-free");
+      // first maximum of exp(log_sum / counted) (observation.cpp:110), in
+      // candidate order with a strict > (evaluation.cpp:51-57)
+      std::vector<double> score_h;
+      for (int q = 0; q < n; ++q) {
+        if (cnt[q] == 0) {  // every likelihood is 1.0: the first candidate wins
+          winner[q] = 0;
+          continue;
+        }
+        int best = bix[q];
+        if (nearc[q] > 0) {
+          // glibc exp may merge log sums just below the maximum: redo this
+          // query's earlier candidates on the host (same FP64 sequence)
+          if (score_h.empty()) {
+            score_h.resize(static_cast<size_t>(W) * H);
+            CK(cudaMemcpy(score_h.data(), tb.d_score, sizeof(double) * score_h.size(), cudaMemcpyDeviceToHost));
+          }
+          std::vector<double> reach;
+          std::vector<int> bidx;
+          for (int b = 0; b < beams; b += a.stride) {
+            const double r = ranges[static_cast<size_t>(q) * beams + b];
+            if (r >= cfg->max_range - 1e-9) continue;
+            bidx.push_back(b);
+            reach.push_back(r + a.half_cell);
+          }
+          const double lbest = std::exp(bls[q] / cnt[q]);
+          for (int idx = 0; idx < bix[q]; ++idx) {
+            const int c = idx / bins, t = idx - c * bins;
+            const double x = cx_of(cells[2 * c]), y = cy_of(cells[2 * c + 1]);
+            double ls = 0.0;
+            for (size_t s = 0; s < bidx.size(); ++s) {
+              const double* cs = &dir[2 * (static_cast<size_t>(t) * beams + bidx[s])];
+              const double ex = x + reach[s] * cs[0];
+              const double ey = y + reach[s] * cs[1];
+              const int ci = static_cast<int>(std::floor((ex - ox) / res));
+              const int cj = static_cast<int>(std::floor((ey - oy) / res));
+              const bool in = ci >= 0 && ci < W && cj >= 0 && cj < H;
+              ls += in ? score_h[static_cast<size_t>(cj) * W + ci] : tb.oob;
+            }
+            if (std::exp(ls / cnt[q]) == lbest) {
+              best = idx;
+              break;
+            }
+          }
+        }
+        winner[q] = best / bins;
+      }
+    }
+    size_t n_wrong = 0;
+    for (int q = 0; q < n; ++q) {
+      const int c = winner[q];
+      const double e = std::hypot(cx_of(cells[2 * c]) - cx_of(cells[2 * q]), cy_of(cells[2 * c + 1]) - cy_of(cells[2 * q + 1]));
+      n_wrong += e > cfg->error_threshold ? 1 : 0;
+    }
+    *out = static_cast<double>(n_wrong) / static_cast<double>(n);
   });
 }
 

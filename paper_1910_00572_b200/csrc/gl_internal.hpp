@@ -35,6 +35,11 @@ struct StepState {
   unsigned long long gmax_bits;
   unsigned int blocks_done;
   int status;  // GL_OK or GL_E_EXTINGUISHED for the latest step
+  // high-word max mode (fused FAST steps): the step kernel tracks only the
+  // high 32 bits of the max; when they cannot decide max >= 1e-6 the last
+  // CTA sets need_exact and the step epilogue kernel takes the exact max
+  int need_exact;
+  int pad;
 };
 
 struct DeviceBlock {  // one allocation per tensor
@@ -49,9 +54,10 @@ struct DeviceBlock {  // one allocation per tensor
 // table in their parameters.
 struct ChanRec {
   double w00, w10, w01, w11;
-  int ox, oy;     // floor(dx), floor(dy), clamped to +-2^29
-  int integral;   // round(dx) == dx && round(dy) == dy
-  int pad;
+  int ox, oy;             // floor(dx), floor(dy), clamped to +-2^29
+  int integral : 8;       // round(dx) == dx && round(dy) == dy
+  int map : 8;            // fused launch: 0 own buffer, 1 / 2 left / right neighbour's
+  int z;                  // fused launch: source plane in that buffer
 };
 void chan_rec(double dx, double dy, ChanRec* r);  // host_math.cpp
 
@@ -71,6 +77,7 @@ struct gl_context {
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   int path = GL_PATH_AUTO;
   bool allow_fast = true;  // use the FAST fused variant on clean buffers
+  int himax_mode = 0;      // high-word step max: 0 auto (large tensors), 1 always, 2 never
   bool host_exp = true;    // likelihood geometric mean: exp by host glibc (exact)
   void* d_kind = nullptr;  // likelihood case codes
   size_t kind_bytes = 0;
@@ -233,6 +240,7 @@ void launch_plane_max(gl_context* ctx, const double* buf, size_t n,
 
 // k_fused.cu
 bool fused_supported(int r, const AngTaps& ang, int c);
+void fused_counters(unsigned long long* out4);  // diagnostics
 void fused_box(int r, int H, int* bw, int* bh);
 void launch_fused_step(gl_context* ctx, const StepArgs& a,
                        const CUtensorMap* tmap, const double* sep, int r,
@@ -240,6 +248,29 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
 // 1 if any value has its sign bit set or is not finite (buffer not "clean")
 void launch_scan_unclean(gl_context* ctx, const double* buf, size_t n,
                          unsigned int* d_flag);
+
+// k_difficulty.cu (map_difficulty, evaluation.cpp:25-72)
+constexpr int kMaxDifficultyBeams = 256;
+struct DifficultyArgs {
+  const uint8_t* occ;
+  const double* score;     // per-cell beam log-score (host libm)
+  double oob;              // log-score of an out-of-grid endpoint
+  int w, h;
+  double res, ox, oy;
+  const int2* cells;       // query == candidate cells, reference order
+  int n;
+  const double2* ray;      // beams: (cos, sin) of the scan beam angles (pose theta 0)
+  const double2* dir;      // bins x beams: (cos, sin) of test_angle + beam angle
+  int beams, bins, stride;
+  double max_range, half_cell;
+  double* ranges;          // n x beams
+  double* best_ls;         // n
+  int* best_idx;           // n
+  int* counted;            // n
+  int* near;               // n (zeroed)
+  int* bad;                // 1 (zeroed)
+};
+void launch_difficulty(gl_context* ctx, const DifficultyArgs& a);
 
 // k_observe.cu
 void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,

@@ -146,7 +146,8 @@ void chan_rec(double dx, double dy, ChanRec* r) {
   r->ox = clamp(fx0);
   r->oy = clamp(fy0);
   r->integral = (std::round(dx) == dx && std::round(dy) == dy) ? 1 : 0;
-  r->pad = 0;
+  r->map = 0;
+  r->z = 0;
 }
 
 // ------------------------------------------------------------------ maps

@@ -46,6 +46,9 @@
 #ifndef GL_FUSED_STCS
 #define GL_FUSED_STCS 1         // 1: output stores with the evict-first (.cs) hint
 #endif
+#ifndef GL_FUSED_HIMAX
+#define GL_FUSED_HIMAX 1        // high-word max + exact epilogue fallback (FAST steps)
+#endif
 #ifndef GL_FUSED_ROWS_H3
 #define GL_FUSED_ROWS_H3 4      // tile rows for H >= 2 (Theta = 360: H = 3)
 #endif
@@ -59,6 +62,11 @@
 namespace glb {
 
 namespace {
+
+// HIMAX decision bound: the high word of 1e-6 (0x3EB0C6F7A0B5ED8D) with a
+// zero low word. A max whose high word exceeds it is > 1e-6 (no rescale, not
+// extinguished); at or below it the exact max is taken.
+constexpr int kHiWord1em6 = 0x3EB0C6F7;
 
 __device__ __forceinline__ double dmax_ref(double a, double b) {
   return (a < b) ? b : a;
@@ -129,10 +137,7 @@ struct FusedParams {
   int plane_off;             // shard: storage plane of iteration 0 (= halo - H)
   int out_off;               // shard: storage plane of output channel 0 (= halo)
   int defer_finalize;        // shard: leave the local max for a cross-rank all-reduce
-  // shard with peers: storage planes s < halo are read from the left
-  // neighbour's buffer (its plane s + lo_add), planes s >= halo + c from the
-  // right neighbour's (plane s - c), through their own tensor maps
-  int peer_read, halo, lo_add;
+
   int tiles_x, n_tiles;
   int k_base, k_end;         // this launch's output channels (a window of <= kParamChannels - 2H)
   int k_chunk, n_chunks;     // output channels per warp, chunks per tile
@@ -239,7 +244,7 @@ __device__ __forceinline__ double row_pass(const FusedParams& p, double s) {
   return dot_seq<2 * R + 1, FAST>(p.sep, nb);
 }
 
-template <int R, int H, int ROWS, int NS, bool FAST>
+template <int R, int H, int ROWS, int NS, bool FAST, bool HIMAX>
 __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
                                             const CUtensorMap* tmap_lo,
                                             const CUtensorMap* tmap_hi,
@@ -255,34 +260,18 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
   const bool scaled = p.src_state->scaled != 0;  // pending 1/max rescale
   const double sc = p.src_state->scale;
 
-  // storage plane of iteration it. One GPU: circular channel m = k0 + it - H
-  // in [-H, C-1+H] (H < C). theta-slab shard: planes are stored with their
-  // neighbours' halo planes, so the walk is linear from plane_off. The shift
-  // record index is linear in both cases.
-  auto chan_of = [&](int it) {
-    if (p.shard) return p.plane_off + k0 + it;
-    const int m = k0 + it - H;
-    return m < 0 ? m + C : (m >= C ? m - C : m);
-  };
+  // Iteration it reads record rec0 + it: the host resolved its source plane
+  // (z) and tensor map (own buffer; circular channel walk on one GPU, linear
+  // over halo storage for a theta-slab shard, or a neighbour's buffer over
+  // peer memory for a shard's halo planes, so no halo exchange step exists).
   const int rec0 = k0 - p.k_base;
   auto issue = [&](int it, int stage) {
-    int kc = chan_of(it);
-    const CUtensorMap* m = tmap;
-    if (p.peer_read) {
-      // theta-slab halo planes come straight from the neighbours' buffers
-      // (peer memory over NVLink): no halo exchange step exists
-      if (kc < p.halo) {
-        m = tmap_lo;
-        kc += p.lo_add;
-      } else if (kc >= p.halo + C) {
-        m = tmap_hi;
-        kc -= C;
-      }
-    }
-    const int2 o = make_int2(p.rec[rec0 + it].ox, p.rec[rec0 + it].oy);
+    const ChanRec& rc = p.rec[rec0 + it];
+    const int map = rc.map;
+    const CUtensorMap* m = map == 0 ? tmap : (map == 1 ? tmap_lo : tmap_hi);
     mbar_arrive_expect(&mbar[stage], G::B_BYTES);
-    tma_load_3d(Bs + stage * G::STAGE, m, (x0 - R - o.x - 1) & ~1,
-                y0 - R - o.y - 1, kc, &mbar[stage]);
+    tma_load_3d(Bs + stage * G::STAGE, m, (x0 - R - rc.ox - 1) & ~1,
+                y0 - R - rc.oy - 1, rc.z, &mbar[stage]);
   };
 
   if (lane == 0) {
@@ -325,6 +314,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
 
   double ring[NG][ROWS];
   double vmax = 0.0;
+  unsigned int hmax = 0u;  // HIMAX: max of the outputs' high words
 
   // One channel: wait for its box, S -> row pass -> column pass -> D_m into
   // ring slot U; with EMIT, output channel k = it - 2H row by row.
@@ -389,7 +379,14 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
           }
           // std::max from 0.0 over free cells (belief_tensor.cpp:464-471);
           // masked cells contribute +0.0, which never raises the max
-          vmax = dmax_ref(vmax, o);
+          if constexpr (HIMAX) {
+            // clean outputs are finite and >= +0.0: their bit patterns order
+            // like their values, so the high word bounds the max (one
+            // integer max instead of DSETP + 2 FSEL per output row)
+            hmax = max(hmax, static_cast<unsigned int>(__double2hiint(o)));
+          } else {
+            vmax = dmax_ref(vmax, o);
+          }
           const bool ok = (store_ok >> r) & 1u;
 #if GL_FUSED_STCS
           if (ok) __stcs(orow, o);  // streaming: the output is not re-read this step
@@ -419,10 +416,11 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
       if (it < n_iter) channel(it, std::integral_constant<int, (2 * H + v) % NG>{}, std::true_type{});
     });
   }
+  if constexpr (HIMAX) vmax = __hiloint2double(static_cast<int>(hmax), 0);
   return vmax;
 }
 
-template <int R, int H, int ROWS, int NS, int NWARP, bool FAST>
+template <int R, int H, int ROWS, int NS, int NWARP, bool FAST, bool HIMAX>
 __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_MINB_H3)
     k_fused_step(const __grid_constant__ CUtensorMap tmap,
                  const __grid_constant__ CUtensorMap tmap_lo,
@@ -461,8 +459,8 @@ __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_
   const int y0 = (tile / p.tiles_x) * ROWS;
   const int k0 = p.k_base + chunk * p.k_chunk;
   const int n_out = min(p.k_chunk, p.k_end - k0);
-  double vmax = warp_tile<R, H, ROWS, NS, FAST>(&tmap, &tmap_lo, &tmap_hi, p, Bs, mbar, lane, x0, y0, k0, n_out,
-                                                active);
+  double vmax = warp_tile<R, H, ROWS, NS, FAST, HIMAX>(&tmap, &tmap_lo, &tmap_hi, p, Bs, mbar, lane, x0, y0, k0,
+                                                       n_out, active);
 
   // global max -> the last CTA finalises status and the pending rescale
 #pragma unroll
@@ -482,6 +480,15 @@ __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_
       __threadfence();
       const unsigned long long bits = atomicAdd(&st->gmax_bits, 0ull);
       const double g = __longlong_as_double(static_cast<long long>(bits));
+      if (HIMAX && g <= __hiloint2double(kHiWord1em6, 0)) {
+        // the high word cannot tell max >= 1e-6 (or > 0): the step epilogue
+        // kernel takes the exact max of the output and finalises
+        st->need_exact = 1;
+      } else if (HIMAX) {
+        st->status = GL_OK;  // max >= 2^-20 > 1e-6: no rescale
+        p.dst_state->scaled = 0;
+        p.dst_state->scale = 1.0;
+      } else {
       st->status = (g <= 0.0) ? GL_E_EXTINGUISHED : GL_OK;
       if (g > 0.0 && g < 1e-6) {
         p.dst_state->scaled = 1;
@@ -490,14 +497,69 @@ __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_
         p.dst_state->scaled = 0;
         p.dst_state->scale = 1.0;
       }
+      }
       st->gmax_bits = 0ull;
       st->blocks_done = 0u;
     }
   }
 }
 
+// HIMAX step epilogue (launched after every HIMAX step, one CTA per SM):
+// when the high-word max could not decide (max <= ~1e-6: the rescale branch,
+// or an extinguished belief — in the cmd_bench stream the rescale fires every
+// ~50 steps) it takes the exact max of the output at full HBM bandwidth with
+// the reference's std::max-from-0.0 rule and the last CTA finalises status and
+// the pending 1/max rescale (belief_tensor.cpp:480-493). Otherwise every CTA
+// exits at once. Every CTA reads the flag before it counts itself, so the last
+// CTA's reset cannot race a late reader.
+__device__ unsigned long long g_fused_counters[4];  // [0] exact HIMAX epilogues run
+
+__global__ void __launch_bounds__(1024) k_himax_epilogue(const double* __restrict__ buf, size_t n,
+                                                         StepState* st, BufState* dst) {
+  __shared__ int need;
+  __shared__ double wm[32];
+  if (threadIdx.x == 0) need = *static_cast<volatile int*>(&st->need_exact);
+  __syncthreads();
+  if (!need) return;
+  double m = 0.0;
+  const double2* b2 = reinterpret_cast<const double2*>(buf);  // n even (TMA needs even W)
+  const size_t n2 = n / 2;
+  for (size_t q = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; q < n2;
+       q += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const double2 v = b2[q];
+    m = dmax_ref(m, v.x);
+    m = dmax_ref(m, v.y);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = dmax_ref(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bm = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) bm = dmax_ref(bm, wm[w]);
+    if (bm > 0.0) atomicMax(&st->gmax_bits, static_cast<unsigned long long>(__double_as_longlong(bm)));
+    __threadfence();
+    if (atomicAdd(&st->blocks_done, 1u) == gridDim.x - 1) {
+      __threadfence();
+      const double g = __longlong_as_double(static_cast<long long>(atomicAdd(&st->gmax_bits, 0ull)));
+      st->status = (g <= 0.0) ? GL_E_EXTINGUISHED : GL_OK;
+      if (g > 0.0 && g < 1e-6) {
+        dst->scaled = 1;
+        dst->scale = 1.0 / g;
+      } else {
+        dst->scaled = 0;
+        dst->scale = 1.0;
+      }
+      st->gmax_bits = 0ull;
+      st->blocks_done = 0u;
+      st->need_exact = 0;
+      atomicAdd(&g_fused_counters[0], 1ull);
+    }
+  }
+}
+
 #ifndef GL_FUSED_NS
-#define GL_FUSED_NS 2
+#define GL_FUSED_NS 3  // measured: 3 stages 0.247-0.256 ms vs 2 stages 0.253-0.261 ms at 1024^2 x 72
 #endif
 constexpr int kNS = GL_FUSED_NS;  // TMA stages per warp
 constexpr int kNWARP = 4;  // warps (independent tiles) per CTA
@@ -513,13 +575,13 @@ constexpr size_t smem_bytes() {
   return 128 + static_cast<size_t>(kNWARP) * kNS * G::STAGE * 8 + kNWARP * kNS * 8 + kNWARP * 8;
 }
 
-template <int R, int H, bool FAST>
+template <int R, int H, bool FAST, bool HIMAX>
 void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& fp) {
   const int n_win = fp.k_end - fp.k_base;
   constexpr int ROWS = rows_for<H>();
   using G = Geo<R, ROWS>;
   constexpr size_t smem = smem_bytes<R, ROWS>();
-  auto kern = k_fused_step<R, H, ROWS, kNS, kNWARP, FAST>;
+  auto kern = k_fused_step<R, H, ROWS, kNS, kNWARP, FAST, HIMAX>;
   static uint64_t configured = 0;  // bit per device: the attribute is per device
   const uint64_t bit = 1ull << (ctx->device & 63);
   if (!(configured & bit)) {
@@ -554,22 +616,24 @@ void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& f
 }
 
 template <int R, int H>
-void launch_rh(gl_context* ctx, const CUtensorMap* const* tmap, FusedParams& fp, bool fast) {
-  if (fast) {
-    launch_rhf<R, H, true>(ctx, tmap, fp);
+void launch_rh(gl_context* ctx, const CUtensorMap* const* tmap, FusedParams& fp, bool fast, bool himax) {
+  if (fast && himax) {
+    launch_rhf<R, H, true, true>(ctx, tmap, fp);
+  } else if (fast) {
+    launch_rhf<R, H, true, false>(ctx, tmap, fp);
   } else {
-    launch_rhf<R, H, false>(ctx, tmap, fp);
+    launch_rhf<R, H, false, false>(ctx, tmap, fp);
   }
 }
 
 template <int R>
 void launch_r(gl_context* ctx, const CUtensorMap* const* tmap, FusedParams& fp, int H,
-              bool fast) {
+              bool fast, bool himax) {
   switch (H) {
-    case 0: launch_rh<R, 0>(ctx, tmap, fp, fast); break;
-    case 1: launch_rh<R, 1>(ctx, tmap, fp, fast); break;
-    case 2: launch_rh<R, 2>(ctx, tmap, fp, fast); break;
-    default: launch_rh<R, 3>(ctx, tmap, fp, fast); break;
+    case 0: launch_rh<R, 0>(ctx, tmap, fp, fast, himax); break;
+    case 1: launch_rh<R, 1>(ctx, tmap, fp, fast, himax); break;
+    case 2: launch_rh<R, 2>(ctx, tmap, fp, fast, himax); break;
+    default: launch_rh<R, 3>(ctx, tmap, fp, fast, himax); break;
   }
 }
 
@@ -597,6 +661,10 @@ void fused_box(int r, int H, int* bw, int* bh) {
   *bh = rows + 2 * r + 1;
 }
 
+void fused_counters(unsigned long long* out4) {
+  cudaMemcpyFromSymbol(out4, g_fused_counters, sizeof(unsigned long long) * 4);
+}
+
 void launch_fused_step(gl_context* ctx, const StepArgs& a,
                        const CUtensorMap* tmap, const double* sep, int r,
                        const AngTaps& ang, bool fast) {
@@ -617,16 +685,25 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
   fp.src_state = a.src_state;
   fp.dst_state = a.dst_state;
   fp.step_state = a.step_state;
-  fp.peer_read = (a.tmap_lo != nullptr && a.tmap_hi != nullptr) ? 1 : 0;
-  fp.halo = a.halo > 0 ? a.halo : 0;
-  fp.lo_add = a.lo_add;
-  const CUtensorMap* maps[3] = {tmap, fp.peer_read ? a.tmap_lo : tmap, fp.peer_read ? a.tmap_hi : tmap};
+  // shard with peers: storage planes s < halo are read from the left
+  // neighbour's buffer (its plane s + lo_add), planes s >= halo + c from the
+  // right neighbour's (plane s - c), through their own tensor maps
+  const bool peer_read = a.tmap_lo != nullptr && a.tmap_hi != nullptr;
+  const int halo = a.halo > 0 ? a.halo : 0;
+  const CUtensorMap* maps[3] = {tmap, peer_read ? a.tmap_lo : tmap, peer_read ? a.tmap_hi : tmap};
   for (int t = 0; t < 2 * r + 1; ++t) fp.sep[t] = sep[t];
   for (int t = 0; t < ang.n; ++t) fp.ang[t] = ang.w[t];
   // The shift records ride in the launch parameters; more than
   // kParamChannels - 2H output channels take several launches over channel
   // windows. Only the last one finalises the max (a shard never does: its
   // max goes to the cross-rank all-reduce first).
+  // high-word max for clean buffers whose step finalises on this device
+  // (a partial theta-shard's max goes to the cross-rank all-reduce exact),
+  // on tensors large enough that the epilogue launch (~3 us) is noise:
+  // measured 4096^2 x 360 25.05 vs 25.78 ms; 1024^2 x 72 0.258 vs 0.255 ms
+  const size_t elems = static_cast<size_t>(a.w) * a.h * a.c;
+  const bool himax = GL_FUSED_HIMAX && fast && (!fp.shard || a.full_shard) &&
+                     (ctx->himax_mode == 1 || (ctx->himax_mode == 0 && elems >= (size_t(1) << 27)));
   const int win = kParamChannels - 2 * H;
   for (int kb = 0; kb < a.c; kb += win) {
     const int ke = std::min(a.c, kb + win);
@@ -637,20 +714,36 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
     for (int q = 0; q < ke - kb + 2 * H; ++q) {
       // h_motion: one (dx, dy) per channel (whole tensor) or per storage
       // plane (shard: plane q <-> channel c_begin - halo + q)
-      int src;
+      int src, z, map = 0;
       if (fp.shard) {
-        src = fp.plane_off + kb + q;
+        src = z = fp.plane_off + kb + q;  // storage plane
+        if (peer_read && z < halo) {
+          map = 1;
+          z += a.lo_add;
+        } else if (peer_read && z >= halo + a.c) {
+          map = 2;
+          z -= a.c;
+        }
       } else {
-        src = kb - H + q;
+        src = kb - H + q;  // circular channel
         src = src < 0 ? src + a.c : (src >= a.c ? src - a.c : src);
+        z = src;
       }
       chan_rec(a.h_motion[2 * src], a.h_motion[2 * src + 1], &fp.rec[q]);
+      fp.rec[q].z = z;
+      fp.rec[q].map = map;
     }
     switch (r) {
-      case 0: launch_r<0>(ctx, maps, fp, H, fast); break;
-      case 1: launch_r<1>(ctx, maps, fp, H, fast); break;
-      default: launch_r<2>(ctx, maps, fp, H, fast); break;
+      case 0: launch_r<0>(ctx, maps, fp, H, fast, himax); break;
+      case 1: launch_r<1>(ctx, maps, fp, H, fast, himax); break;
+      default: launch_r<2>(ctx, maps, fp, H, fast, himax); break;
     }
+  }
+  if (himax) {
+    const size_t plane = static_cast<size_t>(a.w) * a.h;
+    k_himax_epilogue<<<ctx->sm_count > 0 ? ctx->sm_count : 148, 1024, 0, ctx->stream>>>(
+        a.dst + plane * fp.out_off, plane * a.c, a.step_state, a.dst_state);
+    ctx->launches++;
   }
 }
 

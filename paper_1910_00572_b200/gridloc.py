@@ -153,6 +153,10 @@ class Context:
         """FAST fused variant on clean tensors (bitwise-identical results)."""
         check(self.lib.gl_context_set_fast(self.h, int(enable)))
 
+    def set_himax(self, mode: int):
+        """0 auto, 1 always, 2 never: the fused step's high-word max."""
+        check(self.lib.gl_context_set_himax(self.h, int(mode)))
+
     def synchronize(self):
         check(self.lib.gl_context_synchronize(self.h))
 

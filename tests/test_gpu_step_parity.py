@@ -226,3 +226,26 @@ def test_channel_windows_bit_exact(ctx, port):
     _run_pair(ctx, port, occ, 400, (0.03, 0.03, 0.012), motions, GL_PATH_FUSED)
     B0 = random_tensor(occ, 400, seed=4) * 1e-9  # max < 1e-6: deferred rescale
     _run_pair(ctx, port, occ, 400, (0.03, 0.03, 0.012), motions, GL_PATH_FUSED, B0=B0)
+
+
+@pytest.mark.parametrize("himax", [1, 2])
+def test_high_word_max_modes_bit_exact(ctx, port, himax):
+    """The fused FAST kernel's high-word max (forced on small tensors here;
+    automatic on >= 2^27 states) must give the reference's status and
+    pending rescale: decisive steps, the rescale branch (max < 1e-6, taken by
+    the exact full-grid epilogue) and extinguish, every step bit-exact."""
+    occ = make_floorplan(96, 80, seed=2)
+    ctx.set_himax(himax)
+    try:
+        rng = Rng(9)
+        motions = [random_motion(rng) for _ in range(3)] + [(0.1, 0.0, 0.0), (0.0, 0.0, 0.1)]
+        _run_pair(ctx, port, occ, 72, (0.03, 0.03, 0.012), motions, GL_PATH_FUSED)
+        B0 = random_tensor(occ, 72, seed=3) * 1e-9  # rescale every step
+        _run_pair(ctx, port, occ, 72, (0.03, 0.03, 0.012), motions, GL_PATH_FUSED, B0=B0)
+        B0 = random_tensor(occ, 72, seed=4) * 1e-300  # denormal range: hi words near 0
+        _run_pair(ctx, port, occ, 72, (0.03, 0.03, 0.012), motions[:2], GL_PATH_FUSED, B0=B0)
+        occx = np.ones((8, 8), np.uint8)
+        occx[3, 3] = 0
+        _run_pair(ctx, port, occx, 4, (0.001, 0.001, 0.0001), [(0.4, 0.0, 0.0)], GL_PATH_FUSED)
+    finally:
+        ctx.set_himax(0)

@@ -1,4 +1,2 @@
-# A/B of fused-kernel variants, two passes to see box drift
-bash tools/sweep_variants.sh --config c2 > gpurun_out/sweep5a_c2.txt 2>&1; cat gpurun_out/sweep5a_c2.txt
-bash tools/sweep_variants.sh --config c2 > gpurun_out/sweep5b_c2.txt 2>&1; cat gpurun_out/sweep5b_c2.txt
-bash tools/sweep_variants.sh --config c4 --steps 100 > gpurun_out/sweep5_c4.txt 2>&1; cat gpurun_out/sweep5_c4.txt
+python -m pytest tests/test_gpu_difficulty.py tests/test_gpu_step_parity.py -x -q > gpurun_out/gpu_tests_new.log 2>&1; tail -3 gpurun_out/gpu_tests_new.log
+python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; tail -2 gpurun_out/gpu_tests.log
