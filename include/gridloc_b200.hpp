@@ -433,6 +433,31 @@ inline PoseEstimate argmax_state(const BeliefTensor& t) {  // :512-541
   return p;
 }
 
+// evaluation.hpp:21-36: map_difficulty on the device (bit-exact)
+struct DifficultyConfig {
+  double error_threshold = 1.0;
+  int beam_count = 8;
+  double fov = 2.0 * M_PI;
+  double max_range = 8.0;
+  int stride = 1;
+  int theta_bins = 8;
+  LikelihoodParams likelihood{0.2, 0.05, 1};
+};
+inline double map_difficulty(const OccupancyMap& map, const DistanceField& field, const DifficultyConfig& cfg,
+                             ThreadPool& pool) {
+  gl_difficulty_config c;
+  c.error_threshold = cfg.error_threshold;
+  c.beam_count = cfg.beam_count;
+  c.fov = cfg.fov;
+  c.max_range = cfg.max_range;
+  c.stride = cfg.stride;
+  c.theta_bins = cfg.theta_bins;
+  c.likelihood = gl_likelihood{cfg.likelihood.sigma_hit, cfg.likelihood.weight_floor, cfg.likelihood.beam_stride};
+  double out = 0.0;
+  check(gl_map_difficulty(pool.get(), map.handle(), field.handle(), &c, &out));
+  return out;
+}
+
 // belief_tensor.hpp:144-148: BLF1 snapshot (float32 payload, lossy)
 inline void write_belief_snapshot(const BeliefTensor& t, const std::string& path) {
   check(gl_write_belief_snapshot(t.pool().get(), t.get(), path.c_str()));

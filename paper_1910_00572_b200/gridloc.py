@@ -25,7 +25,7 @@ __all__ = [
     "load_map", "init_uniform", "motion_vector", "build_kernels", "make_activation", "step", "step_async",
     "apply_motion", "belief_map", "argmax_state", "dither_samples", "scan_likelihood", "observation_update",
     "distance_field", "wrap_angle", "compose_delta", "Localizer", "LocalizerConfig",
-    "write_belief_snapshot", "read_belief_snapshot",
+    "write_belief_snapshot", "read_belief_snapshot", "DifficultyConfig", "map_difficulty",
     "BeliefExtinguishedError", "MapParseError", "CudaError", "GridlocError",
 ]
 
@@ -551,6 +551,31 @@ def belief_map(tensor: BeliefTensor) -> np.ndarray:
     out = np.empty((tensor.height(), tensor.width()))
     check(tensor.ctx.lib.gl_belief_map(tensor.ctx.h, tensor.h, _d(out)))
     return out
+
+
+@dataclass
+class DifficultyConfig:
+    """evaluation.hpp:21-29."""
+    error_threshold: float = 1.0
+    beam_count: int = 8
+    fov: float = 2.0 * math.pi
+    max_range: float = 8.0
+    stride: int = 1
+    theta_bins: int = 8
+    likelihood: LikelihoodParams = dc_field(default_factory=lambda: LikelihoodParams(0.2, 0.05, 1))
+
+
+def map_difficulty(m: OccupancyMap, f: DistanceField, cfg: DifficultyConfig = None, ctx=None) -> float:
+    """evaluation.cpp:25-72 on the device (bit-exact)."""
+    from ._lib import DifficultyC
+    cfg = cfg or DifficultyConfig()
+    ctx = _ctx(ctx)
+    lk = cfg.likelihood
+    c = DifficultyC(cfg.error_threshold, cfg.beam_count, cfg.fov, cfg.max_range, cfg.stride, cfg.theta_bins,
+                    LikelihoodC(lk.sigma_hit, lk.weight_floor, lk.beam_stride))
+    out = C.c_double()
+    check(ctx.lib.gl_map_difficulty(ctx.h, m.h, f.h, C.byref(c), C.byref(out)))
+    return out.value
 
 
 def write_belief_snapshot(tensor: BeliefTensor, path: str):
