@@ -1002,7 +1002,7 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
       ang.off[q] = kernels->ang_off[q];
       ang.w[q] = kernels->ang_w[q];
     }
-    fused = glb::fused_supported(r, ang, t->c) && (t->halo < 0 || ang.n / 2 <= t->halo);
+    fused = glb::fused_supported(r, r > 0 ? kernels->sep.data() : nullptr, ang, t->c) && (t->halo < 0 || ang.n / 2 <= t->halo);
   }
   const CUtensorMap* tm = nullptr;
   if (fused) {

@@ -239,7 +239,7 @@ void launch_plane_max(gl_context* ctx, const double* buf, size_t n,
                       unsigned long long* d_gmax);
 
 // k_fused.cu
-bool fused_supported(int r, const AngTaps& ang, int c);
+bool fused_supported(int r, const double* sep, const AngTaps& ang, int c);
 void fused_counters(unsigned long long* out4);  // diagnostics
 void fused_box(int r, int H, int* bw, int* bh);
 void launch_fused_step(gl_context* ctx, const StepArgs& a,

@@ -15,10 +15,14 @@
 //   2. Rolling down the rows: S = mask(shift(B)) (2 smem loads per row), the
 //      row pass of the separable Gaussian from S(l-R..l+R) via warp shuffles,
 //      the column pass over a rolling window of row results -> D_m(row).
-//   3. As soon as D_m(row) exists, output channel k = m - H for that row is
-//      out = sum_t w_t * D[k - off_t] (first tap initialises) from a
-//      (2H+1)-slot register ring, masked, times the activation inverse,
-//      stored, max-reduced. Only 2H ring slots stay live across channels.
+//   3. Channels are walked in DESCENDING order, so output channel k's
+//      angular sum out = sum_t w_t * D[k - off_t] receives its terms in the
+//      reference's order (D[k+H] first) as D_m(row) appears: 2H running
+//      sums per row stay live in registers; when D_{k-H}(row) arrives the
+//      sum is finished, masked, times the activation inverse, stored,
+//      max-reduced. Every tap set is symmetric bitwise, so each D value (and
+//      each S and row-pass value) is multiplied by its distinct taps once and
+//      the products are shared (same products, same addition order).
 // The last CTA turns the global max into the extinguish status and the
 // output buffer's pending 1/max rescale (gl_internal.hpp: BufState).
 //
@@ -30,6 +34,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "gl_internal.hpp"
@@ -231,17 +236,34 @@ __device__ __forceinline__ double dot_seq(const double* w, const double* x) {
   return acc;
 }
 
+// Row pass of the separable Gaussian, acc = 0; acc += t[d+R] * S(i+d),
+// d = -R..R (belief_tensor.cpp:211-214). The taps are symmetric bitwise
+// (t[R-d] == t[R+d]: build_kernels evaluates exp(-0.5*d*d/..) at d and -d,
+// and the host checks it), so the product t[R+d] * S(i+d) that lane i needs
+// is the product t[R-|d|] * S(i+d) its neighbour forms for itself: each lane
+// multiplies its S by the R+1 distinct taps once and the shuffles move
+// products instead of S values (R+1 DMUL per S instead of 2R+1; same values,
+// same addition order).
 template <int R, bool FAST>
 __device__ __forceinline__ double row_pass(const FusedParams& p, double s) {
-  // acc = 0; acc += t[d+R] * S(i+d), d = -R..R (belief_tensor.cpp:211-214)
-  double nb[2 * R + 1];
-  nb[R] = s;
+  double q[R + 1];
 #pragma unroll
-  for (int d = 1; d <= R; ++d) {
-    nb[R - d] = __shfl_up_sync(0xffffffffu, s, d);
-    nb[R + d] = __shfl_down_sync(0xffffffffu, s, d);
+  for (int j = 0; j <= R; ++j) q[j] = p.sep[j] * s;
+  double acc = __shfl_up_sync(0xffffffffu, q[0], R);  // d = -R
+  if constexpr (!FAST) acc = 0.0 + acc;
+#pragma unroll
+  for (int d = -R + 1; d <= R; ++d) {
+    double v;
+    if (d < 0) {
+      v = __shfl_up_sync(0xffffffffu, q[R + d], -d);
+    } else if (d == 0) {
+      v = q[R];
+    } else {
+      v = __shfl_down_sync(0xffffffffu, q[R - d], d);
+    }
+    acc += v;
   }
-  return dot_seq<2 * R + 1, FAST>(p.sep, nb);
+  return acc;
 }
 
 template <int R, int H, int ROWS, int NS, bool FAST, bool HIMAX>
@@ -260,13 +282,14 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
   const bool scaled = p.src_state->scaled != 0;  // pending 1/max rescale
   const double sc = p.src_state->scale;
 
-  // Iteration it reads record rec0 + it: the host resolved its source plane
+  // Iteration it reads record rec0 + n_iter - 1 - it (the channel walk is
+  // descending, see channel() below): the host resolved its source plane
   // (z) and tensor map (own buffer; circular channel walk on one GPU, linear
   // over halo storage for a theta-slab shard, or a neighbour's buffer over
   // peer memory for a shard's halo planes, so no halo exchange step exists).
   const int rec0 = k0 - p.k_base;
   auto issue = [&](int it, int stage) {
-    const ChanRec& rc = p.rec[rec0 + it];
+    const ChanRec& rc = p.rec[rec0 + n_iter - 1 - it];  // descending walk
     const int map = rc.map;
     const CUtensorMap* m = map == 0 ? tmap : (map == 1 ? tmap_lo : tmap_hi);
     mbar_arrive_expect(&mbar[stage], G::B_BYTES);
@@ -312,17 +335,28 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
   const double* inv_tile = inv_col + static_cast<size_t>(y0) * W;
   double* const out_tile = p.dst + static_cast<size_t>(y0) * W + (out_lane ? si : 0);
 
-  double ring[NG][ROWS];
+  // Angular accumulators: output channel k's sum lives in slot
+  // (iteration of its last term) % NG; with the channel walk reversed its
+  // terms arrive in the reference's tap order (D[k+H] first).
+  double aacc[NG][ROWS];
   double vmax = 0.0;
   unsigned int hmax = 0u;  // HIMAX: max of the outputs' high words
 
-  // One channel: wait for its box, S -> row pass -> column pass -> D_m into
-  // ring slot U; with EMIT, output channel k = it - 2H row by row.
-  auto channel = [&](const int it, auto Ut, auto Et) {
+  // One channel: wait for its box, S -> row pass -> column pass -> D_m, whose
+  // products with the angular taps go into the output accumulators; with
+  // EMIT, output channel m + H (its last term) is finished row by row.
+  // Channels are walked DOWNWARD (iteration it reads input channel
+  // k0 + n_out - 1 + H - it): output k = sum_t w_t * D[k - (t - H)] adds
+  // D[k+H] first (belief_tensor.cpp:449-463), so a descending walk turns the
+  // angular stencil into running sums whose symmetric taps (w_t == w_{2H-t}
+  // bitwise, host-checked) need H+1 products per D value, not 2H+1.
+  auto channel = [&](const int it, auto Ut, auto Et, auto Pt) {
     constexpr int u = decltype(Ut)::value;
     constexpr bool emit = decltype(Et)::value;
+    constexpr int tmax = decltype(Pt)::value;  // terms t <= tmax exist (prologue)
     const int stage = it % NS;
-    const ChanShift cs = chan_shift(p.rec[rec0 + it]);
+    const int q_in = n_iter - 1 - it;  // relative input channel
+    const ChanShift cs = chan_shift(p.rec[rec0 + q_in]);
     double* stage_ptr = Bs + stage * G::STAGE;
     mbar_wait(&mbar[stage], static_cast<uint32_t>((it / NS) & 1));
     if (scaled) {
@@ -332,10 +366,11 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
       __syncwarp();
     }
     const double* Bb = stage_ptr + ((x0 - R - cs.sx - 1) & 1) + lane;
-    double* orow = out_tile + plane * static_cast<size_t>(p.out_off + k0 + (emit ? it - 2 * H : 0));  // += W per row
+    // emitted output channel k0 + q_in (its last tap reads input q_in = k - H)
+    double* orow = out_tile + plane * static_cast<size_t>(p.out_off + k0 + (emit ? q_in : 0));  // += W per row
 
     double lo_c0 = Bb[1], lo_c1 = Bb[0];
-    double rw[2 * R + 1];  // rolling window of row-pass results
+    double cacc[ROWS];  // column-pass running sums per output row
 #pragma unroll
     for (int lj = 0; lj < G::SH; ++lj) {
       const double hi_c0 = Bb[(lj + 1) * G::BW + 1];
@@ -350,22 +385,56 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
         r = lj;
         d = s;
       } else {
+        // column pass: orow = 0; += t[d] * row(j+d), d = -R..R (:227-238).
+        // Row lj is term t = lj - r of output row r (first for r = lj, last
+        // for r = lj - 2R); symmetric taps: R+1 products per row result.
+        const double x = row_pass<R, FAST>(p, s);
+        double cq[R + 1];
 #pragma unroll
-        for (int q = 0; q < 2 * R; ++q) rw[q] = rw[q + 1];
-        rw[2 * R] = row_pass<R, FAST>(p, s);
+        for (int j = 0; j <= R; ++j) cq[j] = p.sep[j] * x;
+#pragma unroll
+        for (int t = 0; t <= 2 * R; ++t) {
+          const int rr = lj - t;
+          if (rr >= 0 && rr < ROWS) {
+            const double v = cq[t <= R ? t : 2 * R - t];
+            if (t == 0) {
+              if constexpr (FAST) {
+                cacc[rr] = v;
+              } else {
+                cacc[rr] = 0.0 + v;
+              }
+            } else {
+              cacc[rr] += v;
+            }
+          }
+        }
         if (lj >= 2 * R) {
-          // column pass: orow = 0; += t[d] * row(j+d) (:227-238)
           r = lj - 2 * R;
-          d = dot_seq<2 * R + 1, FAST>(p.sep, rw);
+          d = cacc[r];
         }
       }
       if (r >= 0) {
-        ring[u][r] = d;
-        if constexpr (emit) {
-          // angular taps, mask, x inverse, max (belief_tensor.cpp:454-474)
-          double o = p.ang[0] * ring[u][r];
+        // angular taps (belief_tensor.cpp:449-463): D_m is term t of the
+        // output finished 2H - t iterations later, slot (u + 2H - t) % NG
+        double aq[H + 1];
 #pragma unroll
-          for (int t = 1; t < NG; ++t) o += p.ang[t] * ring[(u - t + NG) % NG][r];
+        for (int j = 0; j <= H; ++j) aq[j] = p.ang[j] * d;
+        double o = 0.0;
+#pragma unroll
+        for (int t = 0; t <= 2 * H; ++t) {
+          if (t > tmax) continue;
+          const double v = aq[t <= H ? t : 2 * H - t];
+          const int slot = (u + 2 * H - t) % NG;
+          if (t == 2 * H) {
+            o = (H == 0) ? v : aacc[slot][r] + v;
+          } else if (t == 0) {
+            aacc[slot][r] = v;
+          } else {
+            aacc[slot][r] += v;
+          }
+        }
+        if constexpr (emit) {
+          // mask, x inverse, max (belief_tensor.cpp:464-474)
           double iv;
           if constexpr (INVREG) {
             iv = invr[r];
@@ -406,14 +475,16 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
 
   // channels m = -H .. H-1 only fill the ring (slots 0 .. 2H-1) ...
   static_for<0, 2 * H>([&](auto U) {
-    channel(decltype(U)::value, U, std::false_type{});
+    channel(decltype(U)::value, U, std::false_type{}, U);
   });
   // ... then every channel emits output channel it - 2H; slot = it % NG
   for (int base = 2 * H; base < n_iter; base += NG) {
     static_for<0, NG>([&](auto V) {
       constexpr int v = decltype(V)::value;
       const int it = base + v;
-      if (it < n_iter) channel(it, std::integral_constant<int, (2 * H + v) % NG>{}, std::true_type{});
+      if (it < n_iter)
+        channel(it, std::integral_constant<int, (2 * H + v) % NG>{}, std::true_type{},
+                std::integral_constant<int, 2 * H>{});
     });
   }
   if constexpr (HIMAX) vmax = __hiloint2double(static_cast<int>(hmax), 0);
@@ -643,12 +714,19 @@ void launch_r(gl_context* ctx, const CUtensorMap* const* tmap, FusedParams& fp, 
 // count: separable (isotropic) or impulse spatial kernels with radius <= 2,
 // and angular taps that are exactly offsets -H..H in ascending order (the
 // unfolded build_kernels output, H <= 3) or the degenerate single tap.
-bool fused_supported(int r, const AngTaps& ang, int c) {
+// Both tap sets must be symmetric bit for bit (w[t] == w[n-1-t]; always so
+// for build_kernels output, which evaluates exp(-0.5*d*d/..) at d and -d):
+// the kernel shares each product between the two taps that use it.
+bool fused_supported(int r, const double* sep, const AngTaps& ang, int c) {
   if (r < 0 || r > kFusedMaxRadius) return false;
   if (ang.n < 1 || ang.n > 2 * kFusedMaxHalf + 1 || (ang.n % 2) == 0) return false;
   const int H = ang.n / 2;
   for (int t = 0; t < ang.n; ++t) {
     if (ang.off[t] != t - H) return false;
+    if (std::memcmp(&ang.w[t], &ang.w[ang.n - 1 - t], sizeof(double)) != 0) return false;
+  }
+  for (int t = 0; r > 0 && t < 2 * r + 1; ++t) {
+    if (std::memcmp(&sep[t], &sep[2 * r - t], sizeof(double)) != 0) return false;
   }
   return c >= 1;
 }
