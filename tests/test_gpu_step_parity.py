@@ -249,3 +249,53 @@ def test_high_word_max_modes_bit_exact(ctx, port, himax):
         _run_pair(ctx, port, occx, 4, (0.001, 0.001, 0.0001), [(0.4, 0.0, 0.0)], GL_PATH_FUSED)
     finally:
         ctx.set_himax(0)
+
+
+def _custom_kernels(ctx, port, channels, sep, ang):
+    """The same explicit KernelSet for the GPU and the oracle."""
+    import oracle
+    sep = np.asarray(sep, np.float64)
+    dense = np.outer(sep, sep).ravel()
+    spatial = np.tile(dense, channels)
+    ks = g.KernelSet.from_arrays(1, True, sep, spatial, ang, channels, ctx=ctx)
+    pks = oracle.Kernels(1, True, sep, spatial, [a[0] for a in ang], [a[1] for a in ang])
+    return ks, pks
+
+
+@pytest.mark.parametrize("symmetric", [True, False])
+def test_custom_tap_sets_route_by_symmetry(ctx, port, symmetric):
+    """v10's product sharing needs bitwise-symmetric taps (fused_supported
+    checks it); an asymmetric user KernelSet must fall back to the generic
+    chain and stay bit-exact, and forcing the fused path must fail loudly."""
+    occ = make_floorplan(96, 80, seed=21)
+    C_ = 24
+    if symmetric:
+        sep, ang = [0.25, 0.5, 0.25], [(-1, 0.2), (0, 0.6), (1, 0.2)]
+    else:
+        sep, ang = [0.2, 0.5, 0.3], [(-1, 0.1), (0, 0.6), (1, 0.3)]
+    ks, pks = _custom_kernels(ctx, port, C_, sep, ang)
+    h, w = occ.shape
+    m = g.OccupancyMap(w, h, 0.1, occ, ctx=ctx)
+    act = g.make_activation(m, ks, C_, ctx)
+    cells = m.cells()
+    _, pinv = port.make_activation(cells, pks, C_)
+    rng = Rng(5)
+    motions = [random_motion(rng) for _ in range(4)]
+    for path in (GL_PATH_AUTO, GL_PATH_FUSED):
+        ctx.set_path(path)
+        try:
+            t = g.init_uniform(m, C_, ctx)
+            B = port.init_uniform(cells, C_)
+            th = 0.0
+            for (u, v, w_) in motions:
+                rc, th = port.step(B, th, u, v, w_, cells, 0.1, pks, pinv)
+                assert rc == 0
+                if path == GL_PATH_FUSED and not symmetric:
+                    with pytest.raises(ValueError):
+                        g.step(t, g.OdometryDelta(u, v, w_), m, ks, act, ctx)
+                    break
+                g.step(t, g.OdometryDelta(u, v, w_), m, ks, act, ctx)
+            else:
+                assert_bitwise(t.values(), B, f"custom taps symmetric={symmetric} path={path}")
+        finally:
+            ctx.set_path(GL_PATH_AUTO)
