@@ -21,6 +21,7 @@
 #include <fstream>
 #include <iterator>
 #include <memory>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -83,6 +84,11 @@ inline Pose2 compose(const Pose2& a, const Pose2& b) {
   return Pose2{a.x + c * b.x - s * b.y, a.y + s * b.x + c * b.y, wrap_angle(a.theta + b.theta)};
 }
 inline Pose2 compose(const Pose2& a, const OdometryDelta& d) { return compose(a, Pose2{d.u, d.v, d.w}); }
+inline OdometryDelta relative_delta(const Pose2& a, const Pose2& b) {  // geometry.hpp:44-51
+  const double c = std::cos(a.theta), s = std::sin(a.theta);
+  const double dx = b.x - a.x, dy = b.y - a.y;
+  return OdometryDelta{c * dx + s * dy, -s * dx + c * dy, wrap_angle(b.theta - a.theta)};
+}
 inline OdometryDelta compose_delta(const OdometryDelta& a, const OdometryDelta& b) {
   const double c = std::cos(a.w), s = std::sin(a.w);
   return OdometryDelta{a.u + c * b.u - s * b.v, a.v + s * b.u + c * b.v, a.w + b.w};
@@ -604,5 +610,115 @@ class Localizer {  // localizer.hpp:28-71, localizer.cpp:7-66
   double trigger_rot_;
   int steps_run_ = 0;
 };
+
+// ---------------------------------------------------------- wire formats
+// the recorded-log inputs that feed the device Localizer.
+// Host-side parsing with the reference's record grammar, clamping and
+// exceptions (carmen_log.hpp:20-34, carmen_log.cpp:9-69; observation.hpp,
+// observation.cpp:172-208); oracle/ref/dropin_parity.cpp checks them field by
+// field (bitwise) and byte by byte against the reference.
+struct CarmenEvent {  // carmen_log.hpp:13-18
+  double timestamp = 0.0;
+  Pose2 odom;
+  bool has_scan = false;
+  LidarScan scan;
+};
+
+namespace detail {
+// "FLASER n r_1..r_n lx ly lt ox oy ot ts ..." after the tag; false drops
+// the record (no beams, short or non-numeric fields)
+inline bool carmen_flaser(std::istringstream& in, double fov, double max_range, CarmenEvent* ev) {
+  std::size_t n = 0;
+  in >> n;
+  if (!in || n == 0) return false;
+  ev->has_scan = true;
+  ev->scan.max_range = max_range;
+  ev->scan.ranges.resize(n);
+  ev->scan.angles.resize(n);
+  for (std::size_t b = 0; b < n; ++b) {
+    double& r = ev->scan.ranges[b];
+    if (!(in >> r)) return false;
+    if (r >= max_range) r = max_range;  // no return: the sentinel
+    // beams span [-fov/2, fov/2]; the expression keeps the reference's
+    // operation order (bitwise-equal angles)
+    ev->scan.angles[b] = n > 1 ? -fov / 2.0 + fov * static_cast<double>(b) / (n - 1) : 0.0;
+  }
+  double laser_x, laser_y, laser_t;  // laser pose: the filter tracks the robot frame
+  in >> laser_x >> laser_y >> laser_t;
+  in >> ev->odom.x >> ev->odom.y >> ev->odom.theta >> ev->timestamp;
+  return static_cast<bool>(in);
+}
+
+// "ODOM x y theta tv rv accel ts ..." after the tag
+inline bool carmen_odom(std::istringstream& in, CarmenEvent* ev) {
+  double tv, rv, accel;
+  in >> ev->odom.x >> ev->odom.y >> ev->odom.theta >> tv >> rv >> accel >> ev->timestamp;
+  return static_cast<bool>(in);
+}
+}  // namespace detail
+
+// FLASER and ODOM records in file order; everything else (comments, PARAM,
+// other sensors, malformed records) is skipped.
+inline std::vector<CarmenEvent> read_carmen_log(const std::string& path, double fov = M_PI,
+                                                double max_range = 10.0) {
+  std::ifstream file(path);
+  if (!file) throw std::runtime_error("cannot open carmen log: " + path);
+  std::vector<CarmenEvent> events;
+  for (std::string line; std::getline(file, line);) {
+    if (line.empty() || line.front() == '#') continue;
+    std::istringstream in(line);
+    std::string tag;
+    in >> tag;
+    CarmenEvent ev;
+    const bool keep = tag == "FLASER" ? detail::carmen_flaser(in, fov, max_range, &ev)
+                      : tag == "ODOM" ? detail::carmen_odom(in, &ev)
+                                      : false;
+    if (keep) events.push_back(std::move(ev));
+  }
+  return events;
+}
+
+// Body-frame odometry between consecutive events; the first is zero.
+inline std::vector<OdometryDelta> carmen_odometry_deltas(const std::vector<CarmenEvent>& events) {
+  std::vector<OdometryDelta> out(events.size());
+  for (std::size_t q = 1; q < events.size(); ++q) out[q] = relative_delta(events[q - 1].odom, events[q].odom);
+  return out;
+}
+
+// One line per scan: "t,n,max_range,a_1..a_n,r_1..r_n" with 9 significant
+// digits (observation.cpp:172-183).
+inline void write_scan_csv(const std::string& path, const std::vector<std::pair<double, LidarScan>>& scans) {
+  std::ofstream file(path);
+  if (!file) throw std::runtime_error("cannot open for writing: " + path);
+  file.precision(9);
+  for (const auto& entry : scans) {
+    const LidarScan& sc = entry.second;
+    file << entry.first << "," << sc.angles.size() << "," << sc.max_range;
+    for (double a : sc.angles) file << "," << a;
+    for (double r : sc.ranges) file << "," << r;
+    file << "\n";
+  }
+}
+
+inline std::vector<std::pair<double, LidarScan>> read_scan_csv(const std::string& path) {
+  std::ifstream file(path);
+  if (!file) throw std::runtime_error("cannot open scan csv: " + path);
+  std::vector<std::pair<double, LidarScan>> scans;
+  for (std::string line; std::getline(file, line);) {
+    if (line.empty()) continue;
+    std::vector<double> f;
+    std::istringstream in(line);
+    for (std::string tok; std::getline(in, tok, ',');) f.push_back(std::stod(tok));  // stod throws on junk
+    if (f.size() < 3) throw std::runtime_error("short scan csv line");
+    const auto n = static_cast<std::size_t>(f[1]);
+    if (f.size() != 3 + 2 * n) throw std::runtime_error("scan csv line length mismatch");
+    LidarScan sc;
+    sc.max_range = f[2];
+    sc.angles.assign(f.begin() + 3, f.begin() + 3 + static_cast<std::ptrdiff_t>(n));
+    sc.ranges.assign(f.begin() + 3 + static_cast<std::ptrdiff_t>(n), f.end());
+    scans.emplace_back(f[0], std::move(sc));
+  }
+  return scans;
+}
 
 }  // namespace gridloc_b200

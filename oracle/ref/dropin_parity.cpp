@@ -9,13 +9,24 @@
 //   2. a full Localizer run (reference simulator + trigger logic + sampled
 //      LIDAR observations) with both implementations in lockstep: identical
 //      estimate() poses, belief bit-exact after every blind step, and
-//      relative L1 <= 1e-5 after observations (likelihood exp on the device).
+//      relative L1 <= 1e-5 after observations (likelihood exp on the device);
+//   3. (--io-only runs just this, no GPU needed) the wire formats: CARMEN
+//      logs (hand-written edge cases + a seeded random log) parsed field by
+//      field bitwise-equal, odometry deltas bitwise-equal, scan CSV files
+//      byte-identical and read back bitwise-equal, malformed CSV lines
+//      rejected by both.
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <iterator>
+#include <fstream>
+#include <string>
 #include <vector>
 
 #include "gridloc/belief_tensor.hpp"
+#include "gridloc/carmen_log.hpp"
 #include "gridloc/localizer.hpp"
 #include "gridloc/observation.hpp"
 #include "gridloc/occupancy_map.hpp"
@@ -149,7 +160,155 @@ static void check_localizer(const ref::OccupancyMap& rmap, b2::ThreadPool& pool,
               channels, ticks, steps, observes, worst_l1, pose_mismatch);
 }
 
-int main() {
+
+static bool same_bits(double a, double b) { return std::memcmp(&a, &b, 8) == 0; }
+
+static bool same_bits(const std::vector<double>& a, const std::vector<double>& b) {
+  return a.size() == b.size() && (a.empty() || std::memcmp(a.data(), b.data(), 8 * a.size()) == 0);
+}
+
+static std::string slurp(const std::string& path) {
+  std::ifstream f(path, std::ios::binary);
+  return std::string(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+}
+
+static void check_carmen(const std::string& path, double fov, double max_range) {
+  const auto re = ref::read_carmen_log(path, fov, max_range);
+  const auto be = b2::read_carmen_log(path, fov, max_range);
+  EXPECT(re.size() == be.size(), "%s: %zu vs %zu events", path.c_str(), re.size(), be.size());
+  size_t bad = 0;
+  for (size_t q = 0; q < std::min(re.size(), be.size()); ++q) {
+    const auto& a = re[q];
+    const auto& b = be[q];
+    bad += !(same_bits(a.timestamp, b.timestamp) && same_bits(a.odom.x, b.odom.x) &&
+             same_bits(a.odom.y, b.odom.y) && same_bits(a.odom.theta, b.odom.theta) && a.has_scan == b.has_scan &&
+             same_bits(a.scan.max_range, b.scan.max_range) && same_bits(a.scan.angles, b.scan.angles) &&
+             same_bits(a.scan.ranges, b.scan.ranges));
+  }
+  EXPECT(bad == 0, "%s: %zu events differ", path.c_str(), bad);
+  const auto rd = ref::carmen_odometry_deltas(re);
+  const auto bd = b2::carmen_odometry_deltas(be);
+  size_t dbad = rd.size() != bd.size();
+  for (size_t q = 0; q < std::min(rd.size(), bd.size()); ++q) {
+    dbad += !(same_bits(rd[q].u, bd[q].u) && same_bits(rd[q].v, bd[q].v) && same_bits(rd[q].w, bd[q].w));
+  }
+  EXPECT(dbad == 0, "%s: %zu odometry deltas differ", path.c_str(), dbad);
+  std::printf("{\"carmen\": {\"fov\": %.4f, \"max_range\": %.1f, \"events\": %zu, \"scans\": %zu}}\n", fov,
+              max_range, re.size(),
+              static_cast<size_t>(std::count_if(re.begin(), re.end(), [](const ref::CarmenEvent& e) { return e.has_scan; })));
+}
+
+template <class F>
+static std::string what_of(F&& f) {
+  try {
+    f();
+  } catch (const std::exception& e) {
+    return e.what();
+  }
+  return "<no exception>";
+}
+
+static void check_wire_formats(const std::string& dir) {
+  // CARMEN: the reference test's records plus the grammar's edge cases
+  const std::string hand = dir + "/dropin_hand.log";
+  {
+    std::ofstream out(hand);
+    out << "# comment line\n";
+    out << "PARAM robot_frontlaser_offset 0.08\n";
+    out << "FLASER 4 1.0 2.0 3.0 81.9 0.1 0.2 0.05 0.1 0.2 0.05 1000.1 host 1000.1\n";
+    out << "ODOM 0.5 0.3 0.10 0.2 0.0 0.0 1000.2 host 1000.2\n";
+    out << "\n";
+    out << "FLASER 0 0.1 0.2 0.05 0.1 0.2 0.05 1000.3 host 1000.3\n";        // no beams: dropped
+    out << "FLASER 3 1.0 2.0\n";                                            // truncated ranges: dropped
+    out << "FLASER 2 1.0 2.0 0.1 0.2 0.05 0.1 0.2\n";                        // missing odometry: dropped
+    out << "FLASER 1 12.5 0.0 0.0 0.0 -1.5 2.25 3.1 1000.4 host 1000.4\n";   // one beam, clamped
+    out << "FLASER 3 1e-3 nan 7.5 0 0 0 1 2 -3.0 1000.5\n";                  // exotic numbers
+    out << "ODOM 0.6 0.35\n";                                                // truncated: dropped
+    out << "RLASER 2 1.0 1.0 0 0 0 0 0 0 1000.6\n";                         // other sensor: skipped
+    out << "ODOM 1.0e1 -2.5 6.0 0 0 0 1000.7\n";
+    out << "  ODOM 0.7 0.4 0.2 0 0 0 1000.8 host 1000.8\n";                   // leading blank
+  }
+  check_carmen(hand, M_PI, 10.0);
+  check_carmen(hand, 4.71238898038469, 8.0);
+  // a seeded random log (odometry random walk, 181-beam scans)
+  const std::string rnd = dir + "/dropin_random.log";
+  {
+    ref::Rng rng(20191001);
+    std::ofstream out(rnd);
+    out.precision(17);
+    double x = 0, y = 0, th = 0, t = 1000.0;
+    for (int q = 0; q < 400; ++q) {
+      x += rng.uniform(-0.05, 0.2);
+      y += rng.uniform(-0.05, 0.05);
+      th += rng.uniform(-0.1, 0.1);
+      t += 0.05;
+      if (q % 3 == 0) {
+        out << "FLASER 181";
+        for (int b = 0; b < 181; ++b) out << " " << rng.uniform(0.05, 12.0);
+        out << " " << x << " " << y << " " << th << " " << x << " " << y << " " << th << " " << t << " host " << t
+            << "\n";
+      } else {
+        out << "ODOM " << x << " " << y << " " << th << " 0.3 0.1 0 " << t << " host " << t << "\n";
+      }
+    }
+  }
+  check_carmen(rnd, M_PI, 10.0);
+  EXPECT(what_of([] { ref::read_carmen_log("/nonexistent/x.log"); }) ==
+             what_of([] { b2::read_carmen_log("/nonexistent/x.log"); }),
+         "missing-file errors differ");
+
+  // scan CSV: byte-identical files, bitwise read-back, same rejections
+  std::vector<std::pair<double, ref::LidarScan>> rs;
+  std::vector<std::pair<double, b2::LidarScan>> bs;
+  ref::Rng rng(7);
+  for (int q = 0; q < 50; ++q) {
+    ref::LidarScan sc;
+    sc.max_range = q % 2 ? 8.0 : 30.0;
+    const int n = 1 + q % 37;
+    for (int b = 0; b < n; ++b) {
+      sc.angles.push_back(-M_PI + 2.0 * M_PI * b / n);
+      sc.ranges.push_back(b % 5 == 0 ? sc.max_range : rng.uniform(0.0, sc.max_range));
+    }
+    const double t = 0.05 * q + rng.uniform(0.0, 1e-6);
+    rs.emplace_back(t, sc);
+    bs.emplace_back(t, b2::LidarScan{sc.angles, sc.ranges, sc.max_range});
+  }
+  const std::string rcsv = dir + "/dropin_ref.csv", bcsv = dir + "/dropin_b2.csv";
+  ref::write_scan_csv(rcsv, rs);
+  b2::write_scan_csv(bcsv, bs);
+  const std::string rbytes = slurp(rcsv), bbytes = slurp(bcsv);
+  EXPECT(!rbytes.empty() && rbytes == bbytes, "scan csv files differ (%zu vs %zu bytes)", rbytes.size(),
+         bbytes.size());
+  const auto rb = ref::read_scan_csv(rcsv);
+  const auto bb = b2::read_scan_csv(rcsv);
+  size_t bad = rb.size() != bb.size();
+  for (size_t q = 0; q < std::min(rb.size(), bb.size()); ++q) {
+    bad += !(same_bits(rb[q].first, bb[q].first) && same_bits(rb[q].second.max_range, bb[q].second.max_range) &&
+             same_bits(rb[q].second.angles, bb[q].second.angles) &&
+             same_bits(rb[q].second.ranges, bb[q].second.ranges));
+  }
+  EXPECT(bad == 0, "%zu scan csv records differ", bad);
+  for (const char* line : {"1.0,2\n", "1.0,2,8.0,0.1\n", "1.0,x,8.0\n", "0.5,1,8.0,0.0,1.0\n\n2.0,0,4.0\n"}) {
+    const std::string bad_csv = dir + "/dropin_bad.csv";
+    {
+      std::ofstream out(bad_csv);
+      out << line;
+    }
+    const std::string rw = what_of([&] { ref::read_scan_csv(bad_csv); });
+    const std::string bw = what_of([&] { b2::read_scan_csv(bad_csv); });
+    EXPECT(rw == bw, "scan csv '%s': reference '%s' vs b200 '%s'", line, rw.c_str(), bw.c_str());
+  }
+  std::printf("{\"scan_csv\": {\"scans\": %zu, \"bytes\": %zu}}\n", rb.size(), rbytes.size());
+}
+
+int main(int argc, char** argv) {
+  const char* tmp = std::getenv("TMPDIR");
+  const std::string dir = tmp ? tmp : "/tmp";
+  check_wire_formats(dir);
+  if (argc > 1 && std::strcmp(argv[1], "--io-only") == 0) {
+    std::printf("{\"dropin_parity\": \"%s\", \"failures\": %d}\n", g_fail ? "FAIL" : "ok", g_fail);
+    return g_fail ? 1 : 0;
+  }
   b2::ThreadPool pool(0, 0);
   ref::ThreadPool rpool(4);
   const ref::OccupancyMap office = ref::make_asymmetric_office_map();
