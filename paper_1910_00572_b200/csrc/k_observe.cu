@@ -106,6 +106,131 @@ __device__ __forceinline__ bool fs_spec_groups(const double* pre, double* err,
   return false;
 }
 
+// Software-pipelined form of the 32-pixel speculative groups (the row's main
+// body). Measured on one thread (tools/probe_fs_chain3.cu): the bare
+// DADD->DMUL chain costs 17.2 cycles/pixel, but any instruction that
+// consumes a value the chain JUST produced (a store of it, an integer max of
+// its high word) blocks the in-order issue behind the FP64->store/INT
+// forwarding latency (29.5 cycles/pixel with a store per pixel pair). So
+// group g's screen (max of its high words) and stores are issued during
+// group g+1's chain, from the other register buffer, and group g is
+// verified one group late: on an emission in g, g+1's values are dropped
+// and the caller replays g exactly. Progress (the shared counter + CTA fence
+// of fs_spec_groups) is published every GL_FS_PUBN verified groups.
+// Measured (GL_DEBUG_DITHER, 1024^2): sweep 28.3 M cycles with
+// fs_spec_groups<32> -> 25.2 M (publishing every 2 groups; 25.9 M every
+// group, 26.2 M every 4).
+// Returns true with (q, carry) at the start of the group to replay; false at
+// the row tail (q then points past the last verified group).
+#ifndef GL_FS_PUBN
+#define GL_FS_PUBN 2
+#endif
+template <bool kConstC>
+__device__ __forceinline__ bool fs_spec_pipe(const double* __restrict__ pre, double* __restrict__ err,
+                                             const unsigned int* __restrict__ sup, int& q,
+                                             double& carry, double c_reg, int w,
+                                             volatile int* progress) {
+  constexpr int G = 32;
+  const double c = kConstC ? 7.0 / 16.0 : c_reg;
+  if (q + G > w - 1) return false;
+  double2 pb[2][G / 2];
+  double2 head = *reinterpret_cast<const double2*>(pre + q + 1);
+  int q_p = 0;
+  double carry_p = 0.0;
+  int npub = 0;
+  // masked emission test of the pending group (rare: the unmasked screen
+  // fires whenever error piles up across non-emitting wall cells)
+  auto emits = [&](auto Pt) -> bool {
+    constexpr int P = decltype(Pt)::value;
+    const unsigned long long sw = static_cast<unsigned long long>(sup[q_p >> 5]) |
+                                  (static_cast<unsigned long long>(sup[(q_p >> 5) + 1]) << 32);
+    const unsigned int swq = static_cast<unsigned int>(sw >> (q_p & 31));
+    int ms = 0;
+#pragma unroll
+    for (int k = 0; k < G / 2; ++k) {
+      ms = max(ms, __double2hiint(pb[P][k].x) & -static_cast<int>((swq >> (2 * k)) & 1u));
+      ms = max(ms, __double2hiint(pb[P][k].y) & -static_cast<int>((swq >> (2 * k + 1)) & 1u));
+    }
+    return ms >= 0x3FE00000;
+  };
+  // 0 = continue, 1 = replay (q, carry set), 2 = tail reached
+  auto group = [&](auto Bt, auto Pendt) -> int {
+    constexpr int B = decltype(Bt)::value;
+    constexpr int P = 1 - B;
+    constexpr bool pend = decltype(Pendt)::value;
+    const int qn = q + G;
+    const bool more = qn + G <= w - 1;
+    {
+      const double2* p2 = reinterpret_cast<const double2*>(pre + q + 1);
+      pb[B][0] = head;
+#pragma unroll
+      for (int k = 1; k < G / 2; ++k) pb[B][k] = p2[k];
+      if (more) head = *reinterpret_cast<const double2*>(pre + qn + 1);
+    }
+    double2* ep = reinterpret_cast<double2*>(err + q_p + 1);
+    double cr = carry;
+    int hm = 0;
+#pragma unroll
+    for (int k = 0; k < G / 2; ++k) {
+      const double2 in = pb[B][k];
+      const double v0 = in.x + cr;
+      cr = v0 * c;
+      const double v1 = in.y + cr;
+      cr = v1 * c;
+      pb[B][k] = make_double2(v0, v1);
+      if constexpr (pend) {  // the previous group: long-ready registers, off the chain
+        hm = max(hm, max(__double2hiint(pb[P][k].x), __double2hiint(pb[P][k].y)));
+        ep[k] = pb[P][k];
+      }
+    }
+    if constexpr (pend) {
+      if (__builtin_expect(hm >= 0x3FE00000, 0) && emits(std::integral_constant<int, P>{})) {
+        q = q_p;  // replay the pending group; this group's values are dropped
+        carry = carry_p;
+        return 1;
+      }
+      // the pending group is final; published every GL_FS_PUBN groups (a
+      // CTA fence per group costs more than the helper gains from it)
+      if (++npub == GL_FS_PUBN) {
+        npub = 0;
+        fence_cta();
+        *progress = q;
+      }
+    }
+    q_p = q;
+    carry_p = carry;
+    carry = cr;
+    q = qn;
+    if (more) return 0;
+    // drain: screen and store the last group
+    int hl = 0;
+    double2* el = reinterpret_cast<double2*>(err + q_p + 1);
+#pragma unroll
+    for (int k = 0; k < G / 2; ++k) {
+      hl = max(hl, max(__double2hiint(pb[B][k].x), __double2hiint(pb[B][k].y)));
+      el[k] = pb[B][k];
+    }
+    if (__builtin_expect(hl >= 0x3FE00000, 0) && emits(std::integral_constant<int, B>{})) {
+      q = q_p;
+      carry = carry_p;
+      return 1;
+    }
+    fence_cta();
+    *progress = q;
+    return 2;
+  };
+  // the first group has nothing pending; afterwards every group verifies
+  // and stores its predecessor
+  int r = group(std::integral_constant<int, 0>{}, std::false_type{});
+  if (r) return r == 1;
+  for (;;) {
+    r = group(std::integral_constant<int, 1>{}, std::true_type{});
+    if (r) return r == 1;
+    r = group(std::integral_constant<int, 0>{}, std::true_type{});
+    if (r) return r == 1;
+  }
+}
+
 __device__ long long g_dither_clk[4];  // phase timestamps (debug read-out)
 
 __global__ void __launch_bounds__(64) k_dither_pipe(
@@ -256,9 +381,16 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
       // exactly here, then speculation resumes
       auto sweep = [&](auto gsize) {
         constexpr int G = decltype(gsize)::value;
-        while (c_mid == 7.0 / 16.0
-                   ? fs_spec_groups<G, true>(pre, err, sup, q, carry, c_mid, w, &progress)
-                   : fs_spec_groups<G, false>(pre, err, sup, q, carry, c_mid, w, &progress)) {
+        auto spec = [&]() {
+          if constexpr (G == 32) {
+            return c_mid == 7.0 / 16.0 ? fs_spec_pipe<true>(pre, err, sup, q, carry, c_mid, w, &progress)
+                                       : fs_spec_pipe<false>(pre, err, sup, q, carry, c_mid, w, &progress);
+          } else {
+            return c_mid == 7.0 / 16.0 ? fs_spec_groups<G, true>(pre, err, sup, q, carry, c_mid, w, &progress)
+                                       : fs_spec_groups<G, false>(pre, err, sup, q, carry, c_mid, w, &progress);
+          }
+        };
+        while (spec()) {
 #pragma unroll 1
           for (int k = 0; k < G; ++k) {
             const int qk = q + k;
