@@ -267,13 +267,34 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
   }
   __syncthreads();
   // ---- phase A: total = sequential sum in row-major order (:16-17) -------
+  // The helper warp stages each row's NONZERO values, in order, for the
+  // summing thread: total starts at +0.0 and a sum of finite/inf/NaN terms
+  // from +0.0 is never -0.0, so adding a +-0.0 term never changes it
+  // (x + 0.0 == x for every x except -0.0): skipping zeros (occupied cells)
+  // shortens the dependent DADD chain without changing a bit.
+  __shared__ int ring_cnt[3];
   if (warp == 1) {
     for (int r = 0; r < h; ++r) {
       while (r - consumed >= 3) {
       }
       double* dst = ring + static_cast<size_t>(r % 3) * w;
       const double* src = bm + static_cast<size_t>(r) * w;
-      for (int t = lane; t < w; t += 32) dst[t] = src[t];
+      int n = 0;
+      for (int t0 = 0; t0 < w; t0 += 8 * 32) {
+        double v[8];  // 8 loads in flight per lane, then the in-order compaction
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int t = t0 + 32 * k + lane;
+          v[k] = t < w ? src[t] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const unsigned int nz = __ballot_sync(0xffffffffu, v[k] != 0.0);  // NaN kept, +-0 dropped
+          if (v[k] != 0.0) dst[n + __popc(nz & ((1u << lane) - 1u))] = v[k];
+          n += __popc(nz);
+        }
+      }
+      if (lane == 0) ring_cnt[r % 3] = n;
       __syncwarp();
       fence_cta();
       if (lane == 0) filled = r + 1;
@@ -286,15 +307,16 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
       }
       fence_cta();
       const double* row = ring + static_cast<size_t>(r % 3) * w;
+      const int n = ring_cnt[r % 3];
       int t = 0;
-      for (; t + 16 <= w; t += 16) {
+      for (; t + 16 <= n; t += 16) {
         double x[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) x[k] = row[t + k];
 #pragma unroll
         for (int k = 0; k < 16; ++k) total += x[k];
       }
-      for (; t < w; ++t) total += row[t];
+      for (; t < n; ++t) total += row[t];
       fence_cta();
       consumed = r + 1;
     }

@@ -80,6 +80,25 @@ def test_dither_bit_exact_random_maps(ctx, port):
         assert np.array_equal(s.cells, cells), trial
 
 
+def test_dither_signed_zeros_and_negatives(ctx, port):
+    """The device total skips zero terms (exact: a sum started at +0.0 is
+    never -0.0, and x + (+-0.0) == x otherwise); planes with -0.0, negative
+    and denormal entries, widths around the 256-value staging chunks."""
+    rng = np.random.default_rng(11)
+    for trial, (w, h) in enumerate([(255, 9), (256, 7), (257, 8), (300, 5), (1030, 3), (33, 40)]):
+        bm = rng.random((h, w)) * 2.0
+        z = rng.random((h, w))
+        bm[z < 0.2] = 0.0
+        bm[(z >= 0.2) & (z < 0.3)] = -0.0
+        bm[(z >= 0.3) & (z < 0.35)] *= -1.0
+        bm[(z >= 0.35) & (z < 0.37)] = 5e-324
+        budget = int(rng.integers(1, 400))
+        s = g.dither_samples(bm, budget, ctx)
+        cells, mass = port.dither(bm, budget)
+        assert np.float64(s.source_mass).tobytes() == np.float64(mass).tobytes(), trial
+        assert np.array_equal(s.cells, cells), trial
+
+
 def test_dither_reference_test_cases(ctx):
     """test_observation.cpp:36-101 on the GPU path."""
     gg = np.zeros((14, 14))
