@@ -306,6 +306,8 @@ def run_batch(args, cfg, world, rank, local):
     from paper_1910_00572_b200.floorplan import make_floorplan, write_pgm
     W, H, C, B = cfg["W"], cfg["H"], cfg["C"], cfg["batch"]
     ctxs = [g.Context(local) for _ in range(max(1, B // 8))]
+    for c in ctxs:
+        c.set_channel_chunks(1)  # 8 concurrent streams fill the GPU: no chunk recompute
     robots = []
     for r in range(B):
         ctx = ctxs[r % len(ctxs)]

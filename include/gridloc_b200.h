@@ -73,6 +73,13 @@ gl_status gl_context_set_fast(gl_context* ctx, int enable);
  * max >= 1e-6), 1 = always, 2 = never (exact max in the kernel). Results are
  * bit-identical in every mode. */
 gl_status gl_context_set_himax(gl_context* ctx, int mode);
+/* Channel chunks per fused-step launch: 0 = auto (a tensor whose tiles
+ * cannot fill one wave of resident warps splits its channels, each chunk
+ * recomputing its 2H angular neighbours), n >= 1 = exactly n (capped by the
+ * channel count). Batches of small tensors stepped on concurrent streams
+ * fill the GPU together: 1 avoids the recompute (64 x 512^2 x 72: 248 vs 239
+ * batch-Hz). Results are bit-identical for every setting. */
+gl_status gl_context_set_channel_chunks(gl_context* ctx, int n);
 /* scan_likelihood's final exp (the per-pose geometric mean,
  * observation.cpp:110): 1 (default) evaluates it with the host's libm like the
  * reference (bit-exact; one D2H/H2D of <= 512*Theta doubles per observation),

@@ -448,6 +448,14 @@ gl_status gl_context_set_himax(gl_context* ctx, int mode) {
   });
 }
 
+gl_status gl_context_set_channel_chunks(gl_context* ctx, int n) {
+  return guard([&] {
+    need(ctx, "null context");
+    need(n >= 0, "channel chunks must be >= 0 (0 = auto)");
+    ctx->channel_chunks = n;
+  });
+}
+
 gl_status gl_context_launch_count(gl_context* ctx, uint64_t* n) {
   return guard([&] {
     need(ctx && n, "null argument");

@@ -690,6 +690,7 @@ void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& f
     const char* e = std::getenv("GRIDLOC_B200_CHUNKS");  // tuning experiments only
     return e ? std::atoi(e) : 0;
   }();
+  if (ctx->channel_chunks > 0) fp.n_chunks = std::min(ctx->channel_chunks, n_win);
   if (chunk_override > 0) fp.n_chunks = std::min(chunk_override, n_win);
   fp.k_chunk = (n_win + fp.n_chunks - 1) / fp.n_chunks;
   fp.n_chunks = (n_win + fp.k_chunk - 1) / fp.k_chunk;

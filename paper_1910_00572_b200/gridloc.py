@@ -157,6 +157,11 @@ class Context:
         """0 auto, 1 always, 2 never: the fused step's high-word max."""
         check(self.lib.gl_context_set_himax(self.h, int(mode)))
 
+    def set_channel_chunks(self, n: int):
+        """Fused-step channel chunks: 0 auto, n >= 1 fixed (1 for batches of
+        small tensors on concurrent streams). Bit-identical either way."""
+        check(self.lib.gl_context_set_channel_chunks(self.h, int(n)))
+
     def synchronize(self):
         check(self.lib.gl_context_synchronize(self.h))
 

@@ -228,6 +228,21 @@ def test_channel_windows_bit_exact(ctx, port):
     _run_pair(ctx, port, occ, 400, (0.03, 0.03, 0.012), motions, GL_PATH_FUSED, B0=B0)
 
 
+@pytest.mark.parametrize("chunks", [1, 2, 3, 7])
+@pytest.mark.parametrize("channels", [72, 360])
+def test_explicit_channel_chunks_bit_exact(ctx, port, chunks, channels):
+    """gl_context_set_channel_chunks: any split of the channel walk (each
+    chunk recomputing its 2H angular neighbours) gives the same bits."""
+    occ = make_floorplan(96, 64, seed=8)
+    rng = Rng(chunks * 7 + channels)
+    motions = [random_motion(rng) for _ in range(3)]
+    ctx.set_channel_chunks(chunks)
+    try:
+        _run_pair(ctx, port, occ, channels, (0.03, 0.03, 0.012), motions, GL_PATH_FUSED)
+    finally:
+        ctx.set_channel_chunks(0)
+
+
 @pytest.mark.parametrize("himax", [1, 2])
 def test_high_word_max_modes_bit_exact(ctx, port, himax):
     """The fused FAST kernel's high-word max (forced on small tensors here;
