@@ -226,6 +226,26 @@ gl_status gl_tensor_plane_ptr(gl_context* ctx, gl_tensor* t, int q,
 gl_status gl_tensor_max_ptr(gl_context* ctx, gl_tensor* t,
                             unsigned long long** dptr);
 gl_status gl_shard_finalize(gl_context* ctx, gl_tensor* t);
+/* LIDAR observation on theta-slab shards:
+ *   gl_shard_belief_map      local per-cell max over the shard's channels
+ *                            into a DEVICE plane (W*H doubles)
+ *   all-reduce MAX of that plane (exact) -> the global belief_map
+ *   gl_dither_device         (one rank) Floyd-Steinberg on the device plane
+ *   broadcast n, source mass and the cells to every rank
+ *   gl_shard_observe         likelihoods of ALL c_total channels at the
+ *                            samples (every rank forms the reference's
+ *                            sequential mean identically), the quotient
+ *                            multiply of the shard's own channels, local max
+ *                            into *gl_tensor_max_ptr; n == 0 is a no-op (then
+ *                            skip the rest, like observation.cpp:117)
+ *   all-reduce MAX of *gl_tensor_max_ptr
+ *   gl_shard_observe_finalize  the pending 1/max rescale and the extinguish
+ *                            status (observation.cpp:152-169)
+ *   halo refresh             (exchange mode only; peer reads see it)
+ * Bitwise the unsharded dither_samples + observation_update. */
+gl_status gl_shard_belief_map(gl_context* ctx, gl_tensor* t, double* d_plane);
+/* gl_shard_observe: declared after gl_likelihood, below */
+gl_status gl_shard_observe_finalize(gl_context* ctx, gl_tensor* t);
 /* Halo exchange fused into the step over peer memory (NVLink P2P): with
  * peers set, the step's TMA reads its lower halo input planes straight from
  * the left neighbour's buffer and its upper ones from the right neighbour's
@@ -288,6 +308,11 @@ gl_status gl_dither(gl_context* ctx, const double* belief_map, int width,
                     int height, int budget, int32_t* cells, int cap, int* n,
                     double* source_mass);
 /* dither_samples(belief_map(tensor), budget) without a host round trip. */
+/* dither_samples of a belief map already in device memory (W*H doubles,
+ * enqueued work on the context's stream orders it) */
+gl_status gl_dither_device(gl_context* ctx, const double* d_plane, int width,
+                           int height, int budget, int32_t* cells, int cap, int* n,
+                           double* source_mass);
 gl_status gl_dither_tensor(gl_context* ctx, gl_tensor* t, int budget,
                            int32_t* cells, int cap, int* n,
                            double* source_mass);
@@ -310,6 +335,11 @@ gl_status gl_observation_update(gl_context* ctx, gl_tensor* t,
                                 int n_beams, double max_range,
                                 const gl_map* map, const gl_field* field,
                                 gl_likelihood params);
+/* the theta-slab shard form (sequence: see gl_shard_belief_map above) */
+gl_status gl_shard_observe(gl_context* ctx, gl_tensor* t, const int32_t* cells, int n,
+                           const double* angles, const double* ranges, int n_beams,
+                           double max_range, const gl_map* map, const gl_field* field,
+                           gl_likelihood params);
 
 /* diagnostics: out4[0] = step epilogues that took the exact max */
 gl_status gl_debug_counters(gl_context* ctx, unsigned long long* out4);

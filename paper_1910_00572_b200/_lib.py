@@ -137,6 +137,10 @@ SIGNATURES = {
                            C.c_double, LikelihoodC, _dp],
     "gl_observation_update": [_vp, _vp, _ip, C.c_int, _dp, _dp, C.c_int, C.c_double, _vp, _vp,
                               LikelihoodC],
+    "gl_dither_device": [_vp, _vp, C.c_int, C.c_int, C.c_int, _ip, C.c_int, _ip, _dp],
+    "gl_shard_belief_map": [_vp, _vp, _vp],
+    "gl_shard_observe": [_vp, _vp, _ip, C.c_int, _dp, _dp, C.c_int, C.c_double, _vp, _vp, LikelihoodC],
+    "gl_shard_observe_finalize": [_vp, _vp],
 }
 
 _lib = None

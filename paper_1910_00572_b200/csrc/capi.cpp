@@ -1379,6 +1379,17 @@ gl_status gl_dither(gl_context* ctx, const double* belief_map, int width,
   });
 }
 
+gl_status gl_dither_device(gl_context* ctx, const double* d_plane, int width,
+                           int height, int budget, int32_t* cells, int cap, int* n,
+                           double* source_mass) {
+  return guard([&] {
+    need(ctx && d_plane, "null argument");
+    need(width >= 1 && height >= 1, "bad belief map size");
+    DeviceGuard g(ctx->device);
+    run_dither(ctx, d_plane, width, height, budget, cells, cap, n, source_mass);
+  });
+}
+
 gl_status gl_dither_tensor(gl_context* ctx, gl_tensor* t, int budget,
                            int32_t* cells, int cap, int* n,
                            double* source_mass) {
@@ -1505,20 +1516,22 @@ gl_status gl_scan_likelihood(gl_context* ctx, const gl_map* map,
   });
 }
 
-gl_status gl_observation_update(gl_context* ctx, gl_tensor* t,
-                                const int32_t* cells, int n,
-                                const double* angles, const double* ranges,
-                                int n_beams, double max_range,
-                                const gl_map* map, const gl_field* field,
-                                gl_likelihood params) {
-  return guard([&] {
+// observation_update's device work. shard: likelihoods of ALL c_total
+// channels (every rank forms the same sequential mean), multiply only the
+// shard's own channels, leave the local max in the max slot for the
+// cross-rank all-reduce (gl_shard_observe_finalize finishes).
+static void observe_impl(gl_context* ctx, gl_tensor* t, const int32_t* cells, int n,
+                         const double* angles, const double* ranges, int n_beams,
+                         double max_range, const gl_map* map, const gl_field* field,
+                         gl_likelihood params, bool shard) {
+  {
     need(ctx && t && map && field, "null argument");
     if (n == 0) return;  // observation.cpp:117
     need(cells != nullptr && n > 0, "bad sample set");
     need(n_beams >= 1 && angles && ranges, "scan must have matching, nonempty beams");
     DeviceGuard g(ctx->device);
     const ObsTables tb = obs_tables(ctx, field, params);
-    const int C = t->c;
+    const int C = shard ? t->c_total : t->c;
     // scored beams and per-(channel, beam) directions with host libm
     const int stride = std::max(1, params.beam_stride);
     std::vector<int> scored;
@@ -1560,13 +1573,63 @@ gl_status gl_observation_update(gl_context* ctx, gl_tensor* t,
                             map->res, map->ox, map->oy, t->cell, t->ox, t->oy, d_s,
                             n, C, d_dir, ns, d_reach, params.weight_floor, d_L, d_kind);
     if (ctx->host_exp) finish_likelihoods_on_host(ctx, d_L, d_kind, nL, params.weight_floor);
-    glb::launch_observe_apply(ctx, interior(t), t->w, t->h, C, d_s, n, d_L, d_mean);
+    glb::launch_observe_apply(ctx, interior(t), t->w, t->h, t->c, shard ? t->c_begin : 0, C, d_s, n,
+                              d_L, d_mean);
     glb::launch_plane_max(ctx, interior(t), elems_of(t), &t->d_block->step.gmax_bits);
+    if (shard) {
+      CK(cudaGetLastError());
+      return;
+    }
     glb::launch_observe_finalize(ctx, &t->d_block->step, &t->d_block->buf[t->cur]);
     CK(cudaGetLastError());
     if (read_status(ctx, t) == GL_E_EXTINGUISHED) {
       fail(GL_E_EXTINGUISHED, "observation update zeroed the tensor");
     }
+  }
+}
+
+gl_status gl_observation_update(gl_context* ctx, gl_tensor* t,
+                                const int32_t* cells, int n,
+                                const double* angles, const double* ranges,
+                                int n_beams, double max_range,
+                                const gl_map* map, const gl_field* field,
+                                gl_likelihood params) {
+  return guard([&] {
+    observe_impl(ctx, t, cells, n, angles, ranges, n_beams, max_range, map, field, params, false);
+  });
+}
+
+gl_status gl_shard_observe(gl_context* ctx, gl_tensor* t, const int32_t* cells, int n,
+                           const double* angles, const double* ranges, int n_beams,
+                           double max_range, const gl_map* map, const gl_field* field,
+                           gl_likelihood params) {
+  return guard([&] {
+    need(t && t->halo >= 0, "not a sharded tensor");
+    observe_impl(ctx, t, cells, n, angles, ranges, n_beams, max_range, map, field, params, true);
+  });
+}
+
+gl_status gl_shard_observe_finalize(gl_context* ctx, gl_tensor* t) {
+  return guard([&] {
+    need(ctx && t, "null argument");
+    need(t->halo >= 0, "not a sharded tensor");
+    DeviceGuard g(ctx->device);
+    glb::launch_observe_finalize(ctx, &t->d_block->step, &t->d_block->buf[t->cur]);
+    CK(cudaGetLastError());
+    if (read_status(ctx, t) == GL_E_EXTINGUISHED) {
+      fail(GL_E_EXTINGUISHED, "observation update zeroed the tensor");
+    }
+  });
+}
+
+gl_status gl_shard_belief_map(gl_context* ctx, gl_tensor* t, double* d_plane) {
+  return guard([&] {
+    need(ctx && t && d_plane, "null argument");
+    need(t->halo >= 0, "not a sharded tensor");
+    DeviceGuard g(ctx->device);
+    materialize(ctx, t);
+    glb::launch_belief_map(ctx, interior(t), t->w, t->h, t->c, d_plane);
+    CK(cudaGetLastError());
   });
 }
 

@@ -283,9 +283,9 @@ void launch_likelihoods(gl_context* ctx, const uint8_t* occ, const double* score
                         const double2* d_dir, int n_scored,
                         const double* d_reach, double floor_w, double* d_L,
                         uint8_t* d_kind);
-void launch_observe_apply(gl_context* ctx, double* buf, int w, int h, int c,
-                          const int* d_samples, int n, const double* d_L,
-                          double* d_mean);
+void launch_observe_apply(gl_context* ctx, double* buf, int w, int h, int c_local,
+                          int k_off, int c_total, const int* d_samples, int n,
+                          const double* d_L, double* d_mean);
 void launch_observe_finalize(gl_context* ctx, StepState* st, BufState* buf);
 
 }  // namespace glb

@@ -649,16 +649,18 @@ __global__ void k_mean(const double* __restrict__ L, int total,
 }
 
 // B[i,j,k] *= L / mean, quotient first (observation.cpp:145-150).
-__global__ void k_observe_apply(double* __restrict__ B, int w, int h, int c,
-                                const int* __restrict__ samples, int n,
+__global__ void k_observe_apply(double* __restrict__ B, int w, int h, int c_local,
+                                int k_off, int c_total, const int* __restrict__ samples, int n,
                                 const double* __restrict__ L,
                                 const double* __restrict__ mean) {
+  // (sample, local channel) pairs; a theta-slab shard holds global channels
+  // k_off .. k_off + c_local - 1 of c_total, L is indexed s * c_total + k
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= n * c) return;
-  const int s = q / c, k = q % c;
-  const size_t p = static_cast<size_t>(k) * w * h +
+  if (q >= n * c_local) return;
+  const int s = q / c_local, kl = q % c_local;
+  const size_t p = static_cast<size_t>(kl) * w * h +
                    static_cast<size_t>(samples[2 * s + 1]) * w + samples[2 * s];
-  B[p] *= L[q] / *mean;
+  B[p] *= L[static_cast<size_t>(s) * c_total + k_off + kl] / *mean;
 }
 
 // Global max -> status + the buffer's pending 1/max rescale
@@ -714,13 +716,13 @@ void launch_likelihoods(gl_context* ctx, const uint8_t* occ, const double* score
   ctx->launches++;
 }
 
-void launch_observe_apply(gl_context* ctx, double* buf, int w, int h, int c,
-                          const int* d_samples, int n, const double* d_L,
-                          double* d_mean) {
-  k_mean<<<1, 1, 0, ctx->stream>>>(d_L, n * c, d_mean);
-  const int total = n * c;
+void launch_observe_apply(gl_context* ctx, double* buf, int w, int h, int c_local,
+                          int k_off, int c_total, const int* d_samples, int n,
+                          const double* d_L, double* d_mean) {
+  k_mean<<<1, 1, 0, ctx->stream>>>(d_L, n * c_total, d_mean);
+  const int total = n * c_local;
   k_observe_apply<<<(total + 127) / 128, 128, 0, ctx->stream>>>(
-      buf, w, h, c, d_samples, n, d_L, d_mean);
+      buf, w, h, c_local, k_off, c_total, d_samples, n, d_L, d_mean);
   ctx->launches += 2;
 }
 

@@ -129,6 +129,44 @@ def exchange_planes(dist, planes, plan: HaloPlan, group=None):
         w.wait()
 
 
+def observe_collectives(dist, group, rank: int, world: int, root: int, plane, max_bits, local_map, dither,
+                        apply, finalize):
+    """The collective skeleton of a sharded observation,
+    device work injected as callables so the host logic runs under gloo too:
+      local_map(plane)       this rank's per-cell max into `plane` (float64)
+      dither(plane) -> (cells int32 (n, 2), mass)   called on `root` only
+      apply(cells, n)        likelihoods over all channels, own channels
+                             multiplied, local max into `max_bits`
+      finalize()             the 1/max rescale and status
+    Returns (cells, mass), identical on every rank."""
+    import numpy as np
+    import torch
+    local_map(plane)
+    if world > 1:
+        dist.all_reduce(plane, op=dist.ReduceOp.MAX, group=group)
+    hdr = torch.zeros(2, dtype=torch.float64, device=plane.device)  # n, source mass
+    cells = None
+    if rank == root:
+        cells, mass = dither(plane)
+        hdr[0], hdr[1] = float(len(cells)), float(mass)
+    if world > 1:
+        dist.broadcast(hdr, src=root, group=group)
+    n, mass = int(hdr[0].item()), float(hdr[1].item())
+    buf = torch.zeros(max(2 * n, 2), dtype=torch.int32, device=plane.device)
+    if rank == root and n:
+        buf[: 2 * n] = torch.from_numpy(np.ascontiguousarray(cells, dtype=np.int32).reshape(-1)).to(plane.device)
+    if world > 1:
+        dist.broadcast(buf, src=root, group=group)
+    cells = np.ascontiguousarray(buf[: 2 * n].cpu().numpy(), dtype=np.int32).reshape(-1, 2)
+    if n == 0:  # observation.cpp:117: an empty sample set is a no-op
+        return cells, mass
+    apply(cells, n)
+    if world > 1:
+        dist.all_reduce(max_bits, op=dist.ReduceOp.MAX, group=group)
+    finalize()
+    return cells, mass
+
+
 class _CAI:
     """Zero-copy device view for torch.as_tensor(..., device='cuda')."""
 
@@ -241,6 +279,48 @@ class ThetaShard:
     def status(self):
         from .gridloc import tensor_status
         tensor_status(self.t)
+
+    def observe(self, scan, field, params=None, budget: int = 512, root: int = 0):
+        """Sharded Localizer::observe (localizer.cpp:48-59): the global
+        belief_map as a MAX all-reduce of the shards' local maps, dither on
+        `root`, the samples broadcast, every rank's likelihoods over all
+        channels (identical sequential mean), its own channels multiplied,
+        the max all-reduced and the 1/max rescale finalised
+        (observe_collectives). Returns the SampleSet (same on every rank)."""
+        import numpy as np
+        from .gridloc import LikelihoodParams, SampleSet, _d, _i, _lp
+        torch, lib, ctx = self.torch, self.ctx.lib, self.ctx
+        params = params or LikelihoodParams()
+        W, H = self.map.width(), self.map.height()
+        cap = max(1, min(W * H, 4 * max(budget, 1) + 64))
+        a = np.ascontiguousarray(scan.angles, dtype=np.float64)
+        r = np.ascontiguousarray(scan.ranges, dtype=np.float64)
+
+        def local_map(plane):
+            check(lib.gl_shard_belief_map(ctx.h, self.t.h, C.c_void_p(plane.data_ptr())))
+
+        def dither(plane):
+            cells = np.zeros(2 * cap, np.int32)
+            n, mass = C.c_int(), C.c_double()
+            check(lib.gl_dither_device(ctx.h, C.c_void_p(plane.data_ptr()), W, H, budget, _i(cells), cap,
+                                       C.byref(n), C.byref(mass)))
+            return cells[: 2 * n.value].reshape(-1, 2), mass.value
+
+        def apply(cells, n):
+            flat = np.ascontiguousarray(cells, dtype=np.int32).reshape(-1)
+            check(lib.gl_shard_observe(ctx.h, self.t.h, _i(flat), n, _d(a), _d(r), a.size, scan.max_range,
+                                       self.map.h, field.h, _lp(params)))
+
+        def finalize():
+            check(lib.gl_shard_observe_finalize(ctx.h, self.t.h))
+            if self.exchange == "nccl":
+                self.exchange_halos()
+
+        with torch.cuda.stream(self.stream):
+            plane = torch.empty(W * H, dtype=torch.float64, device=f"cuda:{ctx.device}")
+            cells, mass = observe_collectives(self.dist, self.group, self.rank, self.world, root, plane,
+                                              self._max_tensor(), local_map, dither, apply, finalize)
+        return SampleSet(cells.copy(), mass)
 
     def argmax(self):
         """Global argmax_state: local candidate, all-gather, lowest-index rule."""

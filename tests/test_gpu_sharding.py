@@ -146,3 +146,133 @@ def _cai_f64(ptr, n):
         __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3,
                                     "strides": None, "stream": None}
     return _V()
+
+
+def _emulate_max_allreduce(ctx, shards):
+    import torch
+    dev = [torch.as_tensor(_cai(C.cast(_max_bits(ctx, t), C.c_void_p).value), device="cuda") for t in shards]
+    gmax = torch.stack(dev).max()
+    for d in dev:
+        d.copy_(gmax.reshape(1))
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("G,c_total", [(2, 72), (3, 36), (4, 72)])
+def test_sharded_observation_bitwise_equal_unsharded(ctx, G, c_total):
+    """SURVEY §8(e) LIDAR path on G shards of one belief (one device standing
+    in for G ranks): local belief maps max-reduced -> dither on the reduced
+    device plane -> the same samples everywhere -> every shard's likelihoods
+    over all channels, own channels multiplied, max all-reduced, 1/max
+    finalised. Samples, source mass and the tensor (incl. the pending
+    rescale, seen through a following step) bitwise the unsharded path."""
+    import torch
+    from paper_1910_00572_b200.floorplan import simple_scan
+    occ = make_floorplan(128, 96, seed=31)
+    m = g.OccupancyMap(128, 96, 0.1, occ, ctx=ctx)
+    f = g.DistanceField(m, ctx)
+    ks = g.build_kernels(g.MotionNoise(), c_total, 0.1, 2 * math.pi / c_total)
+    act = g.make_activation(m, ks, c_total, ctx)
+    halo = max(len(ks.angular) // 2, 1)
+    full = g.init_uniform(m, c_total, ctx)
+    shards = [_shard(ctx, m, c_total, *partition(c_total, G, r), halo) for r in range(G)]
+    plans = [halo_plan(c_total, G, r, halo) for r in range(G)]
+
+    def exchange():
+        for r, t in enumerate(shards):
+            pl = plans[r]
+            left, right = shards[pl.left], shards[pl.right]
+            lp, rp = plans[pl.left], plans[pl.right]
+            check(ctx.lib.gl_tensor_copy_planes(ctx.h, t.h, pl.recv_left[0], left.h, lp.send_right[0], halo))
+            check(ctx.lib.gl_tensor_copy_planes(ctx.h, t.h, pl.recv_right[0], right.h, rp.send_left[0], halo))
+        ctx.synchronize()
+
+    def step_all(u, v, w):
+        g.step(full, g.OdometryDelta(u, v, w), m, ks, act, ctx)
+        for t in shards:
+            g.step_async(t, g.OdometryDelta(u, v, w), m, ks, act, ctx)
+        ctx.synchronize()
+        _emulate_max_allreduce(ctx, shards)
+        for t in shards:
+            check(ctx.lib.gl_shard_finalize(ctx.h, t.h))
+        exchange()
+
+    rng = Rng(G + c_total)
+    for _ in range(4):
+        step_all(*random_motion(rng))
+    js, is_ = np.nonzero(occ == 0)
+    q = len(is_) // 3
+    a, r = simple_scan(occ, is_[q] * 0.1 + 0.05, js[q] * 0.1 + 0.05, 0.4)
+    scan = g.LidarScan(a, r, 8.0)
+    params = g.LikelihoodParams()
+    for obs in range(2):
+        ref_s = g.dither_samples(full, 512)
+        g.observation_update(full, ref_s, scan, m, f, params)
+        planes = []
+        for t in shards:
+            pl = torch.empty(128 * 96, dtype=torch.float64, device="cuda")
+            check(ctx.lib.gl_shard_belief_map(ctx.h, t.h, C.c_void_p(pl.data_ptr())))
+            planes.append(pl)
+        ctx.synchronize()
+        red = torch.stack(planes).max(dim=0).values.contiguous()
+        torch.cuda.synchronize()
+        cap = 4 * 512 + 64
+        cells = np.zeros(2 * cap, np.int32)
+        n, mass = C.c_int(), C.c_double()
+        check(ctx.lib.gl_dither_device(ctx.h, C.c_void_p(red.data_ptr()), 128, 96, 512,
+                                       cells.ctypes.data_as(C.POINTER(C.c_int)), cap, C.byref(n), C.byref(mass)))
+        cells = cells[: 2 * n.value]
+        assert np.array_equal(cells.reshape(-1, 2), ref_s.cells), f"obs {obs}: samples differ"
+        assert np.float64(mass.value).tobytes() == np.float64(ref_s.source_mass).tobytes()
+        assert n.value > 0
+        aa = np.ascontiguousarray(a, dtype=np.float64)
+        rr = np.ascontiguousarray(r, dtype=np.float64)
+        dp = C.POINTER(C.c_double)
+        for t in shards:
+            check(ctx.lib.gl_shard_observe(ctx.h, t.h, cells.ctypes.data_as(C.POINTER(C.c_int)), n.value,
+                                           aa.ctypes.data_as(dp), rr.ctypes.data_as(dp), aa.size, 8.0, m.h, f.h,
+                                           g.gridloc._lp(params)))
+        ctx.synchronize()
+        _emulate_max_allreduce(ctx, shards)
+        for t in shards:
+            check(ctx.lib.gl_shard_observe_finalize(ctx.h, t.h))
+        exchange()
+        if obs == 0:  # download materialises the pending 1/max rescale ...
+            got = np.concatenate([t.values() for t in shards], axis=0)
+            assert_bitwise(got, full.values(), f"G={G} observation {obs}")
+        step_all(0.1, 0.0, 0.0)  # ... else the next step's kernel applies it
+        got = np.concatenate([t.values() for t in shards], axis=0)
+        assert_bitwise(got, full.values(), f"G={G} step after observation {obs}")
+
+
+@pytest.mark.parametrize("exchange", ["peer", "nccl"])
+def test_theta_shard_observe_world1(ctx, exchange):
+    """ThetaShard.observe (the sharded Localizer::observe glue over
+    observe_collectives) at world size 1: samples and tensor bitwise the
+    unsharded dither_samples + observation_update, then a step."""
+    from paper_1910_00572_b200.floorplan import simple_scan
+    from paper_1910_00572_b200.sharding import ThetaShard
+    occ = make_floorplan(96, 64, seed=5)
+    m = g.OccupancyMap(96, 64, 0.1, occ, ctx=ctx)
+    f = g.DistanceField(m, ctx)
+    C_ = 72
+    ks = g.build_kernels(g.MotionNoise(), C_, 0.1, 2 * math.pi / C_)
+    act = g.make_activation(m, ks, C_, ctx)
+    full = g.init_uniform(m, C_, ctx)
+    sh = ThetaShard(m, C_, 1, 0, 1, ctx, exchange=exchange)
+    try:
+        rng = Rng(9)
+        js, is_ = np.nonzero(occ == 0)
+        a, r = simple_scan(occ, is_[10] * 0.1 + 0.05, js[10] * 0.1 + 0.05, 0.2)
+        scan = g.LidarScan(a, r, 8.0)
+        for it in range(3):
+            u = g.OdometryDelta(*random_motion(rng))
+            g.step(full, u, m, ks, act, ctx)
+            sh.step(u, ks, act)
+            ref_s = g.dither_samples(full, 256)
+            g.observation_update(full, ref_s, scan, m, f)
+            s = sh.observe(scan, f, budget=256)
+            assert np.array_equal(s.cells, ref_s.cells) and s.source_mass == ref_s.source_mass
+            ctx.synchronize()
+            assert_bitwise(sh.t.values(), full.values(), f"{exchange} observe {it}")
+    finally:
+        sh.close()

@@ -122,3 +122,70 @@ def test_peer_plan_reads_the_channels_the_halo_holds(world, c_total, halo):
             q = s - n
             assert halo <= q < halo + pp.hi_count
             assert (rc0 - halo + q) % c_total == (c0 - halo + s) % c_total
+
+
+def _obs_worker(rank, world, port, q, empty):
+    from paper_1910_00572_b200.sharding import observe_collectives
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(rank)
+        mine = rng.random(PLANE)                      # this rank's local belief map
+        calls = {"dither": 0, "apply": None, "finalize": 0}
+        plane = torch.zeros(PLANE, dtype=torch.float64)
+        max_bits = torch.from_numpy(np.array([0.0], np.float64).view(np.int64).copy())
+
+        def local_map(p):
+            p.copy_(torch.from_numpy(mine))
+
+        def dither(p):
+            calls["dither"] += 1
+            if empty:
+                return np.zeros((0, 2), np.int32), 0.0
+            v = p.numpy()
+            idx = np.argsort(-v)[:3]                   # deterministic "samples" from the reduced map
+            return np.stack([idx, idx + 100], axis=1).astype(np.int32), float(v.sum())
+
+        def apply(cells, n):
+            calls["apply"] = (cells.copy(), n)
+            max_bits.copy_(torch.from_numpy(np.array([0.5 + rank], np.float64).view(np.int64)))
+
+        def finalize():
+            calls["finalize"] += 1
+
+        cells, mass = observe_collectives(dist, None, rank, world, 0, plane, max_bits, local_map, dither, apply,
+                                          finalize)
+        gmax = float(max_bits.numpy().view(np.float64)[0])
+        q.put((rank, plane.numpy().copy(), cells, mass, calls["dither"], calls["apply"], calls["finalize"], gmax))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,empty", [(2, False), (3, False), (2, True)])
+def test_observation_collectives(world, empty):
+    """Sharded observation skeleton: the belief map is the elementwise MAX
+    of the ranks' local maps, only the root dithers, every rank gets the
+    root's samples and mass, the step max is MAX-reduced before finalize,
+    and an empty sample set skips apply/finalize everywhere."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_obs_worker, args=(r, world, port, q, empty)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = np.max([np.random.default_rng(r).random(PLANE) for r in range(world)], axis=0)
+    root_cells, root_mass = res[0][2], res[0][3]
+    for rank, plane, cells, mass, nd, applied, nfin, gmax in res:
+        assert np.array_equal(plane, want)
+        assert np.array_equal(cells, root_cells) and mass == root_mass
+        assert nd == (1 if rank == 0 else 0)
+        if empty:
+            assert len(cells) == 0 and applied is None and nfin == 0
+        else:
+            assert len(cells) == 3 and np.array_equal(applied[0], root_cells) and applied[1] == 3
+            assert nfin == 1 and gmax == 0.5 + (world - 1)
