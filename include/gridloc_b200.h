@@ -2,7 +2,7 @@
  * gridloc_b200 — C-ABI of the B200-native belief-tensor filter.
  *
  * Drop-in boundary for the reference `gridloc` C++ library's hot path
- * (/root/reference/proj/include/gridloc/*.hpp). The reference has no FFI; its
+ * (/root/reference/proj/include/gridloc/ *.hpp). The reference has no FFI; its
  * boundary is the C++ API, so each entry point below names the reference
  * function it replaces (file:line). `include/gridloc_b200.hpp` re-exposes the
  * same calls with the reference's C++ signatures, and INTEGRATION.md shows the

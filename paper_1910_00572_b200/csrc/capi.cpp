@@ -157,19 +157,6 @@ void* ensure_misc(gl_context* ctx, size_t bytes) {
   return ctx->d_misc;
 }
 
-void* ensure_host_misc(gl_context* ctx, size_t bytes) {
-  if (ctx->h_misc_bytes < bytes) {
-    if (ctx->h_misc) {
-      CK(cudaStreamSynchronize(ctx->stream));
-      CK(cudaFreeHost(ctx->h_misc));
-    }
-    ctx->h_misc = nullptr;
-    CK(cudaMallocHost(&ctx->h_misc, bytes));
-    ctx->h_misc_bytes = bytes;
-  }
-  return ctx->h_misc;
-}
-
 void ensure_scratch(gl_context* ctx, size_t elems) {
   if (ctx->scratch_elems < elems) {
     CK(cudaStreamSynchronize(ctx->stream));

@@ -279,7 +279,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
                                             bool active, double* invs) {
   using G = Geo<R, ROWS>;
   constexpr int NG = 2 * H + 1;  // ring depth == angular taps
-  const int W = p.w, Hh = p.h, C = p.c;
+  const int W = p.w, Hh = p.h;
   const size_t plane = static_cast<size_t>(W) * Hh;
   const int n_iter = n_out + 2 * H;  // this warp's output channels k0 .. k0+n_out-1
   const bool scaled = p.src_state->scaled != 0;  // pending 1/max rescale
@@ -338,7 +338,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
     if constexpr (INVSM) invs[r * 32 + lane] = ok ? __ldg(inv_col + static_cast<size_t>(y0 + r) * W) : 0.0;
   }
   if constexpr (INVSM) __syncwarp();
-  const double* inv_tile = inv_col + static_cast<size_t>(y0) * W;
+  [[maybe_unused]] const double* inv_tile = inv_col + static_cast<size_t>(y0) * W;
   double* const out_tile = p.dst + static_cast<size_t>(y0) * W + (out_lane ? si : 0);
 
   // Angular accumulators: output channel k's sum lives in slot
@@ -376,7 +376,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
     double* orow = out_tile + plane * static_cast<size_t>(p.out_off + k0 + (emit ? q_in : 0));  // += W per row
 
     double lo_c0 = Bb[1], lo_c1 = Bb[0];
-    double cacc[ROWS];  // column-pass running sums per output row
+    [[maybe_unused]] double cacc[ROWS];  // column-pass running sums per output row (R > 0)
 #pragma unroll
     for (int lj = 0; lj < G::SH; ++lj) {
       const double hi_c0 = Bb[(lj + 1) * G::BW + 1];
