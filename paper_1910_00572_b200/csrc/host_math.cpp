@@ -185,17 +185,24 @@ struct Cursor {
 
 }  // namespace
 
-// load_map (occupancy_map.cpp:148-165) with decode_pgm (:84-145) and the
-// OccupancyMap boundary ring (:32-40).
+// load_map (occupancy_map.cpp:148-165) with decode_pgm (:84-145) or
+// decode_png_gray8 (png_decode.cpp) and the OccupancyMap boundary ring
+// (:32-40).
 MapParse parse_pgm_map(const uint8_t* bytes, size_t n, int threshold) {
   if (threshold <= 0 || threshold >= 255) {
     throw std::invalid_argument("threshold must be in (0, 255)");
   }
   MapParse m;
   auto fail = [](const char* why) { return MapParseFailure(why); };
-  if (n >= 8 && bytes[0] == 0x89 && bytes[1] == 'P' && bytes[2] == 'N' &&
-      bytes[3] == 'G') {
-    throw fail("PNG maps are not supported by gridloc_b200 (convert to PGM)");
+  if (looks_like_png(bytes, n)) {  // occupancy_map.cpp:154-156
+    int pw = 0, ph = 0;
+    const std::vector<uint8_t> gray = decode_png_gray8(bytes, n, &pw, &ph);
+    m.w = pw;
+    m.h = ph;
+    m.occ.resize(gray.size());
+    for (size_t q = 0; q < gray.size(); ++q) m.occ[q] = gray[q] >= threshold ? 0 : 1;
+    force_ring(m.occ.data(), m.w, m.h);
+    return m;
   }
   if (n < 2 || bytes[0] != 'P' || (bytes[1] != '2' && bytes[1] != '5')) {
     throw fail("not a P2/P5 PGM (bad magic)");

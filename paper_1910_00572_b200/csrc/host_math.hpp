@@ -36,6 +36,9 @@ HostKernels build_kernels_host(double sigma_x, double sigma_y,
 void motion_table(double u, double v, int c_begin, int count, double theta_t,
                   double dtheta, double cell, double* out_xy);
 MapParse parse_pgm_map(const uint8_t* bytes, size_t n, int threshold);
+// png_decode.cpp: image_png.cpp:32-100 without libpng
+bool looks_like_png(const uint8_t* bytes, size_t n);
+std::vector<uint8_t> decode_png_gray8(const uint8_t* bytes, size_t n, int* width, int* height);
 void force_ring(uint8_t* occ, int w, int h);
 std::vector<double> distance_field_host(const uint8_t* occ, int w, int h,
                                         double res);
