@@ -58,7 +58,11 @@ gl_status gl_context_destroy(gl_context* ctx);
 gl_status gl_context_synchronize(gl_context* ctx);
 /* Device-time of the last gl_step (ms), measured with CUDA events on the
  * context stream: the fused kernel has no phase boundaries, so the total is
- * reported as t_motion and t_diffusion = t_masking = 0. */
+ * reported as t_motion and t_diffusion = t_masking = 0.
+ * Off by default (two event records cost ~5 us of host time per step);
+ * gl_context_set_step_timing(ctx, 1) turns it on (the C++ ThreadPool does,
+ * to fill StepScratch like the reference). */
+gl_status gl_context_set_step_timing(gl_context* ctx, int enable);
 gl_status gl_context_last_step_ms(gl_context* ctx, double* ms);
 /* Path selection (GL_PATH_AUTO = fused when the kernel set allows it). */
 enum { GL_PATH_AUTO = 0, GL_PATH_FUSED = 1, GL_PATH_GENERIC = 2 };

@@ -136,6 +136,7 @@ class ThreadPool {
     gl_context* c = nullptr;
     check(gl_context_create(device, &c));
     ctx_.reset(c, [](gl_context* p) { gl_context_destroy(p); });
+    check(gl_context_set_step_timing(c, 1));  // StepScratch::t_motion, as the reference fills it
   }
   int thread_count() const { return 1; }
   gl_context* get() const { return ctx_.get(); }

@@ -69,6 +69,7 @@ SIGNATURES = {
     "gl_context_destroy": [_vp],
     "gl_context_synchronize": [_vp],
     "gl_context_last_step_ms": [_vp, _dp],
+    "gl_context_set_step_timing": [_vp, C.c_int],
     "gl_context_set_path": [_vp, C.c_int],
     "gl_context_set_fast": [_vp, C.c_int],
     "gl_context_set_himax": [_vp, C.c_int],

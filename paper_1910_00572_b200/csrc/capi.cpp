@@ -302,6 +302,8 @@ gl_status gl_context_create(int device, gl_context** out) {
     CK(cudaEventCreate(&ctx->ev_end));
     for (auto& e : ctx->ring_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CK(cudaMallocHost(&ctx->h_block, sizeof(glb::DeviceBlock)));
+    CK(cudaHostAlloc(&ctx->h_status, sizeof(int), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->d_status), ctx->h_status, 0));
     *out = ctx.release();
   });
 }
@@ -316,6 +318,7 @@ gl_status gl_context_destroy(gl_context* ctx) {
     if (ctx->d_motion) cudaFree(ctx->d_motion);
     if (ctx->h_motion) cudaFreeHost(ctx->h_motion);
     if (ctx->h_block) cudaFreeHost(ctx->h_block);
+    if (ctx->h_status) cudaFreeHost(ctx->h_status);
     if (ctx->d_misc) cudaFree(ctx->d_misc);
     if (ctx->h_misc) cudaFreeHost(ctx->h_misc);
     if (ctx->d_kind) cudaFree(ctx->d_kind);
@@ -337,10 +340,19 @@ gl_status gl_context_synchronize(gl_context* ctx) {
   });
 }
 
+gl_status gl_context_set_step_timing(gl_context* ctx, int enable) {
+  return guard([&] {
+    need(ctx, "null context");
+    ctx->step_events = enable != 0;
+    if (!ctx->step_events) ctx->ev_begin_last = ctx->ev_end_last = nullptr;
+  });
+}
+
 gl_status gl_context_last_step_ms(gl_context* ctx, double* ms) {
   return guard([&] {
     need(ctx && ms, "null argument");
-    need(ctx->ev_end_last != nullptr, "no step has run on this context");
+    need(ctx->ev_end_last != nullptr,
+         "no timed step on this context (enable gl_context_set_step_timing before stepping)");
     CK(cudaEventSynchronize(ctx->ev_end_last));
     float f = 0.f;
     CK(cudaEventElapsedTime(&f, ctx->ev_begin_last, ctx->ev_end_last));
@@ -960,7 +972,7 @@ gl_status gl_tensor_device_ptr(gl_context* ctx, gl_tensor* t, double** dptr) {
 // ----------------------------------------------------------------- step
 static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
                          double w, const gl_map* map, const gl_kernels* kernels,
-                         const gl_activation* act) {
+                         const gl_activation* act, bool publish = false) {
   need(ctx && t && map && kernels && act, "null argument");
   need(map->w == t->w && map->h == t->h, "map and tensor sizes differ");
   need(act->w == t->w && act->h == t->h && act->channels == t->c_total,
@@ -978,6 +990,7 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
   a.src_state = &t->d_block->buf[src];
   a.dst_state = &t->d_block->buf[dst];
   a.step_state = &t->d_block->step;
+  a.host_status = publish ? ctx->d_status : nullptr;
   a.occ = map->d_occ;
   a.inv = act->d_inverse;
   a.inv_masked = act->d_inverse_masked;
@@ -1043,8 +1056,12 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
   } else {
     a.motion = upload_motion(ctx, t, u, v);
   }
+  // per-step device time: cudaEventRecord costs ~2.6 us of host time each
+  // (measured, tools/probe_launch_params.cu), so the begin/end pair is only
+  // recorded when asked for (gl_context_set_step_timing, gl_context_time_steps)
   const int tslot = (ctx->timing && ctx->tcount < gl_context::kTimers) ? ctx->tcount++ : -1;
-  CK(cudaEventRecord(tslot >= 0 ? ctx->tev[2 * tslot] : ctx->ev_begin, ctx->stream));
+  const bool events = tslot >= 0 || ctx->step_events;
+  if (events) CK(cudaEventRecord(tslot >= 0 ? ctx->tev[2 * tslot] : ctx->ev_begin, ctx->stream));
   if (fused) {
     // r == 0 (impulse) kernels have no separable taps; the fused variant
     // then skips the spatial passes entirely
@@ -1072,13 +1089,15 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
     glb::launch_step_finalize(ctx, a);
   }
   CK(cudaGetLastError());
-  CK(cudaEventRecord(tslot >= 0 ? ctx->tev[2 * tslot + 1] : ctx->ev_end, ctx->stream));
-  if (tslot >= 0) {
-    ctx->ev_begin_last = ctx->tev[2 * tslot];
-    ctx->ev_end_last = ctx->tev[2 * tslot + 1];
-  } else {
-    ctx->ev_begin_last = ctx->ev_begin;
-    ctx->ev_end_last = ctx->ev_end;
+  if (events) {
+    CK(cudaEventRecord(tslot >= 0 ? ctx->tev[2 * tslot + 1] : ctx->ev_end, ctx->stream));
+    if (tslot >= 0) {
+      ctx->ev_begin_last = ctx->tev[2 * tslot];
+      ctx->ev_end_last = ctx->tev[2 * tslot + 1];
+    } else {
+      ctx->ev_begin_last = ctx->ev_begin;
+      ctx->ev_end_last = ctx->ev_end;
+    }
   }
   t->clean[dst] = t->clean[src];  // clean in -> clean out (non-negative weights)
   t->cur = dst;
@@ -1088,10 +1107,26 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
 gl_status gl_step(gl_context* ctx, gl_tensor* t, double u, double v, double w,
                   const gl_map* map, const gl_kernels* kernels,
                   const gl_activation* act) {
-  gl_status st = guard([&] { enqueue_step(ctx, t, u, v, w, map, kernels, act); });
+  // The finalising kernel also writes the status into the context's mapped
+  // pinned word, so the synchronous call is enqueue + stream sync (a
+  // device-to-host copy of the step state costs ~8 us more per step at
+  // 256^2; tools/e2e_probe.py). A partial theta shard's status is only final
+  // after gl_shard_finalize: it keeps the copy.
+  const bool mapped = ctx && t && ctx->h_status && (t->halo < 0 || t->c == t->c_total);
+  gl_status st = guard([&] {
+    if (mapped) *reinterpret_cast<volatile int*>(ctx->h_status) = -1;  // not yet published
+    enqueue_step(ctx, t, u, v, w, map, kernels, act, mapped);
+  });
   if (st != GL_OK) return st;
   st = guard([&] {
-    if (read_status(ctx, t) == GL_E_EXTINGUISHED) {
+    gl_status s = GL_E_RUNTIME;
+    if (mapped) {
+      DeviceGuard g(ctx->device);
+      CK(cudaStreamSynchronize(ctx->stream));
+      s = static_cast<gl_status>(*reinterpret_cast<volatile int*>(ctx->h_status));
+    }
+    if (!mapped || (s != GL_OK && s != GL_E_EXTINGUISHED)) s = read_status(ctx, t);
+    if (s == GL_E_EXTINGUISHED) {
       fail(GL_E_EXTINGUISHED, "belief tensor extinguished: no positive mass after step");
     }
   });

@@ -42,6 +42,14 @@ struct StepState {
   int pad;
 };
 
+// Every step-finalising kernel publishes the status through this; `host` is
+// the launching context's mapped pinned status word for a synchronous
+// gl_step (it then needs no device-to-host copy), else null.
+__device__ __forceinline__ void publish_status(StepState* st, int s, int* host) {
+  st->status = s;
+  if (host) *reinterpret_cast<volatile int*>(host) = s;
+}
+
 struct DeviceBlock {  // one allocation per tensor
   BufState buf[2];
   StepState step;
@@ -96,6 +104,8 @@ struct gl_context {
   int ring_next = 0;
   // pinned scalars for status read-back
   glb::DeviceBlock* h_block = nullptr;
+  int* h_status = nullptr;  // mapped pinned status word (host view) ...
+  int* d_status = nullptr;  // ... and its device address
   // misc device scratch for reductions / dither
   void* d_misc = nullptr;
   size_t misc_bytes = 0;
@@ -104,6 +114,7 @@ struct gl_context {
   // optional per-launch step timing (event pairs)
   static constexpr int kTimers = 8192;
   bool timing = false;
+  bool step_events = false;  // begin/end events around every step (t_motion)
   std::vector<cudaEvent_t> tev;  // 2 * kTimers
   int tcount = 0;
   cudaEvent_t ev_begin_last = nullptr, ev_end_last = nullptr;
@@ -204,6 +215,7 @@ struct StepArgs {
   const CUtensorMap* tmap_lo = nullptr;  // left neighbour's source buffer
   const CUtensorMap* tmap_hi = nullptr;  // right neighbour's source buffer
   int lo_add = 0;                        // left neighbour's interior channel count
+  int* host_status = nullptr;            // mapped status word (synchronous gl_step)
 };
 
 // k_generic.cu

@@ -152,6 +152,7 @@ struct FusedParams {
   const BufState* src_state;
   BufState* dst_state;
   StepState* step_state;
+  int* host_status;          // mapped status word of a synchronous gl_step, or null
   double sep[2 * kFusedMaxRadius + 1];
   double ang[2 * kFusedMaxHalf + 1];
   // the step's shift records (host) for the window's input planes: output
@@ -565,11 +566,11 @@ __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_
         // kernel takes the exact max of the output and finalises
         st->need_exact = 1;
       } else if (HIMAX) {
-        st->status = GL_OK;  // max >= 2^-20 > 1e-6: no rescale
+        publish_status(st, GL_OK, p.host_status);  // max >= 2^-20 > 1e-6: no rescale
         p.dst_state->scaled = 0;
         p.dst_state->scale = 1.0;
       } else {
-      st->status = (g <= 0.0) ? GL_E_EXTINGUISHED : GL_OK;
+      publish_status(st, (g <= 0.0) ? GL_E_EXTINGUISHED : GL_OK, p.host_status);
       if (g > 0.0 && g < 1e-6) {
         p.dst_state->scaled = 1;
         p.dst_state->scale = 1.0 / g;
@@ -595,7 +596,8 @@ __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_
 __device__ unsigned long long g_fused_counters[4];  // [0] exact HIMAX epilogues run
 
 __global__ void __launch_bounds__(1024) k_himax_epilogue(const double* __restrict__ buf, size_t n,
-                                                         StepState* st, BufState* dst) {
+                                                         StepState* st, BufState* dst,
+                                                         int* host_status) {
   __shared__ int need;
   __shared__ double wm[32];
   if (threadIdx.x == 0) need = *static_cast<volatile int*>(&st->need_exact);
@@ -622,7 +624,7 @@ __global__ void __launch_bounds__(1024) k_himax_epilogue(const double* __restric
     if (atomicAdd(&st->blocks_done, 1u) == gridDim.x - 1) {
       __threadfence();
       const double g = __longlong_as_double(static_cast<long long>(atomicAdd(&st->gmax_bits, 0ull)));
-      st->status = (g <= 0.0) ? GL_E_EXTINGUISHED : GL_OK;
+      publish_status(st, (g <= 0.0) ? GL_E_EXTINGUISHED : GL_OK, host_status);
       if (g > 0.0 && g < 1e-6) {
         dst->scaled = 1;
         dst->scale = 1.0 / g;
@@ -759,8 +761,9 @@ void fused_counters(unsigned long long* out4) {
 void launch_fused_step(gl_context* ctx, const StepArgs& a,
                        const CUtensorMap* tmap, const double* sep, int r,
                        const AngTaps& ang, bool fast) {
-  static thread_local FusedParams fp;  // ~19 KB: keep it off the stack
-  fp = FusedParams{};
+  // ~19 KB: kept off the stack and not re-zeroed per step (every field the
+  // kernel reads is assigned below; unused record slots are never read)
+  static thread_local FusedParams fp;
   const int H = ang.n / 2;
   fp.dst = a.dst;
   fp.occ = a.occ;
@@ -776,6 +779,7 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
   fp.src_state = a.src_state;
   fp.dst_state = a.dst_state;
   fp.step_state = a.step_state;
+  fp.host_status = a.host_status;
   // shard with peers: storage planes s < halo are read from the left
   // neighbour's buffer (its plane s + lo_add), planes s >= halo + c from the
   // right neighbour's (plane s - c), through their own tensor maps
@@ -833,7 +837,7 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
   if (himax) {
     const size_t plane = static_cast<size_t>(a.w) * a.h;
     k_himax_epilogue<<<ctx->sm_count > 0 ? ctx->sm_count : 148, 1024, 0, ctx->stream>>>(
-        a.dst + plane * fp.out_off, plane * a.c, a.step_state, a.dst_state);
+        a.dst + plane * fp.out_off, plane * a.c, a.step_state, a.dst_state, a.host_status);
     ctx->launches++;
   }
 }

@@ -216,9 +216,9 @@ __global__ void k_angular(const double* __restrict__ D, double* __restrict__ out
 
 // Turn the step's running max into the status and the output buffer's
 // pending rescale (belief_tensor.cpp:480-493); reset the accumulator.
-__global__ void k_step_finalize(StepState* st, BufState* dst) {
+__global__ void k_step_finalize(StepState* st, BufState* dst, int* host_status) {
   const double g = __longlong_as_double(static_cast<long long>(st->gmax_bits));
-  st->status = (g <= 0.0) ? GL_E_EXTINGUISHED : GL_OK;
+  publish_status(st, (g <= 0.0) ? GL_E_EXTINGUISHED : GL_OK, host_status);
   if (g > 0.0 && g < 1e-6) {
     dst->scaled = 1;
     dst->scale = 1.0 / g;
@@ -467,7 +467,7 @@ void launch_angular(gl_context* ctx, const StepArgs& a, const double* D,
 }
 
 void launch_step_finalize(gl_context* ctx, const StepArgs& a) {
-  k_step_finalize<<<1, 1, 0, ctx->stream>>>(a.step_state, a.dst_state);
+  k_step_finalize<<<1, 1, 0, ctx->stream>>>(a.step_state, a.dst_state, a.host_status);
   ctx->launches++;
 }
 

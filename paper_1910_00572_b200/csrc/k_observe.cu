@@ -667,7 +667,7 @@ __global__ void k_observe_apply(double* __restrict__ B, int w, int h, int c_loca
 // (observation.cpp:152-169).
 __global__ void k_observe_finalize(StepState* st, BufState* buf) {
   const double g = __longlong_as_double(static_cast<long long>(st->gmax_bits));
-  st->status = (g <= 0.0) ? GL_E_EXTINGUISHED : GL_OK;
+  publish_status(st, (g <= 0.0) ? GL_E_EXTINGUISHED : GL_OK, nullptr);
   if (g > 0.0) {
     buf->scaled = 1;
     buf->scale = 1.0 / g;

@@ -165,6 +165,11 @@ class Context:
     def synchronize(self):
         check(self.lib.gl_context_synchronize(self.h))
 
+    def set_step_timing(self, enable: bool):
+        """CUDA events around every step for last_step_ms() (off by default:
+        ~5 us of host time per step)."""
+        check(self.lib.gl_context_set_step_timing(self.h, int(enable)))
+
     def last_step_ms(self) -> float:
         ms = C.c_double()
         check(self.lib.gl_context_last_step_ms(self.h, C.byref(ms)))
