@@ -509,8 +509,9 @@ def run_ours(args, cfg, world, rank, local):
                    "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (one per GPU)",
                    "l2": "belief tensor (604 MB at 1024^2x72) exceeds the 126 MB L2: every step streams it from HBM",
                    "noise": [0.03, 0.03, 0.012], "kernel_path": "fused sm_100a TMA step"},
-        "e2e": {"value": e2e, "unit": "Hz", "h2d_bytes_per_step": 16 * C, "d2h_bytes_per_step": 16,
-                "how": f"{n_e2e} synchronous gl_step calls (motion table H2D in the launch, status D2H), wall clock"},
+        "e2e": {"value": e2e, "unit": "Hz", "h2d_bytes_per_step": 16 * C, "d2h_bytes_per_step": 4,
+                "how": f"{n_e2e} synchronous gl_step calls (motion table H2D in the launch params, the step's "
+                       f"status written by the finalising kernel into mapped pinned host memory), wall clock"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(args.config), "peak_source": peak_src,
                      "bytes_per_launch": bytes_launch, "avg_kernel_ms": avg_kern_s * 1e3, "launches_timed": kern_n},
