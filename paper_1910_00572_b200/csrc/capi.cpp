@@ -1012,12 +1012,14 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
     }
     fused = glb::fused_supported(r, r > 0 ? kernels->sep.data() : nullptr, ang, t->c) && (t->halo < 0 || ang.n / 2 <= t->halo);
   }
+  // TMA descriptor over the source buffer; none for a row pitch TMA cannot
+  // stride (odd W: 8*W is not a multiple of 16), where the fused kernel
+  // loads its boxes with cp.async instead
   const CUtensorMap* tm = nullptr;
   if (fused) {
     int bw = 0, bh = 0;
     glb::fused_box(r, ang.n / 2, &bw, &bh);
     tm = tensor_tmap(t, src, bw, bh);
-    fused = tm != nullptr;
   }
   if (ctx->path == GL_PATH_FUSED && !fused) {
     fail(GL_E_INVALID, "fused path requested but unsupported for this kernel set/grid");
@@ -1041,11 +1043,15 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
     a.halo = t->halo;
     a.full_shard = t->c == t->c_total;
     if (fused && t->peer_lo_buf[src] != nullptr) {
-      int bw = 0, bh = 0;
-      glb::fused_box(r, ang.n / 2, &bw, &bh);
-      a.tmap_lo = tensor_tmap_at(t, t->peer_lo_buf[src], t->peer_lo_count + 2 * t->halo, bw, bh);
-      a.tmap_hi = tensor_tmap_at(t, t->peer_hi_buf[src], t->peer_hi_count + 2 * t->halo, bw, bh);
-      if (a.tmap_lo == nullptr || a.tmap_hi == nullptr) fail(GL_E_CUDA, "tensor map over a peer buffer failed");
+      if (tm != nullptr) {
+        int bw = 0, bh = 0;
+        glb::fused_box(r, ang.n / 2, &bw, &bh);
+        a.tmap_lo = tensor_tmap_at(t, t->peer_lo_buf[src], t->peer_lo_count + 2 * t->halo, bw, bh);
+        a.tmap_hi = tensor_tmap_at(t, t->peer_hi_buf[src], t->peer_hi_count + 2 * t->halo, bw, bh);
+        if (a.tmap_lo == nullptr || a.tmap_hi == nullptr) fail(GL_E_CUDA, "tensor map over a peer buffer failed");
+      }
+      a.src_lo = t->peer_lo_buf[src];
+      a.src_hi = t->peer_hi_buf[src];
       a.lo_add = t->peer_lo_count;
     }
   } else if (fused) {

@@ -215,6 +215,8 @@ struct StepArgs {
   const CUtensorMap* tmap_lo = nullptr;  // left neighbour's source buffer
   const CUtensorMap* tmap_hi = nullptr;  // right neighbour's source buffer
   int lo_add = 0;                        // left neighbour's interior channel count
+  const double* src_lo = nullptr;        // the neighbours' source buffers (storage plane 0)
+  const double* src_hi = nullptr;
   int* host_status = nullptr;            // mapped status word (synchronous gl_step)
 };
 

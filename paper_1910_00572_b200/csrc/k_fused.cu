@@ -153,6 +153,9 @@ struct FusedParams {
   BufState* dst_state;
   StepState* step_state;
   int* host_status;          // mapped status word of a synchronous gl_step, or null
+  // cp.async load path (widths TMA cannot stride: odd W): storage plane 0 of
+  // the own buffer and of the left / right neighbour buffers (peer reads)
+  const double* src_base[3];
   double sep[2 * kFusedMaxRadius + 1];
   double ang[2 * kFusedMaxHalf + 1];
   // the step's shift records (host) for the window's input planes: output
@@ -270,7 +273,7 @@ __device__ __forceinline__ double row_pass(const FusedParams& p, double s) {
   return acc;
 }
 
-template <int R, int H, int ROWS, int NS, bool FAST, bool HIMAX>
+template <int R, int H, int ROWS, int NS, bool FAST, bool HIMAX, bool TMA>
 __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
                                             const CUtensorMap* tmap_lo,
                                             const CUtensorMap* tmap_hi,
@@ -292,21 +295,58 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
   // over halo storage for a theta-slab shard, or a neighbour's buffer over
   // peer memory for a shard's halo planes, so no halo exchange step exists).
   const int rec0 = k0 - p.k_base;
+  // TMA: lane 0 issues one 3-D box copy. Otherwise (a row pitch TMA cannot
+  // stride, i.e. odd W) every lane issues 8-byte cp.async copies of its share
+  // of the same box, zero-filled outside the grid, and arrives on the
+  // stage's mbarrier (count 32) when they land: same smem layout, same
+  // consumer code.
   auto issue = [&](int it, int stage) {
     const ChanRec& rc = p.rec[rec0 + n_iter - 1 - it];  // descending walk
     const int map = rc.map;
-    const CUtensorMap* m = map == 0 ? tmap : (map == 1 ? tmap_lo : tmap_hi);
-    mbar_arrive_expect(&mbar[stage], G::B_BYTES);
-    tma_load_3d(Bs + stage * G::STAGE, m, (x0 - R - rc.ox - 1) & ~1,
-                y0 - R - rc.oy - 1, rc.z, &mbar[stage]);
+    const int bx0 = (x0 - R - rc.ox - 1) & ~1, by0 = y0 - R - rc.oy - 1;
+    if constexpr (TMA) {
+      const CUtensorMap* m = map == 0 ? tmap : (map == 1 ? tmap_lo : tmap_hi);
+      mbar_arrive_expect(&mbar[stage], G::B_BYTES);
+      tma_load_3d(Bs + stage * G::STAGE, m, bx0, by0, rc.z, &mbar[stage]);
+    } else {
+      // row by row: lane l copies box column l (lanes 0, 1 also 32, 33)
+      const double* plane_base = p.src_base[map] + plane * static_cast<size_t>(rc.z);
+      const uint32_t dst0 = smem_u32(Bs + stage * G::STAGE) + 8u * lane;
+      const int gx = bx0 + lane, gx2 = bx0 + 32 + lane;
+      const bool xin = gx >= 0 && gx < W;
+      const bool xin2 = lane < G::BW - 32 && gx2 >= 0 && gx2 < W;
+      ptrdiff_t row = static_cast<ptrdiff_t>(by0) * W;
+#pragma unroll
+      for (int by = 0; by < G::BH; ++by, row += W) {
+        const bool yin = by0 + by >= 0 && by0 + by < Hh;
+        const bool in = xin && yin, in2 = xin2 && yin;
+        const double* src = in ? plane_base + row + gx : plane_base;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst0 + 8u * by * G::BW), "l"(src),
+                     "r"(in ? 8 : 0)
+                     : "memory");
+        if (lane < G::BW - 32) {
+          const double* src2 = in2 ? plane_base + row + gx2 : plane_base;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst0 + 8u * (by * G::BW + 32)),
+                       "l"(src2), "r"(in2 ? 8 : 0)
+                       : "memory");
+        }
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&mbar[stage]))
+                   : "memory");
+    }
   };
 
   if (lane == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&mbar[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&mbar[s], TMA ? 1 : 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < NS && s < n_iter; ++s) issue(s, s);
+    if constexpr (TMA) {
+      for (int s = 0; s < NS && s < n_iter; ++s) issue(s, s);
+    }
   }
   __syncwarp();
+  if constexpr (!TMA) {
+    for (int s = 0; s < NS && s < n_iter; ++s) issue(s, s);
+  }
 
   // Per-tile constants of this lane's column: S mask bits (occupied or
   // outside the grid), store-valid bits, and the activation inverse of the
@@ -476,7 +516,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
       }
     }
     __syncwarp();  // every lane is done with this stage
-    if (lane == 0 && it + NS < n_iter) {
+    if ((!TMA || lane == 0) && it + NS < n_iter) {
       if (scaled) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(it + NS, stage);
     }
@@ -500,7 +540,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
   return vmax;
 }
 
-template <int R, int H, int ROWS, int NS, int NWARP, bool FAST, bool HIMAX>
+template <int R, int H, int ROWS, int NS, int NWARP, bool FAST, bool HIMAX, bool TMA>
 __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_MINB_H3)
     k_fused_step(const __grid_constant__ CUtensorMap tmap,
                  const __grid_constant__ CUtensorMap tmap_lo,
@@ -521,7 +561,7 @@ __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_
   double* wmax = reinterpret_cast<double*>(bars + NWARP * NS);
   double* invs = wmax + NWARP + warp * ROWS * 32;  // GL_FUSED_INVSMEM: [ROWS][32] per warp
 
-  if (threadIdx.x == 0) {
+  if (TMA && threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
   }
   // Surplus warps of the last CTA redo the last tile with stores disabled,
@@ -540,7 +580,7 @@ __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_
   const int y0 = (tile / p.tiles_x) * ROWS;
   const int k0 = p.k_base + chunk * p.k_chunk;
   const int n_out = min(p.k_chunk, p.k_end - k0);
-  double vmax = warp_tile<R, H, ROWS, NS, FAST, HIMAX>(&tmap, &tmap_lo, &tmap_hi, p, Bs, mbar, lane, x0, y0, k0,
+  double vmax = warp_tile<R, H, ROWS, NS, FAST, HIMAX, TMA>(&tmap, &tmap_lo, &tmap_hi, p, Bs, mbar, lane, x0, y0, k0,
                                                        n_out, active, invs);
 
   // global max -> the last CTA finalises status and the pending rescale
@@ -658,13 +698,13 @@ constexpr size_t smem_bytes() {
          (GL_FUSED_INVSMEM ? static_cast<size_t>(kNWARP) * ROWS * 32 * 8 : 0);
 }
 
-template <int R, int H, bool FAST, bool HIMAX>
+template <int R, int H, bool FAST, bool HIMAX, bool TMA>
 void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& fp) {
   const int n_win = fp.k_end - fp.k_base;
   constexpr int ROWS = rows_for<H>();
   using G = Geo<R, ROWS>;
   constexpr size_t smem = smem_bytes<R, ROWS>();
-  auto kern = k_fused_step<R, H, ROWS, kNS, kNWARP, FAST, HIMAX>;
+  auto kern = k_fused_step<R, H, ROWS, kNS, kNWARP, FAST, HIMAX, TMA>;
   static uint64_t configured = 0;  // bit per device: the attribute is per device
   const uint64_t bit = 1ull << (ctx->device & 63);
   if (!(configured & bit)) {
@@ -697,18 +737,26 @@ void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& f
   fp.k_chunk = (n_win + fp.n_chunks - 1) / fp.n_chunks;
   fp.n_chunks = (n_win + fp.k_chunk - 1) / fp.k_chunk;
   const int blocks = ((fp.n_tiles + kNWARP - 1) / kNWARP) * fp.n_chunks;
-  kern<<<blocks, 32 * kNWARP, smem, ctx->stream>>>(*tmaps[0], *tmaps[1], *tmaps[2], fp);
+  static const CUtensorMap kNoMap{};  // the cp.async path never reads its maps
+  kern<<<blocks, 32 * kNWARP, smem, ctx->stream>>>(TMA ? *tmaps[0] : kNoMap, TMA ? *tmaps[1] : kNoMap,
+                                                   TMA ? *tmaps[2] : kNoMap, fp);
   ctx->launches++;
 }
 
 template <int R, int H>
 void launch_rh(gl_context* ctx, const CUtensorMap* const* tmap, FusedParams& fp, bool fast, bool himax) {
-  if (fast && himax) {
-    launch_rhf<R, H, true, true>(ctx, tmap, fp);
+  if (tmap[0] == nullptr) {  // cp.async loads (odd widths); no high-word max variant
+    if (fast) {
+      launch_rhf<R, H, true, false, false>(ctx, tmap, fp);
+    } else {
+      launch_rhf<R, H, false, false, false>(ctx, tmap, fp);
+    }
+  } else if (fast && himax) {
+    launch_rhf<R, H, true, true, true>(ctx, tmap, fp);
   } else if (fast) {
-    launch_rhf<R, H, true, false>(ctx, tmap, fp);
+    launch_rhf<R, H, true, false, true>(ctx, tmap, fp);
   } else {
-    launch_rhf<R, H, false, false>(ctx, tmap, fp);
+    launch_rhf<R, H, false, false, true>(ctx, tmap, fp);
   }
 }
 
@@ -783,9 +831,13 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
   // shard with peers: storage planes s < halo are read from the left
   // neighbour's buffer (its plane s + lo_add), planes s >= halo + c from the
   // right neighbour's (plane s - c), through their own tensor maps
-  const bool peer_read = a.tmap_lo != nullptr && a.tmap_hi != nullptr;
+  const bool peer_read = a.src_lo != nullptr && a.src_hi != nullptr;
   const int halo = a.halo > 0 ? a.halo : 0;
+  // tmap == nullptr: the cp.async load path (a row pitch TMA cannot stride)
   const CUtensorMap* maps[3] = {tmap, peer_read ? a.tmap_lo : tmap, peer_read ? a.tmap_hi : tmap};
+  fp.src_base[0] = a.src;
+  fp.src_base[1] = peer_read ? a.src_lo : a.src;
+  fp.src_base[2] = peer_read ? a.src_hi : a.src;
   for (int t = 0; t < 2 * r + 1; ++t) fp.sep[t] = sep[t];
   for (int t = 0; t < ang.n; ++t) fp.ang[t] = ang.w[t];
   // The shift records ride in the launch parameters; more than
@@ -797,7 +849,7 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
   // on tensors large enough that the epilogue launch (~3 us) is noise:
   // measured 4096^2 x 360 25.05 vs 25.78 ms; 1024^2 x 72 0.258 vs 0.255 ms
   const size_t elems = static_cast<size_t>(a.w) * a.h * a.c;
-  const bool himax = GL_FUSED_HIMAX && fast && (!fp.shard || a.full_shard) &&
+  const bool himax = GL_FUSED_HIMAX && fast && tmap != nullptr && (!fp.shard || a.full_shard) &&
                      (ctx->himax_mode == 1 || (ctx->himax_mode == 0 && elems >= (size_t(1) << 27)));
   const int win = kParamChannels - 2 * H;
   for (int kb = 0; kb < a.c; kb += win) {

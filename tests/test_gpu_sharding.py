@@ -82,9 +82,11 @@ def _cai(ptr):
     return _V()
 
 
-@pytest.mark.parametrize("G,c_total,noise", [(1, 72, (0.03, 0.03, 0.012)), (2, 72, (0.03, 0.03, 0.012)),
-                                             (3, 36, (1e-4, 1e-4, 0.012)), (8, 360, (0.03, 0.03, 0.012))])
-def test_fused_peer_halo_reads_bitwise_equal_unsharded(ctx, G, c_total, noise):
+@pytest.mark.parametrize("G,c_total,noise,W", [(1, 72, (0.03, 0.03, 0.012), 128), (2, 72, (0.03, 0.03, 0.012), 128),
+                                               (3, 36, (1e-4, 1e-4, 0.012), 128), (8, 360, (0.03, 0.03, 0.012), 128),
+                                               (2, 72, (0.03, 0.03, 0.012), 127),   # odd W: cp.async loads
+                                               (3, 360, (0.03, 0.03, 0.012), 95)])
+def test_fused_peer_halo_reads_bitwise_equal_unsharded(ctx, G, c_total, noise, W):
     """Peer mode: each shard's fused step TMA-reads its halo input planes
     straight from the neighbours' buffers (gl_shard_set_peers; here the
     neighbours' buffers on the same device stand in for CUDA-IPC mappings of
@@ -94,8 +96,8 @@ def test_fused_peer_halo_reads_bitwise_equal_unsharded(ctx, G, c_total, noise):
     interior planes circularly."""
     import torch
     from paper_1910_00572_b200.sharding import peer_plan
-    occ = make_floorplan(128, 96, seed=22)
-    m = g.OccupancyMap(128, 96, 0.1, occ, ctx=ctx)
+    occ = make_floorplan(W, 96, seed=22)
+    m = g.OccupancyMap(W, 96, 0.1, occ, ctx=ctx)
     ks = g.build_kernels(g.MotionNoise(*noise), c_total, 0.1, 2 * math.pi / c_total)
     act = g.make_activation(m, ks, c_total, ctx)
     halo = max(len(ks.angular) // 2, 1)
@@ -117,7 +119,7 @@ def test_fused_peer_halo_reads_bitwise_equal_unsharded(ctx, G, c_total, noise):
             for q in list(range(halo)) + list(range(halo + t.channels(), 2 * halo + t.channels())):
                 p = C.POINTER(C.c_double)()
                 check(ctx.lib.gl_tensor_buffer_ptr(ctx.h, t.h, b, q, C.byref(p)))
-                torch.as_tensor(_cai_f64(C.cast(p, C.c_void_p).value, 128 * 96), device="cuda").fill_(float("nan"))
+                torch.as_tensor(_cai_f64(C.cast(p, C.c_void_p).value, W * 96), device="cuda").fill_(float("nan"))
     torch.cuda.synchronize()
     rng = Rng(G * 7 + c_total)
     motions = [random_motion(rng) for _ in range(5)] + [(0.1, 0.0, 0.0), (0.0, 0.0, 0.2)]

@@ -124,6 +124,24 @@ def test_fused_tile_edges_bit_exact(ctx, port):
 
 
 @pytest.mark.parametrize("fast", [True, False])
+@pytest.mark.parametrize("w,h,channels", [(37, 29, 72), (129, 35, 72), (3, 40, 36), (255, 17, 360), (5, 9, 8)])
+def test_fused_odd_widths_bit_exact(ctx, port, fast, w, h, channels):
+    """Odd W: 8*W bytes is not a TMA row stride, so the fused kernel loads
+    its boxes with per-lane cp.async copies (zero-filled outside the grid)
+    instead of one TMA box — same smem layout and arithmetic."""
+    occ = random_map(w, h, 0.12, w * 7 + h)
+    rng = Rng(w + h)
+    B0 = random_tensor(occ, channels, seed=w, free_only=False)
+    motions = [random_motion(rng, 0.3, 0.3, 0.2) for _ in range(3)] + [(0.1, 0.0, 0.0)]
+    ctx.set_fast(fast)
+    try:
+        _run_pair(ctx, port, occ, channels, (0.03, 0.03, 0.012), motions, GL_PATH_FUSED, B0=B0)
+        _run_pair(ctx, port, occ, channels, (0.03, 0.03, 0.012), motions, GL_PATH_FUSED)
+    finally:
+        ctx.set_fast(True)
+
+
+@pytest.mark.parametrize("fast", [True, False])
 def test_fast_and_strict_variants_agree(ctx, port, fast):
     """The FAST fused variant (clean tensors) and the literal STRICT sequence
     are both bit-exact against the oracle."""

@@ -1,0 +1,1 @@
+for i in 1 2; do bash tools/sweep_variants.sh --config c4 --steps 100; done > gpurun_out/sweep_c4.txt 2>&1; cat gpurun_out/sweep_c4.txt
