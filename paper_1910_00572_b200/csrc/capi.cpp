@@ -535,10 +535,19 @@ gl_status gl_field_create(gl_context* ctx, const gl_map* map, gl_field** out) {
     auto f = std::make_unique<gl_field>();
     f->w = map->w;
     f->h = map->h;
-    f->values = glb::distance_field_host(map->occ.data(), map->w, map->h, map->res);
-    CK(cudaMalloc(&f->d_values, f->values.size() * sizeof(double)));
-    CK(cudaMemcpy(f->d_values, f->values.data(), f->values.size() * sizeof(double),
-                  cudaMemcpyHostToDevice));
+    // exact EDT on the device; the host copy feeds the per-cell beam score
+    // table, which needs the host libm (obs_tables)
+    const size_t cells = static_cast<size_t>(map->w) * map->h;
+    f->values.resize(cells);
+    CK(cudaMalloc(&f->d_values, cells * sizeof(double)));
+    void* scratch = nullptr;
+    CK(cudaMalloc(&scratch, glb::distance_field_scratch_bytes(map->w, map->h)));
+    glb::launch_distance_field(ctx, map->d_occ, map->w, map->h, map->res, f->d_values, scratch);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(f->values.data(), f->d_values, cells * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaFree(scratch));
     *out = f.release();
   });
 }

@@ -241,6 +241,9 @@ void launch_init_uniform(gl_context* ctx, double* buf, const uint8_t* occ,
 void launch_make_activation(gl_context* ctx, const uint8_t* occ, int w, int h,
                             int c, const gl_kernels* k, double* values,
                             double* inverse, bool k_invariant, double* scratch);
+void launch_distance_field(gl_context* ctx, const uint8_t* d_occ, int w, int h, double res,
+                           double* d_out, void* d_scratch);
+size_t distance_field_scratch_bytes(int w, int h);
 void launch_belief_map(gl_context* ctx, const double* buf, int w, int h,
                        int c, double* out);
 void launch_mask_plane(gl_context* ctx, const double* in, const uint8_t* occ,

@@ -254,65 +254,5 @@ void force_ring(uint8_t* occ, int w, int h) {
   }
 }
 
-// distance_field (occupancy_map.cpp:231-271): per-column two-sweep run
-// lengths squared, then the Felzenszwalb-Huttenlocher lower envelope per
-// row, sqrt * resolution. Setup-time, host side (input to the likelihood
-// table, like the reference's field).
-std::vector<double> distance_field_host(const uint8_t* occ, int w, int h,
-                                        double res) {
-  std::vector<double> sq(static_cast<size_t>(w) * h);
-  const int far = w + h;
-  for (int i = 0; i < w; ++i) {
-    int run = far;
-    for (int j = 0; j < h; ++j) {
-      const size_t p = static_cast<size_t>(j) * w + i;
-      run = occ[p] ? 0 : std::min(far, run + 1);
-      sq[p] = run;
-    }
-    run = far;
-    for (int j = h - 1; j >= 0; --j) {
-      const size_t p = static_cast<size_t>(j) * w + i;
-      run = occ[p] ? 0 : std::min(far, run + 1);
-      const double c = std::min(sq[p], static_cast<double>(run));
-      sq[p] = c * c;
-    }
-  }
-  std::vector<double> f(w), d(w), z(w + 1);
-  std::vector<int> v(w);
-  const double inf = std::numeric_limits<double>::infinity();
-  for (int j = 0; j < h; ++j) {
-    double* row = sq.data() + static_cast<size_t>(j) * w;
-    std::copy(row, row + w, f.begin());
-    int k = 0;
-    v[0] = 0;
-    z[0] = -inf;
-    z[1] = inf;
-    for (int q = 1; q < w; ++q) {
-      double s;
-      for (;;) {
-        const int p = v[k];
-        s = ((f[q] + q * q) - (f[p] + p * p)) / (2.0 * q - 2.0 * p);
-        if (s <= z[k]) {
-          --k;
-        } else {
-          break;
-        }
-      }
-      ++k;
-      v[k] = q;
-      z[k] = s;
-      z[k + 1] = inf;
-    }
-    k = 0;
-    for (int q = 0; q < w; ++q) {
-      while (z[k + 1] < q) ++k;
-      const int p = v[k];
-      d[q] = (q - p) * (q - p) + f[p];
-    }
-    std::copy(d.begin(), d.end(), row);
-  }
-  for (double& x : sq) x = std::sqrt(x) * res;
-  return sq;
-}
 
 }  // namespace glb

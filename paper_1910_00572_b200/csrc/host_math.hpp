@@ -40,7 +40,6 @@ MapParse parse_pgm_map(const uint8_t* bytes, size_t n, int threshold);
 bool looks_like_png(const uint8_t* bytes, size_t n);
 std::vector<uint8_t> decode_png_gray8(const uint8_t* bytes, size_t n, int* width, int* height);
 void force_ring(uint8_t* occ, int w, int h);
-std::vector<double> distance_field_host(const uint8_t* occ, int w, int h,
-                                        double res);
+
 
 }  // namespace glb

@@ -292,6 +292,71 @@ __global__ void k_activation(const double* __restrict__ diff, int diff_per_k,
   }
 }
 
+// distance_field (occupancy_map.cpp:231-271) on the device, in the
+// reference's arithmetic: per-column run lengths by two sweeps (integers),
+// min and square; then per row the Felzenszwalb-Huttenlocher lower envelope
+// of parabolas (IEEE div/sqrt are correctly rounded on both sides, no FMA
+// contraction: bit-identical), sqrt * resolution.
+__global__ void k_edt_cols(const uint8_t* __restrict__ occ, double* __restrict__ sq, int w, int h) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= w) return;
+  const int far = w + h;
+  int run = far;
+  for (int j = 0; j < h; ++j) {
+    const size_t p = static_cast<size_t>(j) * w + i;
+    run = occ[p] ? 0 : (run >= far ? far : run + 1);
+    sq[p] = run;
+  }
+  run = far;
+  for (int j = h - 1; j >= 0; --j) {
+    const size_t p = static_cast<size_t>(j) * w + i;
+    run = occ[p] ? 0 : (run >= far ? far : run + 1);
+    double c = sq[p];
+    c = c < static_cast<double>(run) ? c : static_cast<double>(run);  // std::min(cell, run)
+    sq[p] = c * c;
+  }
+}
+
+// one thread per row; v (int) and z (double) are per-row scratch of w and
+// w + 1 entries (occupancy_map.cpp:197-226)
+__global__ void k_edt_rows(const double* __restrict__ sq, double* __restrict__ out, int* __restrict__ vs,
+                           double* __restrict__ zs, int w, int h, double res) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= h) return;
+  const double* f = sq + static_cast<size_t>(j) * w;
+  int* v = vs + static_cast<size_t>(j) * w;
+  double* z = zs + static_cast<size_t>(j) * (w + 1);
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  int k = 0;
+  v[0] = 0;
+  z[0] = -inf;
+  z[1] = inf;
+  for (int q = 1; q < w; ++q) {
+    double s;
+    for (;;) {
+      const int p = v[k];
+      s = ((f[q] + q * q) - (f[p] + p * p)) / (2.0 * q - 2.0 * p);
+      if (s <= z[k]) {
+        --k;
+      } else {
+        break;
+      }
+    }
+    ++k;
+    v[k] = q;
+    z[k] = s;
+    z[k + 1] = inf;
+  }
+  k = 0;
+  double* o = out + static_cast<size_t>(j) * w;
+  for (int q = 0; q < w; ++q) {
+    while (z[k + 1] < q) ++k;
+    const int p = v[k];
+    const double d = (q - p) * (q - p) + f[p];
+    o[q] = sqrt(d) * res;
+  }
+}
+
 // belief_map (belief_tensor.cpp:500-510).
 __global__ void k_belief_map(const double* __restrict__ B,
                              double* __restrict__ out, size_t plane, int c) {
@@ -555,6 +620,22 @@ void launch_make_activation(gl_context* ctx, const uint8_t* occ, int w, int h,
       diff, k_invariant ? 0 : 1, values, inverse, k->d_ang_off, k->d_ang_w,
       k->info.n_angular, plane, c, c_out);
   ctx->launches++;
+}
+
+void launch_distance_field(gl_context* ctx, const uint8_t* d_occ, int w, int h, double res,
+                           double* d_out, void* d_scratch) {
+  // scratch: sq (w*h doubles) | z (h*(w+1) doubles) | v (h*w ints)
+  double* sq = static_cast<double*>(d_scratch);
+  double* z = sq + static_cast<size_t>(w) * h;
+  int* v = reinterpret_cast<int*>(z + static_cast<size_t>(h) * (w + 1));
+  k_edt_cols<<<(w + 127) / 128, 128, 0, ctx->stream>>>(d_occ, sq, w, h);
+  k_edt_rows<<<(h + 63) / 64, 64, 0, ctx->stream>>>(sq, d_out, v, z, w, h, res);
+  ctx->launches += 2;
+}
+
+size_t distance_field_scratch_bytes(int w, int h) {
+  return sizeof(double) * (static_cast<size_t>(w) * h + static_cast<size_t>(h) * (w + 1)) +
+         sizeof(int) * static_cast<size_t>(w) * h;
 }
 
 void launch_belief_map(gl_context* ctx, const double* buf, int w, int h,

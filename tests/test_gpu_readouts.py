@@ -68,6 +68,20 @@ def test_argmax_tie_rule(ctx):
         g.argmax_state(t)
 
 
+@pytest.mark.parametrize("w,h,p", [(1, 7, 0.0), (7, 1, 0.0), (2, 2, 0.0), (33, 17, 0.1), (64, 64, 0.02),
+                                   (301, 123, 0.3), (512, 384, 0.05), (130, 70, 0.6)])
+def test_distance_field_on_device_bit_exact(ctx, port, w, h, p):
+    """distance_field (occupancy_map.cpp:231-271) runs on the device: column
+    run lengths, Felzenszwalb-Huttenlocher rows, sqrt * res — bitwise the
+    CPU restatement (itself pinned to the reference) on thin, tiny, sparse
+    and dense maps."""
+    occ = random_map(w, h, p, w * 13 + h) if min(w, h) > 2 else np.ones((h, w), np.uint8)
+    m = g.OccupancyMap(w, h, 0.05, occ, ctx=ctx)
+    f = g.DistanceField(m, ctx)
+    want = port.distance_field(m.cells(), 0.05)
+    assert_bitwise(f.values(), want, f"distance field {w}x{h}")
+
+
 def test_dither_bit_exact_random_maps(ctx, port):
     rng = np.random.default_rng(7)
     for trial in range(25):
