@@ -1485,11 +1485,25 @@ ObsTables obs_tables(gl_context* ctx, const gl_field* cf, gl_likelihood p) {
   if (!(f->score_sigma == p.sigma_hit && f->score_floor == p.weight_floor && f->d_score)) {
     const double fl = p.weight_floor;
     const double inv2s2 = 1.0 / (2.0 * p.sigma_hit * p.sigma_hit);
+    // The field takes few distinct values (sqrt(n) * res for the integer
+    // squared cell distances n present), so a direct-mapped memo on the
+    // value's bits evaluates the host-libm expression once per distinct d
+    // (same input, same glibc result: bit-identical to the per-cell loop).
     std::vector<double> score(f->values.size());
+    constexpr int kMemoBits = 16;
+    std::vector<uint64_t> memo_key(size_t(1) << kMemoBits, ~0ull);
+    std::vector<double> memo_val(size_t(1) << kMemoBits);
     for (size_t q = 0; q < f->values.size(); ++q) {
       const double d = f->values[q];
-      const double gauss = std::exp(-d * d * inv2s2);
-      score[q] = std::log((1.0 - fl) * gauss + fl);
+      uint64_t bits;
+      std::memcpy(&bits, &d, 8);
+      const size_t slot = static_cast<size_t>((bits * 0x9E3779B97F4A7C15ull) >> (64 - kMemoBits));
+      if (memo_key[slot] != bits) {
+        const double gauss = std::exp(-d * d * inv2s2);  // observation.cpp:101-106
+        memo_val[slot] = std::log((1.0 - fl) * gauss + fl);
+        memo_key[slot] = bits;
+      }
+      score[q] = memo_val[slot];
     }
     if (!f->d_score) CK(cudaMalloc(&f->d_score, score.size() * sizeof(double)));
     CK(cudaMemcpy(f->d_score, score.data(), score.size() * sizeof(double), cudaMemcpyHostToDevice));
