@@ -464,10 +464,23 @@ __global__ void k_hash(const double* __restrict__ B, size_t n,
 
 __global__ void k_plane_max(const double* __restrict__ B, size_t n,
                             unsigned long long* gmax) {
+  // 16-byte loads over the aligned body (the max is order-independent),
+  // scalar head/tail
   double m = 0.0;
-  for (size_t q = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-       q < n; q += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    m = dmax_ref(m, B[q]);
+  if (n == 0) return;
+  const size_t head = (reinterpret_cast<uintptr_t>(B) & 15) ? 1 : 0;
+  const size_t n2 = (n - head) / 2;
+  const double2* B2 = reinterpret_cast<const double2*>(B + head);
+  const size_t tid = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t q = tid; q < n2; q += stride) {
+    const double2 v = B2[q];
+    m = dmax_ref(m, v.x);
+    m = dmax_ref(m, v.y);
+  }
+  if (tid == 0) {
+    if (head && n > 0) m = dmax_ref(m, B[0]);
+    if (head + 2 * n2 < n) m = dmax_ref(m, B[n - 1]);
   }
   m = warp_max_pos(m);
   if ((threadIdx.x & 31) == 0) atomic_max_pos(gmax, m);

@@ -68,7 +68,7 @@ template <int G, bool kConstC>
 __device__ __forceinline__ bool fs_spec_groups(const double* pre, double* err,
                                                const unsigned int* sup, int& q,
                                                double& carry, double c_reg, int w,
-                                               volatile int* progress) {
+                                               volatile int* /*progress: see the loop end*/) {
   const double c = kConstC ? 7.0 / 16.0 : c_reg;
   for (; q + G <= w - 1; q += G) {
     double2 pv[G / 2];
@@ -100,8 +100,9 @@ __device__ __forceinline__ bool fs_spec_groups(const double* pre, double* err,
     }
     if (__builtin_expect(mx >= 0x3FE00000, 0)) return true;
     carry = cr;
-    fence_cta();
-    *progress = q + G;
+    // no progress publication: these are the row's tail groups, whose
+    // positions only the helper's last chunk reads, after the row end's
+    // publication (a CTA fence per tail group cost ~300 cycles per row)
   }
   return false;
 }
