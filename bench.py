@@ -474,6 +474,17 @@ def run_batch(args, cfg, world, rank, local):
         g.tensor_status(t)
     dt = dist_max(dt, world, "ours")
     value = world * args.steps / dt
+    # e2e: every batch step enqueued through the API (motion tables in the
+    # launches) and every robot's status read back to the host before the next
+    n_e2e = max(1, min(args.steps, args.e2e_steps // 4))
+    dist_barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        batch_step()
+        for ctx, m, ks, act, t in robots:
+            g.tensor_status(t)
+    e2e_s = dist_max(time.perf_counter() - t0, world, "ours")
+    e2e = world * n_e2e / e2e_s
     bytes_batch = B * algo_bytes(W, H, C)
     peak, peak_src = measured_peak()
     if rank != 0:
@@ -486,7 +497,8 @@ def run_batch(args, cfg, world, rank, local):
         "config": {"workload": cfg["workload"], "W": W, "H": H, "channels": C, "robots_per_gpu": B,
                    "parallelism": f"{B} independent tensors per GPU on {len(ctxs)} streams",
                    "timing": "host wall clock around K batch steps with device syncs"},
-        "e2e": None,
+        "e2e": {"value": e2e, "unit": "batch-Hz", "h2d_bytes_per_step": B * 16 * C, "d2h_bytes_per_step": B * 16,
+                "how": f"{n_e2e} batch steps: {B} step_async calls, then every robot's status read back"},
         "roofline": {"bound": "hbm", "achieved": bytes_batch * value / world / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": bytes_batch * value / world / 1e9 / peak, "traffic": None, "peak_source": peak_src,
                      "bytes_per_launch": algo_bytes(W, H, C), "note": "aggregate over the batch's launches"},
