@@ -473,9 +473,16 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
       if (lane == 0) sup[wd] = bits;
     }
     // diffusion weights (t.w / wsum) of row j's sources: interior sources
-    // have wsum == 1 (the quotients are exact); the two scan ends differ
-    auto coef = [&](int s, double wt) {
-      return (s == 0 || s == w - 1) ? wt / fs_wsum(s, j, w, h, pd) : wt;
+    // have wsum == 1 (the quotients are exact); the two scan ends differ.
+    // Their quotients are formed here, before the chain reaches the row: an
+    // FP64 division in the row's last chunk sat on the chain's row-end
+    // critical path (~880 cycles per row for that chunk, measured).
+    const double w_lo = fs_wsum(0, j, w, h, pd), w_hi = fs_wsum(w - 1, j, w, h, pd);
+    const double e1[2] = {(1.0 / 16.0) / w_lo, (1.0 / 16.0) / w_hi};
+    const double e5[2] = {(5.0 / 16.0) / w_lo, (5.0 / 16.0) / w_hi};
+    const double e3[2] = {(3.0 / 16.0) / w_lo, (3.0 / 16.0) / w_hi};
+    auto coef = [&](int s, double wt, const double* edge) {
+      return s == 0 ? edge[0] : (s == w - 1 ? edge[1] : wt);
     };
     for (int base = 0; base < w; base += 32) {
       const int pos = base + lane;  // scan position in row j
@@ -489,9 +496,9 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
         // i.e. scan positions pos-1, pos, pos+1
         const int t = pd == 1 ? pos : w - 1 - pos;
         double v = nrow[t] * scale;
-        if (pos >= 1) v += err[pos] * coef(t - pd, 1.0 / 16.0);
-        v += err[pos + 1] * coef(t, 5.0 / 16.0);
-        if (pos + 1 < w) v += err[pos + 2] * coef(t + pd, 3.0 / 16.0);
+        if (pos >= 1) v += err[pos] * coef(t - pd, 1.0 / 16.0, e1);
+        v += err[pos + 1] * coef(t, 5.0 / 16.0, e5);
+        if (pos + 1 < w) v += err[pos + 2] * coef(t + pd, 3.0 / 16.0, e3);
         pre[w - pos] = v;  // row j+1 scans the other way: position w-1-pos
       }
     }
