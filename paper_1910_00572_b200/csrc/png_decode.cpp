@@ -110,6 +110,7 @@ std::vector<uint8_t> decode_png_gray8(const uint8_t* b, size_t n, int* width, in
       if (data[10] != 0 || data[11] != 0 || interlace > 1) throw MapParseFailure("corrupt PNG stream (IHDR)");
       if (w == 0 || h == 0) throw MapParseFailure("PNG with zero dimension");
       if (w > 0x7fffffffu || h > 0x7fffffffu) throw MapParseFailure("corrupt PNG stream (IHDR size)");
+      if (static_cast<uint64_t>(w) * h > (uint64_t(1) << 32)) throw MapParseFailure("PNG map larger than 2^32 cells");
       if (depth == 16) throw MapParseFailure("16-bit PNG not supported; expected 8-bit grayscale");
       if (color != 0 && color != 4) throw MapParseFailure("PNG is not grayscale");
       const bool ok = color == 0 ? (depth == 1 || depth == 2 || depth == 4 || depth == 8) : depth == 8;
