@@ -84,6 +84,12 @@ gl_status gl_context_set_himax(gl_context* ctx, int mode);
  * fill the GPU together: 1 avoids the recompute (64 x 512^2 x 72: 248 vs 239
  * batch-Hz). Results are bit-identical for every setting. */
 gl_status gl_context_set_channel_chunks(gl_context* ctx, int n);
+/* Wave-tail split of a one-chunk fused-step launch: the last `ctas` CTAs of
+ * the grid (the partial last wave of resident CTAs) run their tiles' channels
+ * in `chunks` chunks, so the tail drains in shorter work items. ctas = -1:
+ * auto (the last ~1/5 of the partial wave, default chunks 3), 0: off.
+ * Results are bit-identical for every setting. */
+gl_status gl_context_set_wave_tail(gl_context* ctx, int ctas, int chunks);
 /* scan_likelihood's final exp (the per-pose geometric mean,
  * observation.cpp:110): 1 (default) evaluates it with the host's libm like the
  * reference (bit-exact; one D2H/H2D of <= 512*Theta doubles per observation),

@@ -74,6 +74,7 @@ SIGNATURES = {
     "gl_context_set_fast": [_vp, C.c_int],
     "gl_context_set_himax": [_vp, C.c_int],
     "gl_context_set_channel_chunks": [_vp, C.c_int],
+    "gl_context_set_wave_tail": [_vp, C.c_int, C.c_int],
     "gl_context_set_host_exp": [_vp, C.c_int],
     "gl_shard_init_uniform": [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _pvp],
     "gl_shard_info": [_vp, _ip, _ip, _ip, _ip],

@@ -455,6 +455,16 @@ gl_status gl_context_set_channel_chunks(gl_context* ctx, int n) {
   });
 }
 
+gl_status gl_context_set_wave_tail(gl_context* ctx, int ctas, int chunks) {
+  return guard([&] {
+    need(ctx, "null context");
+    need(ctas >= -1, "wave-tail CTAs must be >= -1 (-1 = auto, 0 = off)");
+    need(chunks >= 1, "wave-tail chunks must be >= 1");
+    ctx->tail_ctas = ctas;
+    ctx->tail_chunks = chunks;
+  });
+}
+
 gl_status gl_context_launch_count(gl_context* ctx, uint64_t* n) {
   return guard([&] {
     need(ctx && n, "null argument");

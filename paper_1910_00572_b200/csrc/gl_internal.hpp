@@ -87,6 +87,8 @@ struct gl_context {
   bool allow_fast = true;  // use the FAST fused variant on clean buffers
   int himax_mode = 0;      // high-word step max: 0 auto (large tensors), 1 always, 2 never
   int channel_chunks = 0;  // fused step channel chunks: 0 auto, n >= 1 fixed
+  int tail_ctas = -1;      // fused step wave-tail split: -1 auto, 0 off, n CTAs
+  int tail_chunks = 3;     // channel chunks of each wave-tail CTA's tiles
   bool host_exp = true;    // likelihood geometric mean: exp by host glibc (exact)
   void* d_kind = nullptr;  // likelihood case codes
   size_t kind_bytes = 0;

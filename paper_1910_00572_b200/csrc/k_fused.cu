@@ -149,6 +149,10 @@ struct FusedParams {
   int tiles_x, n_tiles;
   int k_base, k_end;         // this launch's output channels (a window of <= kParamChannels - 2H)
   int k_chunk, n_chunks;     // output channels per warp, chunks per tile
+  // wave-tail split: the CTAs from head_ctas on (the last tiles) run their
+  // channels in tail_chunks chunks of tail_k, so the grid's last partial wave
+  // holds shorter work items (head_ctas = grid size: no split)
+  int head_ctas, tail_chunks, tail_k;
   const BufState* src_state;
   BufState* dst_state;
   StepState* step_state;
@@ -571,15 +575,26 @@ __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_
   // chunk (and every shift-record index) derives from blockIdx alone: the
   // compiler keeps the records in uniform registers. Consecutive warps take
   // neighbouring tiles, so their halo rows meet in L2.
-  const int cta_per_chunk = (p.n_tiles + NWARP - 1) / NWARP;
-  const int chunk = blockIdx.x / cta_per_chunk;
-  const int tile_raw = (blockIdx.x - chunk * cta_per_chunk) * NWARP + warp;
+  int tile_raw, k0, n_out;
+  if (static_cast<int>(blockIdx.x) < p.head_ctas) {
+    const int cta_per_chunk = (p.n_tiles + NWARP - 1) / NWARP;
+    const int chunk = blockIdx.x / cta_per_chunk;
+    tile_raw = (blockIdx.x - chunk * cta_per_chunk) * NWARP + warp;
+    k0 = p.k_base + chunk * p.k_chunk;
+    n_out = min(p.k_chunk, p.k_end - k0);
+  } else {  // wave tail (n_chunks == 1 here): tiles from head_ctas * NWARP on, channel chunks of tail_k
+    const int b = blockIdx.x - p.head_ctas;
+    const int first = p.head_ctas * NWARP;
+    const int cta_per_chunk = (p.n_tiles - first + NWARP - 1) / NWARP;
+    const int chunk = b / cta_per_chunk;
+    tile_raw = first + (b - chunk * cta_per_chunk) * NWARP + warp;
+    k0 = p.k_base + chunk * p.tail_k;
+    n_out = min(p.tail_k, p.k_end - k0);
+  }
   const bool active = tile_raw < p.n_tiles;
   const int tile = active ? tile_raw : p.n_tiles - 1;
   const int x0 = (tile % p.tiles_x) * G::OW;
   const int y0 = (tile / p.tiles_x) * ROWS;
-  const int k0 = p.k_base + chunk * p.k_chunk;
-  const int n_out = min(p.k_chunk, p.k_end - k0);
   double vmax = warp_tile<R, H, ROWS, NS, FAST, HIMAX, TMA>(&tmap, &tmap_lo, &tmap_hi, p, Bs, mbar, lane, x0, y0, k0,
                                                        n_out, active, invs);
 
@@ -698,6 +713,17 @@ constexpr size_t smem_bytes() {
          (GL_FUSED_INVSMEM ? static_cast<size_t>(kNWARP) * ROWS * 32 * 8 : 0);
 }
 
+// Wave-tail default (measured, profiles/r01_sweeps.md "wave tail"): with
+// 4 resident CTAs per SM, a grid of more than one wave whose last partial
+// wave holds rem CTAs splits its last ~rem/5 CTAs (rounded down to 32) into
+// 3 channel chunks. 1024^2 x 72 (1120 CTAs, rem 528 -> 96): 0.2475 ->
+// 0.2384 ms; 128 CTAs measured the same, 64 / 160 / 4 chunks gave nothing.
+inline int auto_tail_ctas(const gl_context* ctx, int blocks) {
+  const int slots = 4 * (ctx->sm_count > 0 ? ctx->sm_count : 148);
+  if (blocks <= slots) return 0;
+  return ((blocks % slots) / 5) & ~31;
+}
+
 template <int R, int H, bool FAST, bool HIMAX, bool TMA>
 void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& fp) {
   const int n_win = fp.k_end - fp.k_base;
@@ -736,7 +762,33 @@ void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& f
   if (chunk_override > 0) fp.n_chunks = std::min(chunk_override, n_win);
   fp.k_chunk = (n_win + fp.n_chunks - 1) / fp.n_chunks;
   fp.n_chunks = (n_win + fp.k_chunk - 1) / fp.k_chunk;
-  const int blocks = ((fp.n_tiles + kNWARP - 1) / kNWARP) * fp.n_chunks;
+  int blocks = ((fp.n_tiles + kNWARP - 1) / kNWARP) * fp.n_chunks;
+  // Wave tail: with one chunk, the grid's last partial wave of CTAs leaves
+  // slots idle while it runs; the last tail CTAs' tiles are split into
+  // channel chunks so the tail drains in shorter work items.
+  static const int tail_override = [] {
+    const char* e = std::getenv("GRIDLOC_B200_TAIL");  // tuning experiments only: "ctas[,chunks]"
+    return e ? std::atoi(e) : -1;
+  }();
+  static const int tail_chunks_override = [] {
+    const char* e = std::getenv("GRIDLOC_B200_TAIL");
+    const char* c = e ? std::strchr(e, ',') : nullptr;
+    return c ? std::atoi(c + 1) : 0;
+  }();
+  fp.head_ctas = blocks;
+  fp.tail_chunks = 1;
+  fp.tail_k = fp.k_chunk;
+  int tail = ctx->tail_ctas >= 0 ? ctx->tail_ctas : auto_tail_ctas(ctx, blocks);
+  if (tail_override >= 0) tail = tail_override;
+  tail = fp.n_chunks == 1 ? std::min(tail, blocks) : 0;
+  const int tail_chunks = std::max(1, std::min(tail_chunks_override > 0 ? tail_chunks_override : ctx->tail_chunks, n_win));
+  if (tail > 0 && tail_chunks > 1) {
+    fp.head_ctas = blocks - tail;
+    fp.tail_k = (n_win + tail_chunks - 1) / tail_chunks;
+    fp.tail_chunks = (n_win + fp.tail_k - 1) / fp.tail_k;
+    const int tail_tiles = fp.n_tiles - fp.head_ctas * kNWARP;
+    blocks = fp.head_ctas + ((tail_tiles + kNWARP - 1) / kNWARP) * fp.tail_chunks;
+  }
   static const CUtensorMap kNoMap{};  // the cp.async path never reads its maps
   kern<<<blocks, 32 * kNWARP, smem, ctx->stream>>>(TMA ? *tmaps[0] : kNoMap, TMA ? *tmaps[1] : kNoMap,
                                                    TMA ? *tmaps[2] : kNoMap, fp);

@@ -162,6 +162,12 @@ class Context:
         small tensors on concurrent streams). Bit-identical either way."""
         check(self.lib.gl_context_set_channel_chunks(self.h, int(n)))
 
+    def set_wave_tail(self, ctas: int, chunks: int = 3):
+        """Fused-step wave-tail split: the grid's last `ctas` CTAs run their
+        channels in `chunks` chunks (-1 auto: last ~1/5 of the partial wave,
+        3 chunks; 0 off). Bit-identical."""
+        check(self.lib.gl_context_set_wave_tail(self.h, int(ctas), int(chunks)))
+
     def synchronize(self):
         check(self.lib.gl_context_synchronize(self.h))
 

@@ -261,6 +261,23 @@ def test_explicit_channel_chunks_bit_exact(ctx, port, chunks, channels):
         ctx.set_channel_chunks(0)
 
 
+@pytest.mark.parametrize("tail", [(1, 2), (5, 3), (100000, 2), (0, 2)])
+@pytest.mark.parametrize("channels", [72, 360])
+def test_wave_tail_split_bit_exact(ctx, port, tail, channels):
+    """gl_context_set_wave_tail: the grid's last CTAs splitting their tiles'
+    channels (up to every CTA) gives the same bits as the unsplit walk."""
+    occ = make_floorplan(200, 120, seed=5)
+    rng = Rng(tail[0] + channels)
+    motions = [random_motion(rng) for _ in range(3)]
+    ctx.set_channel_chunks(1)
+    ctx.set_wave_tail(*tail)
+    try:
+        _run_pair(ctx, port, occ, channels, (0.03, 0.03, 0.012), motions, GL_PATH_FUSED)
+    finally:
+        ctx.set_wave_tail(-1, 3)
+        ctx.set_channel_chunks(0)
+
+
 @pytest.mark.parametrize("himax", [1, 2])
 def test_high_word_max_modes_bit_exact(ctx, port, himax):
     """The fused FAST kernel's high-word max (forced on small tensors here;
