@@ -22,8 +22,14 @@ gridloc_main.cpp:207-233: u = (res, 0, 0), main kernels, every step).
            reference sources) on this host's cores, bounded sample.
 
 --impl reference runs the reference's CPU implementation of the same path
-(oracle/_ref; rank 0 only under torchrun) and prints the same line.
-N > 1: independent replicas per rank (weak scaling), no data-path collective.
+(oracle/_ref; rank 0 only under torchrun) and prints the same line; it never
+maps the product library (checked through /proc/self/maps).
+
+--gpus N > 1 re-execs itself under torch.distributed.run (one rank per GPU)
+unless already launched that way, and by default runs configs[3]: ONE
+4096^2x360 belief theta-slab sharded across the N GPUs (strong scaling; halo
+planes read over peer memory inside the step kernel, an 8-byte NCCL MAX
+all-reduce per step). --config c2 with N > 1 runs independent replicas.
 """
 from __future__ import annotations
 
@@ -52,8 +58,8 @@ CONFIGS = {
     "c4s": dict(W=2048, H=2048, C=360, workload="2048x2048x360 floor-plan (config-4 angular width, 1/4 area)"),
     "c5": dict(W=512, H=512, C=72, batch=64, workload="batch of 64 independent robots/maps at 512x512x72 "
                                                       "(BASELINE configs[4])"),
-    "c4": dict(W=4096, H=4096, C=360, workload="4096x4096x360 floor-plan on ONE B200 (BASELINE configs[3]; "
-                                              "2 x 48.3 GB ping-pong in HBM)"),
+    "c4": dict(W=4096, H=4096, C=360, workload="4096x4096x360 floor-plan, theta-slab sharded across the N GPUs "
+                                              "(BASELINE configs[3]; 2 x 48.3 GB ping-pong in HBM at N = 1)"),
 }
 METRIC = "belief updates/sec (Hz) at 1024^2x72"  # the headline (configs[1])
 
@@ -63,6 +69,22 @@ def metric_for(W, H, C, lidar=0):
         return f"belief updates/sec (Hz) at {W}^2x{C} with a LIDAR observation every {lidar} steps"
     return f"belief updates/sec (Hz) at {W}^2x{C}" if W == H else f"belief updates/sec (Hz) at {W}x{H}x{C}"
 HBM_FALLBACK = 6650.0
+
+
+def config_for(cfg):
+    """The workload description both arms print (identical dicts, so the
+    driver's same-config check compares like with like)."""
+    W, H, C = cfg["W"], cfg["H"], cfg["C"]
+    out = {"workload": cfg["workload"], "W": W, "H": H, "channels": C,
+           "l2": f"inputs larger than L2: the FP64 belief ({8 * W * H * C / 1e6:.0f} MB) exceeds the 126 MB L2, "
+                 "so every step streams it from HBM (no flush needed)"
+           if 8 * W * H * C > 126e6 else "belief fits L2 (latency-bound small config; no flush)"}
+    if cfg.get("lidar"):
+        out["observe_every"] = cfg["lidar"]
+        out["sample_budget"] = 512
+    if cfg.get("batch"):
+        out["robots_per_gpu"] = cfg["batch"]
+    return out
 
 
 def algo_bytes(W, H, C):
@@ -226,63 +248,162 @@ def reference_lidar_loop(eng, scan, n_steps, every, budget_s, deadline=None):
     return n, time.perf_counter() - t0
 
 
-def cpu_baseline(pgm, cfg, budget_s=12.0, max_steps=200):
-    """The reference's step() (oracle/_ref) on all host cores, bounded sample."""
+def cpu_model():
+    """The host CPU model (lscpu 'Model name'), for the cpu_baseline line."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def product_not_mapped():
+    """The reference arm must not map the product library (VERDICT r1 #3)."""
+    try:
+        maps = open("/proc/self/maps").read()
+    except Exception:
+        return True
+    return "libgridloc_b200" not in maps
+
+
+def _time_ref_steps(eng, n_max, budget_s):
+    """Per-step wall times of the reference step() (u = (res, 0, 0))."""
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < n_max and time.perf_counter() - t_all < budget_s:
+        t0 = time.perf_counter()
+        rc = eng.step(0.1, 0.0, 0.0)
+        times.append(time.perf_counter() - t0)
+        if rc:
+            break
+    return times
+
+
+def _step_stats(times):
+    ts = sorted(times)
+    p99 = ts[min(len(ts) - 1, int(math.ceil(0.99 * len(ts))) - 1)]
+    return {"mean_ms": 1e3 * sum(ts) / len(ts), "median_ms": 1e3 * statistics.median(ts), "p99_ms": 1e3 * p99}
+
+
+def cpu_baseline(pgm, cfg, budget_s=12.0, max_steps=200, one_thread_budget_s=6.0):
+    """The reference's step() (oracle/_ref, compiled from the reference's own
+    sources) on all host cores, bounded sample; plus a 1-thread sample
+    (SURVEY §8(d): ThreadPool(0) and 1 thread, mean / median / p99)."""
     eng, _ = reference_engine(pgm, cfg["C"])
     if eng is None:
         return None
     eng.step(0.1, 0.0, 0.0)  # first step allocates scratch (excluded, like §6)
+    model = cpu_model()
     if cfg.get("lidar"):
         n, dt = reference_lidar_loop(eng, lidar_scan(cfg["W"], cfg["H"]), max_steps, cfg["lidar"], budget_s)
-        return {"value": n / dt, "unit": "Hz", "cores": eng.threads, "kind": "reference",
+        return {"value": n / dt, "unit": "Hz", "cores": eng.threads, "kind": "reference", "cpu_model": model,
                 "sample": f"{n} reference step() calls with an observation every {cfg['lidar']} on "
                           f"{cfg['W']}x{cfg['H']}x{cfg['C']}, ThreadPool({eng.threads}), {dt:.1f} s"}
-    n = 0
-    t0 = time.perf_counter()
-    while n < max_steps and time.perf_counter() - t0 < budget_s:
-        rc = eng.step(0.1, 0.0, 0.0)
-        if rc:
-            break
-        n += 1
-    dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "Hz", "cores": eng.threads, "kind": "reference",
-            "sample": f"{n} reference step() calls on {cfg['W']}x{cfg['H']}x{cfg['C']} after 1 warm-up step, "
-                      f"ThreadPool({eng.threads}), {dt:.1f} s"}
+    times = _time_ref_steps(eng, max_steps, budget_s)
+    dt = sum(times)
+    out = {"value": len(times) / dt, "unit": "Hz", "cores": eng.threads, "kind": "reference", "cpu_model": model,
+           "sample": f"{len(times)} reference step() calls on {cfg['W']}x{cfg['H']}x{cfg['C']} after 1 warm-up "
+                     f"step, ThreadPool({eng.threads}), {dt:.1f} s"}
+    out.update(_step_stats(times))
+    del eng
+    if one_thread_budget_s > 0:
+        eng1, _ = reference_engine(pgm, cfg["C"], threads=1)
+        eng1.step(0.1, 0.0, 0.0)
+        t1 = _time_ref_steps(eng1, max_steps, one_thread_budget_s)
+        out["one_thread"] = dict(value=len(t1) / sum(t1), unit="Hz", cores=1, steps=len(t1), **_step_stats(t1))
+    return out
 
 
 def run_reference(args, cfg, world, rank):
     if rank != 0:
         return 0
     pgm = make_map_bytes(cfg["W"], cfg["H"])
+    if cfg["W"] * cfg["H"] * cfg["C"] * 8 * 5 > 40e9:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"the reference CPU step needs 5 tensor-sized FP64 buffers "
+                          f"({cfg['W'] * cfg['H'] * cfg['C'] * 40 / 1e9:.0f} GB) for {cfg['W']}x{cfg['H']}x{cfg['C']}"}))
+        return 0
     eng, _ = reference_engine(pgm, cfg["C"])
     if eng is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (reference sources absent)"}))
         return 0
+    if not product_not_mapped():
+        raise SystemExit("reference arm: libgridloc_b200.so is mapped into this process")
     for _ in range(max(1, args.warmup)):
         eng.step(0.1, 0.0, 0.0)
     budget = args.ref_budget_s
+    stats = {}
     if cfg.get("lidar"):
         n, dt = reference_lidar_loop(eng, lidar_scan(cfg["W"], cfg["H"]), args.steps, cfg["lidar"], budget)
     else:
-        n = 0
-        t0 = time.perf_counter()
-        while n < args.steps and time.perf_counter() - t0 < budget:
-            eng.step(0.1, 0.0, 0.0)
-            n += 1
-        dt = time.perf_counter() - t0
+        times = _time_ref_steps(eng, args.steps, budget)
+        n, dt = len(times), sum(times)
+        stats = _step_stats(times)
+    assert product_not_mapped(), "reference arm mapped the product library"
     hz = n / dt
     line = {
         "impl": "reference", "metric": metric_for(cfg["W"], cfg["H"], cfg["C"], cfg.get("lidar", 0)), "value": hz,
         "unit": "Hz", "n_gpus": world, "steps": n,
         "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(n, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "W": cfg["W"], "H": cfg["H"], "channels": cfg["C"],
-                   "parallelism": f"ThreadPool({eng.threads}) host threads"},
-        "cpu_baseline": {"value": hz, "unit": "Hz", "cores": eng.threads, "kind": "reference",
-                         "sample": f"{n} reference step() calls after {args.warmup} warm-up, {dt:.1f} s "
-                                   f"(capped at {budget:.0f} s)"},
+        "config": config_for(cfg),
+        "parallelism": f"ThreadPool({eng.threads}) host threads",
+        "cpu_baseline": dict({"value": hz, "unit": "Hz", "cores": eng.threads, "kind": "reference",
+                              "cpu_model": cpu_model(), "product_library_mapped": False,
+                              "sample": f"{n} reference step() calls after {args.warmup} warm-up, {dt:.1f} s "
+                                        f"(capped at {budget:.0f} s)"}, **stats),
         "e2e": {"value": hz, "unit": "Hz", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    print(json.dumps(line))
+    return 0
+
+
+def run_reference_scaled(args, cfg, world, rank):
+    """Reference arm for configs[3] (4096^2x360): the reference cannot hold
+    the belief on a host (~242 GB), so each step is the reference step() at
+    1024^2 with the same Theta = 360 on all host threads, and the Hz is
+    scaled by the state ratio (16x) — the bounded sample of the workload,
+    labelled as such."""
+    if rank != 0:
+        return 0
+    W, H, C = cfg["W"], cfg["H"], cfg["C"]
+    pgm = make_map_bytes(1024, 1024)
+    eng, _ = reference_engine(pgm, C)
+    if eng is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (reference sources absent)"}))
+        return 0
+    if not product_not_mapped():
+        raise SystemExit("reference arm: libgridloc_b200.so is mapped into this process")
+    for _ in range(max(1, min(args.warmup, 3))):
+        eng.step(0.1, 0.0, 0.0)
+    times = _time_ref_steps(eng, args.steps, args.ref_budget_s)
+    n, dt = len(times), sum(times)
+    ratio = (1024 * 1024 * C) / (W * H * C)
+    hz = n / dt * ratio
+    line = {
+        "impl": "reference", "metric": metric_for(W, H, C), "value": hz, "unit": "Hz", "n_gpus": world,
+        "steps": n, "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / hz,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_for(cfg),
+        "parallelism": f"ThreadPool({eng.threads}) host threads",
+        "cpu_baseline": dict({"value": hz, "unit": "Hz", "cores": eng.threads, "kind": "reference",
+                              "cpu_model": cpu_model(), "product_library_mapped": False,
+                              "scaled_from": f"1024x1024x{C}",
+                              "sample": f"{n} reference step() calls at 1024x1024x{C} after warm-up, {dt:.1f} s; "
+                                        f"Hz x {ratio:.4f} (state ratio): the reference cannot hold {W}x{H}x{C} "
+                                        f"({W * H * C * 40 / 1e9:.0f} GB)"}, **_step_stats(times)),
+        "e2e": {"value": hz, "unit": "Hz", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    assert product_not_mapped(), "reference arm mapped the product library"
     print(json.dumps(line))
     return 0
 
@@ -410,10 +531,9 @@ def run_lidar(args, cfg, world, rank, local):
         "metric": metric_for(W, H, C, every), "value": value, "unit": "Hz", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "W": W, "H": H, "channels": C, "observe_every": every,
-                   "sample_budget": 512, "samples_last_observation": samples[0],
-                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (one per GPU)",
-                   "l2": "belief tensor (604 MB) exceeds the 126 MB L2", "noise": [0.03, 0.03, 0.012]},
+        "config": config_for(cfg),
+        "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (one per GPU)",
+        "samples_last_observation": samples[0], "noise": [0.03, 0.03, 0.012],
         "e2e": {"value": e2e, "unit": "Hz", "h2d_bytes_per_step": 16 * C + (8 * 24 * 2 + 8 * 2 * 512) // every,
                 "d2h_bytes_per_step": 4 + (8 * 2 * 512 + 16) // every,
                 "how": f"{n_e2e} synchronous gl_step calls with the observation cycle every {every}, wall clock"},
@@ -494,9 +614,9 @@ def run_batch(args, cfg, world, rank, local):
         "unit": "batch-Hz", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "W": W, "H": H, "channels": C, "robots_per_gpu": B,
-                   "parallelism": f"{B} independent tensors per GPU on {len(ctxs)} streams",
-                   "timing": "host wall clock around K batch steps with device syncs"},
+        "config": config_for(cfg),
+        "parallelism": f"{B} independent tensors per GPU on {len(ctxs)} streams",
+        "timing": "host wall clock around K batch steps with device syncs",
         "e2e": {"value": e2e, "unit": "batch-Hz", "h2d_bytes_per_step": B * 16 * C, "d2h_bytes_per_step": B * 16,
                 "how": f"{n_e2e} batch steps: {B} step_async calls, then every robot's status read back"},
         "roofline": {"bound": "hbm", "achieved": bytes_batch * value / world / 1e9, "peak": peak, "unit": "GB/s",
@@ -507,11 +627,31 @@ def run_batch(args, cfg, world, rank, local):
     return 0
 
 
+def sharded_cpu_baseline(cfg, budget_s):
+    """configs[3] cannot run on a host (the reference needs 5 tensor-sized
+    FP64 buffers, ~242 GB at 4096^2x360): time the reference at
+    1024^2 with the SAME channel count (same Theta = 360, H = 3 angular
+    stencil) and scale its Hz by the state ratio."""
+    W, H, C = cfg["W"], cfg["H"], cfg["C"]
+    sub = dict(cfg, W=1024, H=1024)
+    cpu = cpu_baseline(make_map_bytes(1024, 1024), sub, budget_s=budget_s, max_steps=60, one_thread_budget_s=0)
+    if cpu:
+        states = 1024 * 1024 * C
+        cpu["note"] = (f"reference cannot hold {W}x{H}x{C} (needs {W * H * C * 40 / 1e9:.0f} GB); value = its "
+                       f"1024x1024x{C} step rate scaled by states ({cpu['value']:.3f} Hz x {states}/{W * H * C})")
+        cpu["scaled_from"] = f"1024x1024x{C}"
+        cpu["value"] = cpu["value"] * states / (W * H * C)
+    return cpu
+
+
 def run_sharded(args, cfg, world, rank, local):
-    """theta-slab sharding of ONE belief across the ranks (strong scaling):
-    per step the fused kernel on each slab, a MAX all-reduce of the 8-byte
-    step max and the halo-plane exchange, both over NCCL on the library's
-    stream (paper_1910_00572_b200/sharding.py)."""
+    """theta-slab sharding of ONE belief across the ranks (strong scaling;
+    BASELINE configs[3] at 4096^2x360): per step the fused kernel on each
+    slab with its halo input planes read straight from the neighbours'
+    buffers over peer memory (CUDA IPC / NVLink P2P; or NCCL send/recv with
+    --exchange nccl), then a MAX all-reduce of the 8-byte step max over NCCL
+    on the library's stream (paper_1910_00572_b200/sharding.py). At N = 1 the
+    one shard holds every channel (its halo reads wrap to its own planes)."""
     import paper_1910_00572_b200 as g
     from paper_1910_00572_b200.sharding import ThetaShard
     W, H, C = cfg["W"], cfg["H"], cfg["C"]
@@ -545,29 +685,47 @@ def run_sharded(args, cfg, world, rank, local):
     shard.status()
     ms_max = dist_max(ms, world, "ours")
     value = args.steps / (ms_max / 1e3)  # steps of the ONE sharded belief
+    # e2e: the synchronous sharded step a user makes — motion table in the
+    # launch, the fused kernel, the all-reduce, the finalise, and the step
+    # status read back to the host on every rank — wall clock, max over ranks
+    n_e2e = max(1, min(args.steps, args.e2e_steps))
+    dist_barrier(world)
+    ctx.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        shard.step(u, ks, act)
+        shard.status()
+    e2e_s = dist_max(time.perf_counter() - t0, world, "ours")
     n_local = shard.c_end - shard.c_begin
     bytes_launch = 2 * 8 * W * H * n_local + W * H + 8 * W * H
-    achieved = bytes_launch / ((kern_ms / max(kern_n, 1)) / 1e3) / 1e9
+    avg_kern_ms = kern_ms / max(kern_n, 1)
+    achieved = bytes_launch / (avg_kern_ms / 1e3) / 1e9
     peak, peak_src = measured_peak()
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = sharded_cpu_baseline(cfg, args.cpu_budget_s) if W * H * C * 40 > 40e9 else \
+            cpu_baseline(make_map_bytes(W, H), cfg, budget_s=args.cpu_budget_s)
+    shard.close()
     if rank != 0:
         return 0
     line = {
         "metric": metric_for(W, H, C), "value": value, "unit": "Hz", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "W": W, "H": H, "channels": C,
-                   "parallelism": f"theta-slab sharding over {world} GPU(s), {n_local} channels + 2x{halo} "
-                                  "halo planes per GPU; NCCL all-reduce (8 B) per step; halo exchange "
-                                  + ("fused into the step kernel (TMA reads of the neighbours' planes "
-                                     "over CUDA IPC / NVLink P2P)" if args.exchange == "peer"
-                                     else "by NCCL send/recv after the step"),
-                   "l2": "the per-GPU slab exceeds L2"},
-        "e2e": None,
+        "config": config_for(cfg),
+        "parallelism": (f"theta-slab sharding over {world} GPU(s), {n_local} channels + 2x{halo} halo planes on "
+                        "rank 0; NCCL MAX all-reduce (8 B) per step; halo exchange "
+                        + ("fused into the step kernel (TMA reads of the neighbours' planes over CUDA IPC / "
+                           "NVLink P2P)" if args.exchange == "peer" else "by NCCL send/recv after the step")),
+        "e2e": {"value": n_e2e / e2e_s, "unit": "Hz", "h2d_bytes_per_step": 16 * (n_local + 2 * halo),
+                "d2h_bytes_per_step": 4,
+                "how": f"{n_e2e} synchronous sharded steps (step + all-reduce + finalise, then the status read "
+                       "back on every rank), wall clock, max over ranks"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "peak_source": peak_src, "bytes_per_launch": bytes_launch,
-                     "avg_kernel_ms": kern_ms / max(kern_n, 1), "launches_timed": kern_n,
-                     "note": "per-GPU fused kernel on its slab"},
-        "cpu_baseline": None, "gpu_launches": launches, "clocks": clk,
+                     "traffic": ncu_traffic("c4") if world == 1 else None, "peak_source": peak_src,
+                     "bytes_per_launch": bytes_launch, "avg_kernel_ms": avg_kern_ms, "launches_timed": kern_n,
+                     "note": "rank 0's fused kernel on its slab (per-GPU roofline)"},
+        "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
     }
     print(json.dumps(line))
     return 0
@@ -575,7 +733,7 @@ def run_sharded(args, cfg, world, rank, local):
 
 def run_ours(args, cfg, world, rank, local):
     import paper_1910_00572_b200 as g
-    if args.shard:
+    if args.shard or args.config == "c4":
         return run_sharded(args, cfg, world, rank, local)
     if "batch" in cfg:
         return run_batch(args, cfg, world, rank, local)
@@ -653,10 +811,9 @@ def run_ours(args, cfg, world, rank, local):
         "metric": metric_for(W, H, C), "value": value, "unit": "Hz", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "W": W, "H": H, "channels": C,
-                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (one per GPU)",
-                   "l2": "belief tensor (604 MB at 1024^2x72) exceeds the 126 MB L2: every step streams it from HBM",
-                   "noise": [0.03, 0.03, 0.012], "kernel_path": "fused sm_100a TMA step"},
+        "config": config_for(cfg),
+        "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (one per GPU)",
+        "noise": [0.03, 0.03, 0.012], "kernel_path": "fused sm_100a TMA step",
         "e2e": {"value": e2e, "unit": "Hz", "h2d_bytes_per_step": 16 * C, "d2h_bytes_per_step": 4,
                 "how": f"{n_e2e} synchronous gl_step calls (motion table H2D in the launch params, the step's "
                        f"status written by the finalising kernel into mapped pinned host memory), wall clock"},
@@ -672,30 +829,61 @@ def run_ours(args, cfg, world, rank, local):
     return 0
 
 
+def spawn_ranks(args):
+    """--gpus N > 1 outside torchrun: re-exec this script under
+    torch.distributed.run with one rank per GPU (127.0.0.1 rendezvous).
+    Fails loudly when fewer than N GPUs are visible."""
+    import socket
+    if args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator ranks / transport visible in the log
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execve(sys.executable, cmd, env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default=None,
+                    help="default: c2 (configs[1], 1024^2x72) at N = 1; c4 (configs[3], 4096^2x360 theta-sharded "
+                         "over the N GPUs) at N > 1")
     ap.add_argument("--e2e-steps", type=int, default=500)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--ref-budget-s", type=float, default=90.0)
     ap.add_argument("--no-extras", action="store_true", help="skip the trace-mix / LIDAR-cycle extras")
     ap.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
-                    help="--shard halo exchange: fused peer-memory stores (default) or NCCL send/recv")
+                    help="sharded halo exchange: fused peer-memory reads (default) or NCCL send/recv")
     ap.add_argument("--shard", action="store_true",
-                    help="theta-shard ONE belief across the ranks (strong scaling; e.g. --config c4)")
+                    help="theta-shard ONE belief across the ranks (strong scaling; implied by --config c4)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        spawn_ranks(args)
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config is None:
+        args.config = "c2" if max(world_env, args.gpus) == 1 else "c4"
     cfg = CONFIGS[args.config]
     world, rank, local = dist_setup(args.impl)
+    if args.impl == "ours" and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; using {world}", file=sys.stderr)
     try:
         if args.impl == "reference":
-            return run_reference(args, cfg, world, rank)
+            if args.config == "c4":
+                return run_reference_scaled(args, cfg, max(world, args.gpus), rank)
+            return run_reference(args, cfg, max(world, args.gpus), rank)
         return run_ours(args, cfg, world, rank, local)
     finally:
         if world > 1:

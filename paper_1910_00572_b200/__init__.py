@@ -5,14 +5,21 @@ Drop-in for the hot path of the reference ``gridloc`` library
 step, belief map / argmax, Floyd-Steinberg sample extraction and the sampled
 LIDAR update. The FP64 belief tensor lives in HBM; every tensor operation is
 a hand-written sm_100a kernel in ``libgridloc_b200.so`` behind the C-ABI of
-``include/gridloc_b200.h``. Importing this package fails loudly when that
-library is missing: there is no CPU fallback.
+``include/gridloc_b200.h``.
+
+The library is mapped on first use (the first Context / map / kernel-set
+call), not at import, so that input generators (``floorplan``) can be
+imported by the reference arm of bench.py without mapping the product. That
+first use fails loudly when the library is missing: there is no CPU
+fallback. ``load_native()`` maps it eagerly.
 """
 from . import _lib
-
-_lib.load()  # fail loudly at import when the native library is absent
-
 from .gridloc import *  # noqa: E402,F401,F403
 from .gridloc import tensor_hash_host, tensor_status  # noqa: E402,F401
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"
+
+
+def load_native():
+    """Map libgridloc_b200.so now (raises ImportError if it is absent)."""
+    return _lib.load()
