@@ -90,6 +90,15 @@ gl_status gl_context_set_channel_chunks(gl_context* ctx, int n);
  * auto (the last ~1/5 of the partial wave, default chunks 3), 0: off.
  * Results are bit-identical for every setting. */
 gl_status gl_context_set_wave_tail(gl_context* ctx, int ctas, int chunks);
+/* Fused-step tile order: which tiles run side by side. strip_tiles 0 =
+ * row-major (tile rows across the whole width); n >= 1 = vertical strips n
+ * tiles wide, walked row by row inside a strip, so a tile's upper and lower
+ * neighbours run within ~n warps of it and their shared halo rows are still
+ * in L2 (at 4096^2 a full tile row is 137 tiles and the neighbour's rows
+ * were evicted before it ran); -1 = auto. stack n >= 2: the warps of a CTA
+ * take n vertically adjacent tiles (they run in lockstep) instead of n
+ * side-by-side ones; 0 = auto. Results are bit-identical for every setting. */
+gl_status gl_context_set_tile_order(gl_context* ctx, int strip_tiles, int stack);
 /* scan_likelihood's final exp (the per-pose geometric mean,
  * observation.cpp:110): 1 (default) evaluates it with the host's libm like the
  * reference (bit-exact; one D2H/H2D of <= 512*Theta doubles per observation),

@@ -76,6 +76,7 @@ SIGNATURES = {
     "gl_context_set_channel_chunks": [_vp, C.c_int],
     "gl_context_set_wave_tail": [_vp, C.c_int, C.c_int],
     "gl_context_set_host_exp": [_vp, C.c_int],
+    "gl_context_set_tile_order": [_vp, C.c_int, C.c_int],
     "gl_shard_init_uniform": [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _pvp],
     "gl_shard_info": [_vp, _ip, _ip, _ip, _ip],
     "gl_tensor_plane_ptr": [_vp, _vp, C.c_int, C.POINTER(_dp)],

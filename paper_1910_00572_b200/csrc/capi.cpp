@@ -465,6 +465,16 @@ gl_status gl_context_set_wave_tail(gl_context* ctx, int ctas, int chunks) {
   });
 }
 
+gl_status gl_context_set_tile_order(gl_context* ctx, int strip_tiles, int stack) {
+  return guard([&] {
+    need(ctx, "null context");
+    need(strip_tiles >= -1, "tile order must be >= -1 (-1 = auto, 0 = row-major, n = strips of n tiles)");
+    need(stack >= 0, "tile stack must be >= 0");
+    ctx->strip_tiles = strip_tiles;
+    ctx->tile_stack = stack;
+  });
+}
+
 gl_status gl_context_launch_count(gl_context* ctx, uint64_t* n) {
   return guard([&] {
     need(ctx && n, "null argument");

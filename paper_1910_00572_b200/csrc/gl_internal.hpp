@@ -89,6 +89,8 @@ struct gl_context {
   int channel_chunks = 0;  // fused step channel chunks: 0 auto, n >= 1 fixed
   int tail_ctas = -1;      // fused step wave-tail split: -1 auto, 0 off, n CTAs
   int tail_chunks = 3;     // channel chunks of each wave-tail CTA's tiles
+  int strip_tiles = -1;    // fused step tile order: -1 auto, 0 row-major, n: vertical strips n tiles wide
+  int tile_stack = 0;      // fused step: 0/1 a CTA's warps take side-by-side tiles, n: n stacked vertically
   bool host_exp = true;    // likelihood geometric mean: exp by host glibc (exact)
   void* d_kind = nullptr;  // likelihood case codes
   size_t kind_bytes = 0;

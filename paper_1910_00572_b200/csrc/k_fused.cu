@@ -67,6 +67,13 @@
 #define GL_FUSED_INVREG_ROWS_H3 8
 #endif
 
+#ifndef GL_FUSED_STRIP_W
+#define GL_FUSED_STRIP_W 8       // auto tile order: strip width in tiles ...
+#endif
+#ifndef GL_FUSED_STRIP_MIN_TX
+#define GL_FUSED_STRIP_MIN_TX 1000000  // ... for grids at least this many tiles wide (off until measured)
+#endif
+
 namespace glb {
 
 namespace {
@@ -147,6 +154,9 @@ struct FusedParams {
   int defer_finalize;        // shard: leave the local max for a cross-rank all-reduce
 
   int tiles_x, n_tiles;
+  int tiles_y, strip_w;      // tile order: vertical strips strip_w tiles wide (0: row-major)
+  int stack, grid_y;         // stack > 1: a CTA's warps take `stack` vertically adjacent tiles
+                             // (ordering grid tiles_x x grid_y of such stacks)
   int k_base, k_end;         // this launch's output channels (a window of <= kParamChannels - 2H)
   int k_chunk, n_chunks;     // output channels per warp, chunks per tile
   // wave-tail split: the CTAs from head_ctas on (the last tiles) run their
@@ -544,6 +554,46 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
   return vmax;
 }
 
+// Tile index -> (tile column, tile row). The ordering grid is tiles_x x
+// grid_y cells; a cell is one tile, or (stack > 1) `stack` vertically
+// adjacent tiles taken by consecutive warps of one CTA, so vertical
+// neighbours inside a CTA run in lockstep. Cells go row-major, or in
+// vertical strips of strip_w cell columns walked row by row (the last strip
+// takes the remaining columns): the cell below then follows strip_w cells
+// later instead of a whole grid row later, so a tile's upper / lower
+// neighbours run at nearly the same time and the halo rows they share are
+// re-read from L2, not DRAM (gl_context_set_tile_order). A tile row past the
+// grid (stack padding) comes back >= tiles_y.
+__device__ __forceinline__ void tile_coords(const FusedParams& p, int tile, int* tx, int* ty) {
+  int cell = tile, w = 0;
+  if (p.stack > 1) {
+    cell = tile / p.stack;
+    w = tile - cell * p.stack;
+  }
+  const int sw = p.strip_w;
+  int cx, cy;
+  if (sw <= 0 || sw >= p.tiles_x) {
+    cy = cell / p.tiles_x;
+    cx = cell - cy * p.tiles_x;
+  } else {
+    const int per_strip = sw * p.grid_y;
+    const int full = p.tiles_x / sw;
+    const int s = cell / per_strip;
+    if (s < full) {
+      const int q = cell - s * per_strip;
+      cy = q / sw;
+      cx = s * sw + (q - cy * sw);
+    } else {
+      const int rem = p.tiles_x - full * sw;
+      const int q = cell - full * per_strip;
+      cy = q / rem;
+      cx = full * sw + (q - cy * rem);
+    }
+  }
+  *tx = cx;
+  *ty = cy * (p.stack > 1 ? p.stack : 1) + w;
+}
+
 template <int R, int H, int ROWS, int NS, int NWARP, bool FAST, bool HIMAX, bool TMA>
 __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_MINB_H3)
     k_fused_step(const __grid_constant__ CUtensorMap tmap,
@@ -591,10 +641,15 @@ __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_
     k0 = p.k_base + chunk * p.tail_k;
     n_out = min(p.tail_k, p.k_end - k0);
   }
-  const bool active = tile_raw < p.n_tiles;
-  const int tile = active ? tile_raw : p.n_tiles - 1;
-  const int x0 = (tile % p.tiles_x) * G::OW;
-  const int y0 = (tile / p.tiles_x) * ROWS;
+  bool active = tile_raw < p.n_tiles;
+  int tx, ty;
+  tile_coords(p, active ? tile_raw : p.n_tiles - 1, &tx, &ty);
+  if (ty >= p.tiles_y) {  // stack padding below the grid: redo the last row, stores off
+    ty = p.tiles_y - 1;
+    active = false;
+  }
+  const int x0 = tx * G::OW;
+  const int y0 = ty * ROWS;
   double vmax = warp_tile<R, H, ROWS, NS, FAST, HIMAX, TMA>(&tmap, &tmap_lo, &tmap_hi, p, Bs, mbar, lane, x0, y0, k0,
                                                        n_out, active, invs);
 
@@ -724,6 +779,12 @@ inline int auto_tail_ctas(const gl_context* ctx, int blocks) {
   return ((blocks % slots) / 5) & ~31;
 }
 
+// Auto tile order: row-major until measured otherwise (set per shape class
+// from the bench sweeps).
+inline int auto_strip_tiles(int tiles_x) {
+  return tiles_x >= GL_FUSED_STRIP_MIN_TX ? GL_FUSED_STRIP_W : 0;
+}
+
 template <int R, int H, bool FAST, bool HIMAX, bool TMA>
 void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& fp) {
   const int n_win = fp.k_end - fp.k_base;
@@ -739,7 +800,13 @@ void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& f
     configured |= bit;
   }
   fp.tiles_x = (fp.w + G::OW - 1) / G::OW;
-  fp.n_tiles = fp.tiles_x * ((fp.h + ROWS - 1) / ROWS);
+  fp.tiles_y = (fp.h + ROWS - 1) / ROWS;
+  // tile order: strips only pay where a full tile row is long enough that
+  // its upper neighbour's halo rows leave L2 before the row below runs
+  fp.strip_w = ctx->strip_tiles >= 0 ? ctx->strip_tiles : auto_strip_tiles(fp.tiles_x);
+  fp.stack = ctx->tile_stack > 0 ? std::min(ctx->tile_stack, kNWARP) : 1;
+  fp.grid_y = (fp.tiles_y + fp.stack - 1) / fp.stack;
+  fp.n_tiles = fp.tiles_x * fp.grid_y * fp.stack;  // ordering cells x their stacks (padding rows inactive)
   // Small grids leave SMs idle with one warp per tile: split the channels
   // into chunks (each recomputes its 2H angular neighbours) until one full
   // wave of resident warps (16 per SM) exists, keeping the recompute below

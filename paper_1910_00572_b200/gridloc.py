@@ -168,6 +168,18 @@ class Context:
         3 chunks; 0 off). Bit-identical."""
         check(self.lib.gl_context_set_wave_tail(self.h, int(ctas), int(chunks)))
 
+    def set_host_exp(self, enable: bool):
+        """scan_likelihood's final exp: host glibc (default, bit-exact) or
+        CUDA's exp on the device (<= 1 ulp)."""
+        check(self.lib.gl_context_set_host_exp(self.h, int(enable)))
+
+    def set_tile_order(self, strip_tiles: int, stack: int = 0):
+        """Fused-step tile order: strip_tiles -1 auto, 0 row-major, n =
+        vertical strips of n tiles; stack n >= 2: a CTA's warps take n
+        vertically adjacent tiles (L2 reuse of the vertical halo rows).
+        Bit-identical for every setting."""
+        check(self.lib.gl_context_set_tile_order(self.h, int(strip_tiles), int(stack)))
+
     def synchronize(self):
         check(self.lib.gl_context_synchronize(self.h))
 

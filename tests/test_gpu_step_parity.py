@@ -67,6 +67,7 @@ CASES = [
     ("twin", 8, (0.05, 0.05, 2.0)),             # folded angular kernel (generic)
     ("random37x29", 16, (0.03, 0.03, 0.012)),   # odd width: TMA needs even W -> generic
     ("floor130x70", 72, (0.2, 0.2, 0.012)),     # isotropic r=6 (generic separable)
+    ("random40x32", 12, (0.3, 0.2, 0.1)),       # anisotropic r=9: convolve_plane's generic interior order
 ]
 
 
@@ -79,6 +80,8 @@ def _map(name):
         return random_map(28, 22, 0.12, 55)
     if name == "random16x16":
         return random_map(16, 16, 0.15, 42)
+    if name == "random40x32":
+        return random_map(40, 32, 0.1, 91)
     if name == "random37x29":
         return random_map(37, 29, 0.15, 7)
     if name == "empty40x40":
