@@ -99,6 +99,17 @@ gl_status gl_context_set_wave_tail(gl_context* ctx, int ctas, int chunks);
  * take n vertically adjacent tiles (they run in lockstep) instead of n
  * side-by-side ones; 0 = auto. Results are bit-identical for every setting. */
 gl_status gl_context_set_tile_order(gl_context* ctx, int strip_tiles, int stack);
+/* Wall-crossing mask (an EXTENSION named by the north star, off by default;
+ * the reference masks destination cells only, belief_tensor.cpp:414-416):
+ * with enable = 1, step() also drops every bilinear tap whose straight
+ * segment between source and destination cell centres passes through the
+ * interior of an occupied cell (corner touches excepted), so no mass jumps
+ * through a wall. Fused into the step kernel's shift stage (a per-warp
+ * occupancy bit window; the per-channel crossed-cell lists come from the
+ * host); steps whose motion the kernel's table cannot hold (|floor(d)| > 7,
+ * > 16 distinct floors) run the generic chain. Parity for this mode is
+ * against the oracle's restatement (oracle/gl_oracle.c glo_step_wall). */
+gl_status gl_context_set_wall_mask(gl_context* ctx, int enable);
 /* scan_likelihood's final exp (the per-pose geometric mean,
  * observation.cpp:110): 1 (default) evaluates it with the host's libm like the
  * reference (bit-exact; one D2H/H2D of <= 512*Theta doubles per observation),
@@ -204,6 +215,16 @@ gl_status gl_tensor_clone(gl_context* ctx, gl_tensor* src, gl_tensor** out);
 /* Order-independent 64-bit hash of the tensor's bits, computed on the device:
  * sum over p of splitmix64(bits_p + p * 0x9e3779b97f4a7c15) (parity checks). */
 gl_status gl_tensor_hash(gl_context* ctx, gl_tensor* t, uint64_t* hash);
+/* The same hash of a theta-slab shard's interior taken as the elements
+ * p0 .. p0+n-1 of the whole tensor: the shards' hashes add up (mod 2^64) to
+ * the unsharded tensor's gl_tensor_hash. */
+gl_status gl_tensor_hash_at(gl_context* ctx, gl_tensor* t, uint64_t p0, uint64_t* hash);
+/* argmax_state's building block (belief_tensor.cpp:512-541): the first
+ * strict maximum of the (interior) tensor in [k][j][i] order, its flat
+ * index and the pairwise device sum of all values (multi-shard argmax
+ * combines these; value <= 0 means no positive mass). */
+gl_status gl_tensor_argmax_candidate(gl_context* ctx, gl_tensor* t, double* value, int64_t* flat,
+                                     double* sum);
 /* Raw device pointer of the current buffer (for NCCL halo exchange). */
 gl_status gl_tensor_device_ptr(gl_context* ctx, gl_tensor* t, double** dptr);
 
@@ -381,6 +402,54 @@ typedef struct {
 gl_status gl_map_difficulty(gl_context* ctx, const gl_map* map,
                             const gl_field* field,
                             const gl_difficulty_config* cfg, double* out);
+
+/* ---- multi-device engine (SURVEY.md §8(b) "gl_engine ... device list",
+ * §8(e)) -------------------------------------------------------------------
+ * ONE process driving a theta-slab sharded belief over a device list — the
+ * C++ callers' form of the multi-GPU path (the Python ThetaShard does the
+ * same over torch.distributed, one process per GPU). Shard s owns channels
+ * [s*C/n, (s+1)*C/n) on devices[s] (a device may repeat: shards then share
+ * it). Per step every shard's fused kernel reads its halo input planes
+ * straight from its neighbours' buffers over NVLink P2P (no exchange step),
+ * then the 8-byte step max is MAX-all-reduced — by NCCL (ncclAllReduce,
+ * uint64, ncclMax; needs distinct devices) or by a peer-memory gather
+ * kernel on every device after a cross-device event barrier (P2P) — and
+ * every shard finalises the extinguish status and the pending 1/max rescale
+ * identically. Observation: per-shard belief maps MAX-combined onto shard
+ * 0, Floyd-Steinberg there, every shard's likelihoods at the samples, the
+ * max all-reduced again. argmax: per-shard candidates, the reference's
+ * lowest-flat-index rule. Results are bitwise the unsharded tensor's. */
+typedef struct gl_engine gl_engine;
+enum { GL_ENGINE_AUTO = 0, GL_ENGINE_NCCL = 1, GL_ENGINE_P2P = 2 };
+/* map: W*H occupancy (1 = occupied; ring forced); n_devices <= 16; mode
+ * AUTO = NCCL when the devices are distinct and libnccl loads, else P2P. */
+gl_status gl_engine_create(const int* devices, int n_devices, int width, int height, double resolution,
+                           double origin_x, double origin_y, const uint8_t* occ, int channels, int mode,
+                           gl_engine** out);
+gl_status gl_engine_destroy(gl_engine* e);
+/* shards, the reduction mode in use (NCCL / P2P), halo planes per side */
+gl_status gl_engine_info(const gl_engine* e, int* n_shards, int* mode, int* halo);
+/* Kernel slot (0 = main, 1 = rotation-only, like Localizer): the taps are
+ * copied to every device and the activation built there. Every slot's
+ * angular half-width must fit the halo (the first slot set fixes it). */
+gl_status gl_engine_set_kernels(gl_engine* e, int slot, const gl_kernels* kernels);
+gl_status gl_engine_init_uniform(gl_engine* e);
+gl_status gl_engine_step(gl_engine* e, double u, double v, double w, int slot);
+gl_status gl_engine_step_async(gl_engine* e, double u, double v, double w, int slot);
+gl_status gl_engine_status(gl_engine* e);
+gl_status gl_engine_argmax(gl_engine* e, gl_pose_estimate* out);
+gl_status gl_engine_belief_map(gl_engine* e, double* host_out);
+/* Localizer::observe's update (localizer.cpp:55-58) on the sharded belief:
+ * dither_samples(belief_map, budget) + observation_update; the samples in
+ * emission order go to cells (at most cap pairs; *n is the full count). */
+gl_status gl_engine_observe(gl_engine* e, int budget, const double* angles, const double* ranges,
+                            int n_beams, double max_range, gl_likelihood params, int32_t* cells, int cap,
+                            int* n, double* source_mass);
+gl_status gl_engine_download(gl_engine* e, double* host, double* theta_t);
+gl_status gl_engine_upload(gl_engine* e, const double* host, double theta_t);
+gl_status gl_engine_hash(gl_engine* e, uint64_t* hash);
+/* the shard's context (per-shard tuning / timing), 0 <= s < n_shards */
+gl_status gl_engine_context(gl_engine* e, int s, gl_context** ctx);
 
 #ifdef __cplusplus
 }

@@ -612,6 +612,145 @@ class Localizer {  // localizer.hpp:28-71, localizer.cpp:7-66
   int steps_run_ = 0;
 };
 
+// ------------------------------------------------- multi-device engine
+// one process driving a theta-slab sharded belief over
+// a device list (gl_engine_*). Results are bitwise the single-tensor ones.
+class ShardedEngine {
+ public:
+  ShardedEngine(const std::vector<int>& devices, const OccupancyMap& map, int channels, int mode = GL_ENGINE_AUTO)
+      : channels_(channels), w_(map.width()), h_(map.height()) {
+    gl_engine* e = nullptr;
+    check(gl_engine_create(devices.data(), static_cast<int>(devices.size()), map.width(), map.height(),
+                           map.resolution(), map.origin_x(), map.origin_y(), map.cells().data(), channels, mode, &e));
+    e_.reset(e, [](gl_engine* p) { gl_engine_destroy(p); });
+  }
+  void set_kernels(int slot, const KernelSet& k, ThreadPool& pool) { check(gl_engine_set_kernels(get(), slot, k.get(pool))); }
+  void init_uniform() { check(gl_engine_init_uniform(get())); }
+  void step(const OdometryDelta& u, int slot) { check(gl_engine_step(get(), u.u, u.v, u.w, slot)); }
+  PoseEstimate argmax() const {
+    gl_pose_estimate e;
+    check(gl_engine_argmax(get(), &e));
+    PoseEstimate p;
+    p.pose = Pose2{e.x, e.y, e.theta};
+    p.confidence = e.confidence;
+    p.i = e.i, p.j = e.j, p.k = e.k;
+    return p;
+  }
+  Grid2d belief_map() const {
+    Grid2d g(w_, h_);
+    check(gl_engine_belief_map(get(), g.data.data()));
+    return g;
+  }
+  SampleSet observe(int budget, const LidarScan& scan, const LikelihoodParams& params) {
+    if (scan.angles.empty() || scan.angles.size() != scan.ranges.size())
+      throw std::invalid_argument("scan must have matching, nonempty beams");
+    const int cap = budget * 4 + 64;
+    std::vector<int32_t> cells(2 * static_cast<size_t>(cap));
+    int n = 0;
+    double mass = 0.0;
+    check(gl_engine_observe(get(), budget, scan.angles.data(), scan.ranges.data(),
+                            static_cast<int>(scan.angles.size()), scan.max_range,
+                            gl_likelihood{params.sigma_hit, params.weight_floor, params.beam_stride}, cells.data(), cap,
+                            &n, &mass));
+    SampleSet s;
+    s.source_mass = mass;
+    for (int q = 0; q < n && q < cap; ++q) s.cells.emplace_back(cells[2 * q], cells[2 * q + 1]);
+    return s;
+  }
+  std::vector<double> values() const {
+    std::vector<double> v(static_cast<size_t>(channels_) * w_ * h_);
+    check(gl_engine_download(get(), v.data(), nullptr));
+    return v;
+  }
+  double theta_t() const {
+    double th = 0.0;
+    std::vector<double> v(static_cast<size_t>(channels_) * w_ * h_);
+    check(gl_engine_download(get(), v.data(), &th));
+    return th;
+  }
+  uint64_t hash() const {
+    uint64_t h = 0;
+    check(gl_engine_hash(get(), &h));
+    return h;
+  }
+  int shards() const {
+    int n = 0;
+    check(gl_engine_info(get(), &n, nullptr, nullptr));
+    return n;
+  }
+  gl_engine* get() const { return e_.get(); }
+
+ private:
+  std::shared_ptr<gl_engine> e_;
+  int channels_, w_, h_;
+};
+
+// Localizer (localizer.hpp:28-71, localizer.cpp:7-66) over a ShardedEngine:
+// the same trigger / flush / observe / estimate logic, the belief sharded
+// over `devices`.
+class ShardedLocalizer {
+ public:
+  ShardedLocalizer(const OccupancyMap& map, const DistanceField& field, const LocalizerConfig& config,
+                   const std::vector<int>& devices, int mode = GL_ENGINE_AUTO,
+                   ThreadPool& pool = ThreadPool::default_pool())
+      : map_(map),
+        field_(field),
+        config_(config),
+        engine_(devices, map, config.channels, mode),
+        trigger_trans_m_(config.trigger_cells * map.resolution()),
+        trigger_rot_(M_PI / config.channels) {
+    const double dth = 2.0 * M_PI / config.channels;
+    const KernelSet k = build_kernels(config.motion_noise, config.channels, map.resolution(), dth);
+    const KernelSet rk = build_kernels(MotionNoise{1e-4, 1e-4, config.motion_noise.sigma_theta}, config.channels,
+                                       map.resolution(), dth);
+    engine_.set_kernels(0, k, pool);
+    engine_.set_kernels(1, rk, pool);
+    engine_.init_uniform();
+  }
+
+  bool integrate_odometry(const OdometryDelta& delta) {
+    pending_ = compose_delta(pending_, delta);
+    if (std::hypot(pending_.u, pending_.v) >= trigger_trans_m_ || std::fabs(pending_.w) >= trigger_rot_) {
+      flush();
+      return true;
+    }
+    return false;
+  }
+  void observe(const LidarScan& scan) {
+    if (!config_.use_samples) return;
+    constexpr double kEps = 1e-12;
+    if (std::fabs(pending_.u) > kEps || std::fabs(pending_.v) > kEps || std::fabs(pending_.w) > kEps) flush();
+    engine_.observe(config_.sample_budget, scan, config_.likelihood);
+  }
+  PoseEstimate estimate() const {
+    PoseEstimate est = engine_.argmax();
+    est.pose = compose(est.pose, pending_);
+    est.pose.theta = wrap_angle(est.pose.theta);
+    return est;
+  }
+  void flush() {
+    const bool translated = std::hypot(pending_.u, pending_.v) >= 0.5 * trigger_trans_m_;
+    engine_.step(pending_, translated ? 0 : 1);
+    pending_ = OdometryDelta{};
+    ++steps_run_;
+  }
+  std::vector<double> belief_values() const { return engine_.values(); }
+  const ShardedEngine& engine() const { return engine_; }
+  ShardedEngine& engine() { return engine_; }
+  const OdometryDelta& pending() const { return pending_; }
+  int steps_run() const { return steps_run_; }
+
+ private:
+  const OccupancyMap& map_;
+  const DistanceField& field_;
+  LocalizerConfig config_;
+  ShardedEngine engine_;
+  OdometryDelta pending_{};
+  double trigger_trans_m_;
+  double trigger_rot_;
+  int steps_run_ = 0;
+};
+
 // ---------------------------------------------------------- wire formats
 // the recorded-log inputs that feed the device Localizer.
 // Host-side parsing with the reference's record grammar, clamping and

@@ -102,6 +102,9 @@ class Port:
         L.glo_init_uniform.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, _dp]
         L.glo_step.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_double, _dp, C.c_double, C.c_double, C.c_double,
                                _u8p, C.POINTER(_Kernels), _dp]
+        L.glo_step_wall.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_double, _dp, C.c_double, C.c_double,
+                                    C.c_double, _u8p, C.POINTER(_Kernels), _dp, C.c_int]
+        L.glo_seg_cells.argtypes = [C.c_int, C.c_int, _ip, _ip, C.c_int]
         L.glo_apply_motion.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_double, _dp, C.c_double, C.c_double, C.c_double]
         L.glo_belief_map.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp]
         L.glo_argmax.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
@@ -169,14 +172,26 @@ class Port:
             raise OracleError(rc, "init_uniform")
         return out
 
-    def step(self, B, theta_t, u, v, dw, occ, cell, ks: Kernels, inv):
-        """In-place step on B (C,H,W) float64; returns (status, theta_t)."""
+    def step(self, B, theta_t, u, v, dw, occ, cell, ks: Kernels, inv, wall: bool = False):
+        """In-place step on B (C,H,W) float64; returns (status, theta_t).
+        wall: the wall-crossing mask extension (glo_step_wall)."""
         Cn, h, w = B.shape
         th = C.c_double(theta_t)
         occ = np.ascontiguousarray(occ, dtype=np.uint8)
-        rc = self.lib.glo_step(_d(B), w, h, Cn, cell, C.byref(th), u, v, dw, _u8(occ),
-                               C.byref(self._ks(ks, Cn)), _d(inv))
+        if wall:
+            rc = self.lib.glo_step_wall(_d(B), w, h, Cn, cell, C.byref(th), u, v, dw, _u8(occ),
+                                        C.byref(self._ks(ks, Cn)), _d(inv), 1)
+        else:
+            rc = self.lib.glo_step(_d(B), w, h, Cn, cell, C.byref(th), u, v, dw, _u8(occ),
+                                   C.byref(self._ks(ks, Cn)), _d(inv))
         return rc, th.value
+
+    def seg_cells(self, ox, oy, cap=64):
+        """Cells the tap offset (ox, oy) crosses, relative to the destination."""
+        qx = np.zeros(cap, np.int32)
+        qy = np.zeros(cap, np.int32)
+        n = self.lib.glo_seg_cells(ox, oy, _i(qx), _i(qy), cap)
+        return list(zip(qx[:min(n, cap)].tolist(), qy[:min(n, cap)].tolist())), n
 
     def apply_motion(self, B, theta_t, u, v, dw, cell):
         Cn, h, w = B.shape

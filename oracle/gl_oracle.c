@@ -132,17 +132,57 @@ void glo_motion_vector(double u, double v, int k, double theta_t,
 
 /* ---------------------------------------------------------------- planes */
 
+/* Wall-crossing mask (north-star kernel (2); NOT in the reference, which
+ * masks destination cells only, belief_tensor.cpp:414-416). A bilinear tap
+ * moves mass from source cell s to destination d = s + o (o integer). It is
+ * blocked when the open segment between the two cell centres passes through
+ * the open interior of an occupied cell other than s and d (corner touches
+ * do not count). Exact integer test: cell c (relative to s) is crossed iff
+ * some t in (0,1) has |t*ox - cx| < 1/2 and |t*oy - cy| < 1/2. */
+static int seg_crosses(long ox, long oy, long cx, long cy) {
+  long lo_n = 0, lo_d = 1, hi_n = 1, hi_d = 1; /* t in (lo, hi) */
+  const long o[2] = {ox, oy}, c[2] = {cx, cy};
+  for (int a = 0; a < 2; ++a) {
+    if (o[a] == 0) {
+      if (c[a] != 0) return 0;
+      continue;
+    }
+    const long m = o[a] < 0 ? -o[a] : o[a];
+    const long cc = o[a] < 0 ? -c[a] : c[a];
+    const long ln = 2 * cc - 1, hn = 2 * cc + 1, d = 2 * m;
+    if (ln * lo_d > lo_n * d) { lo_n = ln; lo_d = d; }
+    if (hn * hi_d < hi_n * d) { hi_n = hn; hi_d = d; }
+  }
+  return lo_n * hi_d < hi_n * lo_d;
+}
+
+static int tap_blocked(const uint8_t* occ, int w, int h, long si, long sj, long ox, long oy) {
+  const long x0 = ox < 0 ? ox : 0, x1 = ox < 0 ? 0 : ox;
+  const long y0 = oy < 0 ? oy : 0, y1 = oy < 0 ? 0 : oy;
+  for (long cy = y0; cy <= y1; ++cy)
+    for (long cx = x0; cx <= x1; ++cx) {
+      if ((cx == 0 && cy == 0) || (cx == ox && cy == oy)) continue;
+      if (!seg_crosses(ox, oy, cx, cy)) continue;
+      const long i = si + cx, j = sj + cy;
+      if (i < 0 || i >= w || j < 0 || j >= h || occ[j * w + i]) return 1;
+    }
+  return 0;
+}
+
 /* shift_plane, belief_tensor.cpp:67-124. Integral (dx,dy) copies exactly
  * (:71-86); otherwise the 4-tap blend accumulates w00, w10, w01, w11 from
- * 0.0, skipping taps outside the grid (:107-122). */
+ * 0.0, skipping taps outside the grid (:107-122). wall != NULL: taps
+ * blocked by the wall-crossing rule above are skipped too. */
 static void shift(const double* in, double* out, int w, int h, double dx,
-                  double dy) {
+                  double dy, const uint8_t* wall) {
   if (round(dx) == dx && round(dy) == dy) {
     const long ix = (long)dx, iy = (long)dy;
     for (long j = 0; j < h; ++j)
       for (long i = 0; i < w; ++i) {
         const long si = i - ix, sj = j - iy;
-        out[j * w + i] = (si >= 0 && si < w && sj >= 0 && sj < h) ? in[sj * w + si] : 0.0;
+        const int ok = si >= 0 && si < w && sj >= 0 && sj < h &&
+                       !(wall && tap_blocked(wall, w, h, si, sj, ix, iy));
+        out[j * w + i] = ok ? in[sj * w + si] : 0.0;
       }
     return;
   }
@@ -158,13 +198,30 @@ static void shift(const double* in, double* out, int w, int h, double dx,
       const long c0 = i - sx, c1 = i - sx - 1;
       const int k0 = c0 >= 0 && c0 < w, k1 = c1 >= 0 && c1 < w;
       double acc = 0.0;
-      if (ok0 && k0) acc += w00 * in[r0 * w + c0];
-      if (ok0 && k1) acc += w10 * in[r0 * w + c1];
-      if (ok1 && k0) acc += w01 * in[r1 * w + c0];
-      if (ok1 && k1) acc += w11 * in[r1 * w + c1];
+      if (ok0 && k0 && !(wall && tap_blocked(wall, w, h, c0, r0, sx, sy))) acc += w00 * in[r0 * w + c0];
+      if (ok0 && k1 && !(wall && tap_blocked(wall, w, h, c1, r0, sx + 1, sy))) acc += w10 * in[r0 * w + c1];
+      if (ok1 && k0 && !(wall && tap_blocked(wall, w, h, c0, r1, sx, sy + 1))) acc += w01 * in[r1 * w + c0];
+      if (ok1 && k1 && !(wall && tap_blocked(wall, w, h, c1, r1, sx + 1, sy + 1))) acc += w11 * in[r1 * w + c1];
       out[j * w + i] = acc;
     }
   }
+}
+
+int glo_seg_cells(int ox, int oy, int* qx, int* qy, int cap) {
+  const int x0 = ox < 0 ? ox : 0, x1 = ox < 0 ? 0 : ox;
+  const int y0 = oy < 0 ? oy : 0, y1 = oy < 0 ? 0 : oy;
+  int n = 0;
+  for (int cy = y0; cy <= y1; ++cy)
+    for (int cx = x0; cx <= x1; ++cx) {
+      if ((cx == 0 && cy == 0) || (cx == ox && cy == oy)) continue;
+      if (!seg_crosses(ox, oy, cx, cy)) continue;
+      if (n < cap) {
+        qx[n] = cx - ox;
+        qy[n] = cy - oy;
+      }
+      ++n;
+    }
+  return n;
 }
 
 /* convolve_plane, belief_tensor.cpp:126-193: three summation orders.
@@ -317,6 +374,12 @@ int glo_init_uniform(const uint8_t* occ, int w, int h, int channels,
 int glo_step(double* B, int w, int h, int C, double cell, double* theta_t,
              double u, double v, double dw, const uint8_t* occ,
              const glo_kernels* ks, const double* inverse) {
+  return glo_step_wall(B, w, h, C, cell, theta_t, u, v, dw, occ, ks, inverse, 0);
+}
+
+int glo_step_wall(double* B, int w, int h, int C, double cell, double* theta_t,
+                  double u, double v, double dw, const uint8_t* occ,
+                  const glo_kernels* ks, const double* inverse, int wall_mask) {
   const size_t plane = (size_t)w * h;
   const double dtheta = 2.0 * M_PI / C;
   double* S = (double*)malloc(sizeof(double) * plane * C);
@@ -327,7 +390,7 @@ int glo_step(double* B, int w, int h, int C, double cell, double* theta_t,
     double dx, dy;
     glo_motion_vector(u, v, k, *theta_t, dtheta, cell, &dx, &dy);
     double* s = S + plane * k;
-    shift(B + plane * k, s, w, h, dx, dy);
+    shift(B + plane * k, s, w, h, dx, dy, wall_mask ? occ : NULL);
     for (size_t p = 0; p < plane; ++p)
       if (occ[p]) s[p] = 0.0;
   }
@@ -380,7 +443,7 @@ void glo_apply_motion(double* B, int w, int h, int C, double cell,
     double dx, dy;
     glo_motion_vector(u, v, k, *theta_t, dtheta, cell, &dx, &dy);
     if (dx == 0.0 && dy == 0.0) continue;
-    shift(B + plane * k, tmp, w, h, dx, dy);
+    shift(B + plane * k, tmp, w, h, dx, dy, NULL);
     memcpy(B + plane * k, tmp, sizeof(double) * plane);
   }
   free(tmp);

@@ -69,6 +69,20 @@ int glo_step(double* belief, int w, int h, int channels, double cell,
              const uint8_t* occ, const glo_kernels* ks,
              const double* inverse);
 
+/* glo_step with the wall-crossing mask (wall_mask != 0): an EXTENSION the
+ * reference does not have (it masks destinations only,
+ * belief_tensor.cpp:414-416): a bilinear tap is dropped when the open segment
+ * between its source and destination cell centres crosses the interior of
+ * an occupied cell. Parity for this mode is against this restatement of the
+ * rule only (no reference behaviour exists to pin it to). */
+int glo_step_wall(double* belief, int w, int h, int channels, double cell,
+                  double* theta_t, double u, double v, double dw,
+                  const uint8_t* occ, const glo_kernels* ks,
+                  const double* inverse, int wall_mask);
+/* cells crossed by the tap offset (ox, oy), relative to the destination;
+ * returns the full count, stores at most cap */
+int glo_seg_cells(int ox, int oy, int* qx, int* qy, int cap);
+
 void glo_apply_motion(double* belief, int w, int h, int channels, double cell,
                       double* theta_t, double u, double v, double dw);
 

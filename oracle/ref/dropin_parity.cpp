@@ -23,6 +23,7 @@
 #include <iterator>
 #include <fstream>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "gridloc/belief_tensor.hpp"
@@ -105,8 +106,12 @@ static void check_steps(const ref::OccupancyMap& rmap, b2::ThreadPool& pool, ref
          rsmp.cells.size(), bsmp.cells.size());
 }
 
+static std::vector<double> values_of(const b2::Localizer& l) { return l.belief().values(); }
+static std::vector<double> values_of(const b2::ShardedLocalizer& l) { return l.belief_values(); }
+
+template <class B2Localizer, class... Extra>
 static void check_localizer(const ref::OccupancyMap& rmap, b2::ThreadPool& pool, ref::ThreadPool& rpool,
-                            int channels, int ticks) {
+                            int channels, int ticks, const char* what, Extra&&... extra) {
   const b2::OccupancyMap bmap = to_b2(rmap, pool);
   const ref::DistanceField rfield = ref::distance_field(rmap);
   const b2::DistanceField bfield = b2::distance_field(bmap);
@@ -115,7 +120,7 @@ static void check_localizer(const ref::OccupancyMap& rmap, b2::ThreadPool& pool,
   b2::LocalizerConfig bc;
   bc.channels = channels;
   ref::Localizer rl(rmap, rfield, rc, rpool);
-  b2::Localizer bl(bmap, bfield, bc, pool);
+  B2Localizer bl(bmap, bfield, bc, std::forward<Extra>(extra)...);
   ref::Rng rng(5);
   ref::RobotState robot;
   robot.pose = ref::Pose2{rmap.center_x(12), rmap.center_y(12), 0.3};
@@ -135,9 +140,10 @@ static void check_localizer(const ref::OccupancyMap& rmap, b2::ThreadPool& pool,
     EXPECT(r_step == b_step, "trigger differs at tick %d", tick);
     if (r_step) {
       ++steps;
-      const size_t mm = bit_mismatches(bl.belief().values(), rl.belief().values());
+      const std::vector<double> bv = values_of(bl);
+      const size_t mm = bit_mismatches(bv, rl.belief().values());
       if (observes == 0) EXPECT(mm == 0, "blind step %d: %zu values differ", steps, mm);
-      worst_l1 = std::max(worst_l1, rel_l1(bl.belief().values(), rl.belief().values()));
+      worst_l1 = std::max(worst_l1, rel_l1(bv, rl.belief().values()));
     }
     if (tick % 20 == 19) {
       const ref::LidarScan scan = ref::simulate_scan(rmap, robot.pose, 24, 2.0 * M_PI, 8.0, 0.0, rng);
@@ -145,7 +151,7 @@ static void check_localizer(const ref::OccupancyMap& rmap, b2::ThreadPool& pool,
       b2::LidarScan bscan{scan.angles, scan.ranges, scan.max_range};
       bl.observe(bscan);
       ++observes;
-      worst_l1 = std::max(worst_l1, rel_l1(bl.belief().values(), rl.belief().values()));
+      worst_l1 = std::max(worst_l1, rel_l1(values_of(bl), rl.belief().values()));
     }
     if (tick % 5 == 0) {
       const ref::PoseEstimate re = rl.estimate();
@@ -155,9 +161,9 @@ static void check_localizer(const ref::OccupancyMap& rmap, b2::ThreadPool& pool,
   }
   EXPECT(worst_l1 <= 1e-5, "relative L1 %.3e exceeds 1e-5", worst_l1);
   EXPECT(pose_mismatch == 0, "%d estimate() poses differ", pose_mismatch);
-  std::printf("{\"localizer\": {\"channels\": %d, \"ticks\": %d, \"steps\": %d, \"observes\": %d, "
+  std::printf("{\"%s\": {\"channels\": %d, \"ticks\": %d, \"steps\": %d, \"observes\": %d, "
               "\"worst_rel_l1\": %.3e, \"pose_mismatch\": %d}}\n",
-              channels, ticks, steps, observes, worst_l1, pose_mismatch);
+              what, channels, ticks, steps, observes, worst_l1, pose_mismatch);
 }
 
 
@@ -317,8 +323,15 @@ int main(int argc, char** argv) {
   check_steps(office, pool, rpool, ref::MotionNoise{1e-4, 1e-4, 0.012}, 72);
   check_steps(twin, pool, rpool, ref::MotionNoise{0.06, 0.05, 0.07}, 8);
   check_steps(twin, pool, rpool, ref::MotionNoise{0.05, 0.05, 2.0}, 8);
-  check_localizer(office, pool, rpool, 36, 600);
-  check_localizer(ref::make_loop_corridor_map(), pool, rpool, 72, 600);
+  check_localizer<b2::Localizer>(office, pool, rpool, 36, 600, "localizer", pool);
+  check_localizer<b2::Localizer>(ref::make_loop_corridor_map(), pool, rpool, 72, 600, "localizer", pool);
+  // the same driver over a theta-sharded belief (gl_engine; three shards on
+  // device 0 on a one-GPU box, peer-memory halo reads + P2P max gather)
+  const std::vector<int> devs = {0, 0, 0};
+  check_localizer<b2::ShardedLocalizer>(office, pool, rpool, 36, 600, "sharded_localizer", devs,
+                                        static_cast<int>(GL_ENGINE_P2P), pool);
+  check_localizer<b2::ShardedLocalizer>(ref::make_loop_corridor_map(), pool, rpool, 72, 400, "sharded_localizer",
+                                        devs, static_cast<int>(GL_ENGINE_P2P), pool);
   std::printf("{\"dropin_parity\": \"%s\", \"failures\": %d}\n", g_fail ? "FAIL" : "ok", g_fail);
   return g_fail ? 1 : 0;
 }

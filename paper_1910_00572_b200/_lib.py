@@ -77,6 +77,7 @@ SIGNATURES = {
     "gl_context_set_wave_tail": [_vp, C.c_int, C.c_int],
     "gl_context_set_host_exp": [_vp, C.c_int],
     "gl_context_set_tile_order": [_vp, C.c_int, C.c_int],
+    "gl_context_set_wall_mask": [_vp, C.c_int],
     "gl_shard_init_uniform": [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _pvp],
     "gl_shard_info": [_vp, _ip, _ip, _ip, _ip],
     "gl_tensor_plane_ptr": [_vp, _vp, C.c_int, C.POINTER(_dp)],
@@ -144,7 +145,27 @@ SIGNATURES = {
     "gl_shard_belief_map": [_vp, _vp, _vp],
     "gl_shard_observe": [_vp, _vp, _ip, C.c_int, _dp, _dp, C.c_int, C.c_double, _vp, _vp, LikelihoodC],
     "gl_shard_observe_finalize": [_vp, _vp],
+    "gl_tensor_hash_at": [_vp, _vp, C.c_uint64, C.POINTER(C.c_uint64)],
+    "gl_tensor_argmax_candidate": [_vp, _vp, _dp, C.POINTER(C.c_int64), _dp],
+    "gl_engine_create": [_ip, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, _u8p, C.c_int,
+                         C.c_int, _pvp],
+    "gl_engine_destroy": [_vp],
+    "gl_engine_info": [_vp, _ip, _ip, _ip],
+    "gl_engine_context": [_vp, C.c_int, _pvp],
+    "gl_engine_set_kernels": [_vp, C.c_int, _vp],
+    "gl_engine_init_uniform": [_vp],
+    "gl_engine_step": [_vp, C.c_double, C.c_double, C.c_double, C.c_int],
+    "gl_engine_step_async": [_vp, C.c_double, C.c_double, C.c_double, C.c_int],
+    "gl_engine_status": [_vp],
+    "gl_engine_argmax": [_vp, C.POINTER(PoseEstimateC)],
+    "gl_engine_belief_map": [_vp, _dp],
+    "gl_engine_observe": [_vp, C.c_int, _dp, _dp, C.c_int, C.c_double, LikelihoodC, _ip, C.c_int, _ip, _dp],
+    "gl_engine_download": [_vp, _dp, _dp],
+    "gl_engine_upload": [_vp, _dp, C.c_double],
+    "gl_engine_hash": [_vp, C.POINTER(C.c_uint64)],
 }
+
+GL_ENGINE_AUTO, GL_ENGINE_NCCL, GL_ENGINE_P2P = 0, 1, 2
 
 _lib = None
 

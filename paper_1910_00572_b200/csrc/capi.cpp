@@ -284,6 +284,12 @@ extern "C" {
 
 const char* gl_last_error(void) { return g_err.c_str(); }
 
+extern "C++" {
+namespace glb {
+void set_last_error(const std::string& msg) { g_err = msg; }  // engine.cpp
+}  // namespace glb
+}
+
 const char* gl_version(void) { return "gridloc_b200 0.1 sm_100a fp64"; }
 
 // ---------------------------------------------------------------- context
@@ -462,6 +468,13 @@ gl_status gl_context_set_wave_tail(gl_context* ctx, int ctas, int chunks) {
     need(chunks >= 1, "wave-tail chunks must be >= 1");
     ctx->tail_ctas = ctas;
     ctx->tail_chunks = chunks;
+  });
+}
+
+gl_status gl_context_set_wall_mask(gl_context* ctx, int enable) {
+  return guard([&] {
+    need(ctx, "null context");
+    ctx->wall_mask = enable != 0;
   });
 }
 
@@ -980,11 +993,47 @@ gl_status gl_tensor_hash(gl_context* ctx, gl_tensor* t, uint64_t* hash) {
     DeviceGuard g(ctx->device);
     materialize(ctx, t);
     auto* d = static_cast<unsigned long long*>(ensure_misc(ctx, 64));
-    glb::launch_hash(ctx, interior(t), elems_of(t), d);
+    glb::launch_hash(ctx, interior(t), elems_of(t), d, 0);
     unsigned long long hv = 0;
     CK(cudaMemcpyAsync(&hv, d, sizeof(hv), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     *hash = hv;
+  });
+}
+
+gl_status gl_tensor_hash_at(gl_context* ctx, gl_tensor* t, uint64_t p0, uint64_t* hash) {
+  return guard([&] {
+    need(ctx && t && hash, "null argument");
+    DeviceGuard g(ctx->device);
+    materialize(ctx, t);
+    auto* d = static_cast<unsigned long long*>(ensure_misc(ctx, 64));
+    glb::launch_hash(ctx, interior(t), elems_of(t), d, p0);
+    unsigned long long hv = 0;
+    CK(cudaMemcpyAsync(&hv, d, sizeof(hv), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    *hash = hv;
+  });
+}
+
+gl_status gl_tensor_argmax_candidate(gl_context* ctx, gl_tensor* t, double* value, int64_t* flat, double* sum) {
+  return guard([&] {
+    need(ctx && t && value && flat && sum, "null argument");
+    DeviceGuard g(ctx->device);
+    materialize(ctx, t);
+    const size_t n = elems_of(t);
+    const size_t sb = glb::argmax_scratch_bytes(n);
+    char* d = static_cast<char*>(ensure_misc(ctx, sb + 256));
+    glb::launch_argmax(ctx, interior(t), n, d, sb, d + sb);
+    struct {
+      double v;
+      long long idx;
+      double sum;
+    } res{};
+    CK(cudaMemcpyAsync(&res, d + sb, sizeof(res), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    *value = res.v;
+    *flat = res.idx;
+    *sum = res.sum;
   });
 }
 
@@ -1049,6 +1098,25 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
     int bw = 0, bh = 0;
     glb::fused_box(r, ang.n / 2, &bw, &bh);
     tm = tensor_tmap(t, src, bw, bh);
+  }
+  // wall-crossing mask (extension, wall.hpp): the fused kernel takes it when
+  // its per-window table holds this step's motion vectors (TMA loads only);
+  // anything else runs the generic chain, which tests every tap exactly
+  a.wall = ctx->wall_mask;
+  if (a.wall && fused) {
+    thread_local std::vector<double> wm;
+    const int planes = t->halo >= 0 ? t->c + 2 * t->halo : t->c;
+    wm.resize(2 * static_cast<size_t>(planes));
+    if (t->halo >= 0) {
+      const double dtheta = 2.0 * M_PI / t->c_total;
+      for (int q = 0; q < planes; ++q) {
+        const int k = ((t->c_begin - t->halo + q) % t->c_total + t->c_total) % t->c_total;
+        glb::motion_table(u, v, k, 1, t->theta_t, dtheta, t->cell, wm.data() + 2 * q);
+      }
+    } else {
+      glb::motion_table(u, v, 0, t->c, t->theta_t, 2.0 * M_PI / t->c, t->cell, wm.data());
+    }
+    if (tm == nullptr || !glb::fused_wall_fits(wm.data(), planes)) fused = false;
   }
   if (ctx->path == GL_PATH_FUSED && !fused) {
     fail(GL_E_INVALID, "fused path requested but unsupported for this kernel set/grid");

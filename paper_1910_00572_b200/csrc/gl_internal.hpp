@@ -65,6 +65,7 @@ struct ChanRec {
   int ox, oy;             // floor(dx), floor(dy), clamped to +-2^29
   int integral : 8;       // round(dx) == dx && round(dy) == dy
   int map : 8;            // fused launch: 0 own buffer, 1 / 2 left / right neighbour's
+  int wall : 8;           // fused launch with the wall-crossing mask: entry of FusedParams::wall
   int z;                  // fused launch: source plane in that buffer
 };
 void chan_rec(double dx, double dy, ChanRec* r);  // host_math.cpp
@@ -92,6 +93,7 @@ struct gl_context {
   int strip_tiles = -1;    // fused step tile order: -1 auto, 0 row-major, n: vertical strips n tiles wide
   int tile_stack = 0;      // fused step: 0/1 a CTA's warps take side-by-side tiles, n: n stacked vertically
   bool host_exp = true;    // likelihood geometric mean: exp by host glibc (exact)
+  bool wall_mask = false;  // step phase 1: also drop taps whose motion segment crosses a wall (extension)
   void* d_kind = nullptr;  // likelihood case codes
   size_t kind_bytes = 0;
   uint64_t launches = 0;
@@ -222,6 +224,7 @@ struct StepArgs {
   const double* src_lo = nullptr;        // the neighbours' source buffers (storage plane 0)
   const double* src_hi = nullptr;
   int* host_status = nullptr;            // mapped status word (synchronous gl_step)
+  bool wall = false;                     // the wall-crossing mask (wall.hpp; an extension, off by default)
 };
 
 // k_generic.cu
@@ -255,13 +258,19 @@ void launch_mask_plane(gl_context* ctx, const double* in, const uint8_t* occ,
 size_t argmax_scratch_bytes(size_t n);
 void launch_argmax(gl_context* ctx, const double* buf, size_t n,
                    void* d_scratch, size_t scratch_bytes, void* d_out);
+// order-independent hash of buf[0..n) as the elements p0 .. p0+n-1 of a
+// larger tensor (shard hashes add up to the whole tensor's)
 void launch_hash(gl_context* ctx, const double* buf, size_t n,
-                 unsigned long long* d_out);
+                 unsigned long long* d_out, unsigned long long p0);
 void launch_plane_max(gl_context* ctx, const double* buf, size_t n,
                       unsigned long long* d_gmax);
 
 // k_fused.cu
 bool fused_supported(int r, const double* sep, const AngTaps& ang, int c);
+// the wall-crossing mask fits the fused kernel's table for these motion
+// vectors (<= kWallEntries distinct floors per window, <= kWallSeg crossed
+// cells per tap, within kWallReach); otherwise the generic chain runs it
+bool fused_wall_fits(const double* h_motion, int n);
 void fused_counters(unsigned long long* out4);  // diagnostics
 void fused_box(int r, int H, int* bw, int* bh);
 void launch_fused_step(gl_context* ctx, const StepArgs& a,
@@ -270,6 +279,20 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
 // 1 if any value has its sign bit set or is not finite (buffer not "clean")
 void launch_scan_unclean(gl_context* ctx, const double* buf, size_t n,
                          unsigned int* d_flag);
+
+// k_engine.cu (the single-process multi-device engine, engine.cpp)
+constexpr int kEngineMaxShards = 16;
+struct PtrList {
+  const void* p[kEngineMaxShards];
+  int n;
+};
+// mailbox[slot] = the shard's step max bits (after its fused step)
+void launch_engine_publish(gl_context* ctx, const unsigned long long* gmax, unsigned long long* mailbox);
+// gmax = max over the shards' mailboxes (peer reads), for gl_shard_finalize
+void launch_engine_gather(gl_context* ctx, const PtrList& mailboxes, unsigned long long* gmax);
+// dst[p] = max(dst[p], src_s[p]) over the listed planes (peer reads)
+void launch_plane_max_combine(gl_context* ctx, double* dst, const PtrList& srcs, size_t n);
+void set_last_error(const std::string& msg);  // capi.cpp
 
 // k_difficulty.cu (map_difficulty, evaluation.cpp:25-72)
 constexpr int kMaxDifficultyBeams = 256;

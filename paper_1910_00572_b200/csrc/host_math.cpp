@@ -147,6 +147,7 @@ void chan_rec(double dx, double dy, ChanRec* r) {
   r->oy = clamp(fy0);
   r->integral = (std::round(dx) == dx && std::round(dy) == dy) ? 1 : 0;
   r->map = 0;
+  r->wall = 0;
   r->z = 0;
 }
 

@@ -1,0 +1,8 @@
+// One (R, H) instantiation of the fused step kernels (see k_fused.cuh).
+#include "k_fused.cuh"
+
+namespace glb {
+namespace fk {
+template void launch_rh<2, 0>(gl_context*, const CUtensorMap* const*, FusedParams&, bool, bool, bool);
+}  // namespace fk
+}  // namespace glb

@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "gl_internal.hpp"
+#include "wall.hpp"
 
 namespace glb {
 
@@ -40,15 +41,19 @@ __device__ __forceinline__ double warp_max_pos(double v) {
 
 // shift_plane (belief_tensor.cpp:67-124) for output cell (i, j) of a plane:
 // integral (dx, dy) copies (:71-86); otherwise w00, w10, w01, w11 are added
-// to 0.0 in that order, skipping taps outside the grid (:107-122).
+// to 0.0 in that order, skipping taps outside the grid (:107-122). wall !=
+// null (the wall-crossing mask extension, wall.hpp): taps whose segment
+// crosses an occupied cell are skipped too.
 __device__ __forceinline__ double shifted_value(const double* __restrict__ in,
                                                 int w, int h, int i, int j,
                                                 double dx, double dy,
-                                                bool scaled, double sc) {
+                                                bool scaled, double sc,
+                                                const uint8_t* __restrict__ wall) {
   const double fx = floor(dx), fy = floor(dy);
   if (fx == dx && fy == dy) {
     const long si = i - static_cast<long>(dx), sj = j - static_cast<long>(dy);
     if (si < 0 || si >= w || sj < 0 || sj >= h) return 0.0;
+    if (wall && wall_tap_blocked(wall, w, h, si, sj, static_cast<long>(dx), static_cast<long>(dy))) return 0.0;
     double v = in[sj * static_cast<long>(w) + si];
     return scaled ? v * sc : v;
   }
@@ -66,21 +71,25 @@ __device__ __forceinline__ double shifted_value(const double* __restrict__ in,
     const double v = in[r * w + c];
     return scaled ? v * sc : v;
   };
+  auto open = [&](long c, long r, long ox, long oy) {
+    return wall == nullptr || !wall_tap_blocked(wall, w, h, c, r, ox, oy);
+  };
   double acc = 0.0;
-  if (ok_r0 && ok_c0) acc += w00 * ld(r0, c0);
-  if (ok_r0 && ok_c1) acc += w10 * ld(r0, c1);
-  if (ok_r1 && ok_c0) acc += w01 * ld(r1, c0);
-  if (ok_r1 && ok_c1) acc += w11 * ld(r1, c1);
+  if (ok_r0 && ok_c0 && open(c0, r0, sx, sy)) acc += w00 * ld(r0, c0);
+  if (ok_r0 && ok_c1 && open(c1, r0, sx + 1, sy)) acc += w10 * ld(r0, c1);
+  if (ok_r1 && ok_c0 && open(c0, r1, sx, sy + 1)) acc += w01 * ld(r1, c0);
+  if (ok_r1 && ok_c1 && open(c1, r1, sx + 1, sy + 1)) acc += w11 * ld(r1, c1);
   return acc;
 }
 
-// grid: x over columns, y over rows, z over channels
+// grid: x over columns, y over rows, z over channels. mode 1: step phase 1
+// (shift + mask; wall: the wall-crossing mask), 2: apply_motion.
 __global__ void k_shift_mask(const double* __restrict__ B,
                              double* __restrict__ S,
                              const double2* __restrict__ motion,
                              const uint8_t* __restrict__ occ,
                              const BufState* __restrict__ st, int w, int h,
-                             int mode) {
+                             int mode, int wall) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
   const int k = blockIdx.z;
@@ -98,7 +107,7 @@ __global__ void k_shift_mask(const double* __restrict__ B,
     v = in[p];
     if (scaled) v = v * sc;
   } else {
-    v = shifted_value(in, w, h, i, j, m.x, m.y, scaled, sc);
+    v = shifted_value(in, w, h, i, j, m.x, m.y, scaled, sc, (mode == 1 && wall) ? occ : nullptr);
   }
   if (mode == 1 && occ[p]) v = 0.0;  // phase-1 mask (:414-416)
   S[plane * k + p] = v;
@@ -448,14 +457,14 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   return z ^ (z >> 31);
 }
 
-__global__ void k_hash(const double* __restrict__ B, size_t n,
+__global__ void k_hash(const double* __restrict__ B, size_t n, unsigned long long p0,
                        unsigned long long* out) {
   unsigned long long acc = 0;
   for (size_t q = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
        q < n; q += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const unsigned long long bits =
         static_cast<unsigned long long>(__double_as_longlong(B[q]));
-    acc += mix64(bits + static_cast<unsigned long long>(q) * 0x9e3779b97f4a7c15ull);
+    acc += mix64(bits + (p0 + static_cast<unsigned long long>(q)) * 0x9e3779b97f4a7c15ull);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -513,7 +522,7 @@ int grid_for(size_t n, int threads, int max_blocks = 148 * 16) {
 void launch_shift_mask(gl_context* ctx, const StepArgs& a, double* S, int mode) {
   dim3 grid((a.w + kThreads - 1) / kThreads, a.h, a.c);
   k_shift_mask<<<grid, kThreads, 0, ctx->stream>>>(a.src, S, a.motion, a.occ,
-                                                   a.src_state, a.w, a.h, mode);
+                                                   a.src_state, a.w, a.h, mode, a.wall ? 1 : 0);
   ctx->launches++;
 }
 
@@ -672,9 +681,9 @@ void launch_argmax(gl_context* ctx, const double* buf, size_t n,
 }
 
 void launch_hash(gl_context* ctx, const double* buf, size_t n,
-                 unsigned long long* d_out) {
+                 unsigned long long* d_out, unsigned long long p0) {
   cudaMemsetAsync(d_out, 0, sizeof(unsigned long long), ctx->stream);
-  k_hash<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(buf, n, d_out);
+  k_hash<<<grid_for(n, kThreads), kThreads, 0, ctx->stream>>>(buf, n, p0, d_out);
   ctx->launches++;
 }
 

@@ -26,7 +26,7 @@ __all__ = [
     "apply_motion", "belief_map", "argmax_state", "dither_samples", "scan_likelihood", "observation_update",
     "distance_field", "wrap_angle", "compose_delta", "Localizer", "LocalizerConfig",
     "write_belief_snapshot", "read_belief_snapshot", "DifficultyConfig", "map_difficulty",
-    "BeliefExtinguishedError", "MapParseError", "CudaError", "GridlocError",
+    "BeliefExtinguishedError", "MapParseError", "CudaError", "GridlocError", "Engine",
 ]
 
 
@@ -172,6 +172,11 @@ class Context:
         """scan_likelihood's final exp: host glibc (default, bit-exact) or
         CUDA's exp on the device (<= 1 ulp)."""
         check(self.lib.gl_context_set_host_exp(self.h, int(enable)))
+
+    def set_wall_mask(self, enable: bool):
+        """The wall-crossing mask extension (off by default; not in the
+        reference): step() drops taps whose motion segment crosses a wall."""
+        check(self.lib.gl_context_set_wall_mask(self.h, int(enable)))
 
     def set_tile_order(self, strip_tiles: int, stack: int = 0):
         """Fused-step tile order: strip_tiles -1 auto, 0 row-major, n =
@@ -749,3 +754,86 @@ class Localizer:
 
     def steps_run(self) -> int:
         return self._steps
+
+
+# ------------------------------------------------------------------ engine
+class Engine:
+    """gl_engine: ONE process driving a theta-slab sharded belief over a
+    device list; the Python face of the C++ callers'
+    multi-GPU path. Shard s owns channels [s*C/n, (s+1)*C/n) on devices[s];
+    halo planes are read over peer memory inside the step kernel, the 8-byte
+    step max is all-reduced by NCCL (distinct devices) or a peer-memory
+    gather (P2P). Bitwise the unsharded tensor. Slot 0 = main kernels,
+    slot 1 = rotation-only (Localizer)."""
+
+    def __init__(self, devices, m: "OccupancyMap", channels: int, mode: int = 0):
+        self.lib = _lib.load()
+        devs = (C.c_int * len(devices))(*devices)
+        occ = np.ascontiguousarray(m.cells(), dtype=np.uint8)
+        h = C.c_void_p()
+        check(self.lib.gl_engine_create(devs, len(devices), m.width(), m.height(), m.resolution(), m.origin_x(),
+                                        m.origin_y(), _u8(occ), channels, mode, C.byref(h)))
+        self.h = h
+        self.W, self.H, self.C = m.width(), m.height(), channels
+        self.cell, self.ox, self.oy = m.resolution(), m.origin_x(), m.origin_y()
+
+    def info(self):
+        n, mode, halo = C.c_int(), C.c_int(), C.c_int()
+        check(self.lib.gl_engine_info(self.h, C.byref(n), C.byref(mode), C.byref(halo)))
+        return {"shards": n.value, "mode": {1: "nccl", 2: "p2p"}.get(mode.value, mode.value), "halo": halo.value}
+
+    def set_kernels(self, slot: int, kernels: "KernelSet"):
+        check(self.lib.gl_engine_set_kernels(self.h, slot, kernels.h))
+
+    def init_uniform(self):
+        check(self.lib.gl_engine_init_uniform(self.h))
+
+    def step(self, u: "OdometryDelta", slot: int = 0):
+        check(self.lib.gl_engine_step(self.h, u.u, u.v, u.w, slot))
+
+    def step_async(self, u: "OdometryDelta", slot: int = 0):
+        check(self.lib.gl_engine_step_async(self.h, u.u, u.v, u.w, slot))
+
+    def status(self):
+        check(self.lib.gl_engine_status(self.h))
+
+    def argmax(self) -> PoseEstimate:
+        e = PoseEstimateC()
+        check(self.lib.gl_engine_argmax(self.h, C.byref(e)))
+        return PoseEstimate(Pose2(e.x, e.y, e.theta), e.confidence, e.i, e.j, e.k)
+
+    def belief_map(self) -> np.ndarray:
+        out = np.empty((self.H, self.W))
+        check(self.lib.gl_engine_belief_map(self.h, _d(out)))
+        return out
+
+    def observe(self, scan: "LidarScan", params: "LikelihoodParams" = None, budget: int = 512) -> SampleSet:
+        params = params or LikelihoodParams()
+        a = np.ascontiguousarray(scan.angles, dtype=np.float64)
+        r = np.ascontiguousarray(scan.ranges, dtype=np.float64)
+        cap = max(1, min(self.W * self.H, 4 * max(budget, 1) + 64))
+        cells = np.zeros(2 * cap, np.int32)
+        n, mass = C.c_int(), C.c_double()
+        check(self.lib.gl_engine_observe(self.h, budget, _d(a), _d(r), a.size, scan.max_range, _lp(params),
+                                         _i(cells), cap, C.byref(n), C.byref(mass)))
+        return SampleSet(cells[: 2 * min(n.value, cap)].reshape(-1, 2).copy(), mass.value)
+
+    def values(self):
+        out = np.empty((self.C, self.H, self.W))
+        th = C.c_double()
+        check(self.lib.gl_engine_download(self.h, _d(out), C.byref(th)))
+        return out, th.value
+
+    def set_values(self, vals, theta_t: float = 0.0):
+        v = np.ascontiguousarray(vals, dtype=np.float64)
+        check(self.lib.gl_engine_upload(self.h, _d(v), theta_t))
+
+    def hash(self) -> int:
+        hv = C.c_uint64()
+        check(self.lib.gl_engine_hash(self.h, C.byref(hv)))
+        return hv.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.gl_engine_destroy(self.h)
+            self.h = None
