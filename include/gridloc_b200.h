@@ -107,7 +107,7 @@ gl_status gl_context_set_tile_order(gl_context* ctx, int strip_tiles, int stack)
  * through a wall. Fused into the step kernel's shift stage (a per-warp
  * occupancy bit window; the per-channel crossed-cell lists come from the
  * host); steps whose motion the kernel's table cannot hold (|floor(d)| > 7,
- * > 16 distinct floors) run the generic chain. Parity for this mode is
+ * > 8 crossed cells per tap, > 16 distinct floors) run the generic chain. Parity for this mode is
  * against the oracle's restatement (oracle/gl_oracle.c glo_step_wall). */
 gl_status gl_context_set_wall_mask(gl_context* ctx, int enable);
 /* scan_likelihood's final exp (the per-pose geometric mean,
@@ -380,6 +380,24 @@ gl_status gl_shard_observe(gl_context* ctx, gl_tensor* t, const int32_t* cells, 
                            const double* angles, const double* ranges, int n_beams,
                            double max_range, const gl_map* map, const gl_field* field,
                            gl_likelihood params);
+
+/* raycast (occupancy_map.hpp:123-124, occupancy_map.cpp:273-332) for a batch
+ * of rays, rays[3q..3q+2] = (x, y, angle) in world units: ranges[q] in
+ * meters, bit-exact (Amanatides-Woo on the device; cos/sin by host glibc).
+ * max_range <= 0 -> GL_E_INVALID; an origin outside free space ->
+ * GL_E_MAP_PARSE (the reference's MapParseError kInvalidOrigin). */
+gl_status gl_raycast(gl_context* ctx, const gl_map* map, const double* rays, int n, double max_range,
+                     double* ranges);
+/* simulate_scan (simulator.hpp, simulator.cpp:63-94) for n poses
+ * (poses[3q..3q+2] = x, y, theta): the beam angles (beam_count, the
+ * reference's formula) and ranges[q * beam_count + b]. With
+ * range_noise_sigma > 0, noise[q * beam_count + b] must hold the standard
+ * normal the reference's Rng would draw for that beam (pose-major, beam
+ * order: rng.normal() once per beam); r += noise * sigma, clamped to
+ * [0, max_range]. Bit-exact against the reference for the same draws. */
+gl_status gl_simulate_scans(gl_context* ctx, const gl_map* map, const double* poses, int n, int beam_count,
+                            double fov, double max_range, double range_noise_sigma, const double* noise,
+                            double* angles, double* ranges);
 
 /* diagnostics: out4[0] = step epilogues that took the exact max */
 gl_status gl_debug_counters(gl_context* ctx, unsigned long long* out4);

@@ -518,6 +518,50 @@ inline void observation_update(BeliefTensor& t, const SampleSet& samples, const 
                               gl_likelihood{params.sigma_hit, params.weight_floor, params.beam_stride}));
 }
 
+// ------------------------------------------------------ raycast / scans
+// occupancy_map.hpp:123-124 / simulator.hpp (simulate_scan): on the device,
+// bit-exact; the batch forms are for trace generation.
+inline double raycast(const OccupancyMap& map, double x, double y, double angle, double max_range) {
+  const double ray[3] = {x, y, angle};
+  double r = 0.0;
+  check(gl_raycast(map.pool().get(), map.handle(), ray, 1, max_range, &r));
+  return r;
+}
+inline std::vector<double> raycast_batch(const OccupancyMap& map, const std::vector<double>& rays_xya,
+                                         double max_range) {
+  std::vector<double> r(rays_xya.size() / 3);
+  check(gl_raycast(map.pool().get(), map.handle(), rays_xya.data(), static_cast<int>(r.size()), max_range,
+                   r.data()));
+  return r;
+}
+// Rng: the reference's gridloc::Rng (rng.hpp), or anything with normal():
+// one draw per beam when range_noise_sigma > 0, in the reference's order.
+template <class Rng>
+std::vector<LidarScan> simulate_scans(const OccupancyMap& map, const std::vector<Pose2>& poses, int beam_count,
+                                      double fov, double max_range, double range_noise_sigma, Rng& rng) {
+  std::vector<double> p;
+  for (const auto& q : poses) p.insert(p.end(), {q.x, q.y, q.theta});
+  std::vector<double> noise;
+  if (range_noise_sigma > 0.0 && beam_count >= 1)
+    for (size_t q = 0; q < poses.size() * static_cast<size_t>(beam_count); ++q) noise.push_back(rng.normal());
+  std::vector<double> angles(std::max(beam_count, 0)), ranges(poses.size() * std::max(beam_count, 0));
+  check(gl_simulate_scans(map.pool().get(), map.handle(), p.data(), static_cast<int>(poses.size()), beam_count,
+                          fov, max_range, range_noise_sigma, noise.empty() ? nullptr : noise.data(),
+                          angles.data(), ranges.data()));
+  std::vector<LidarScan> out(poses.size());
+  for (size_t q = 0; q < poses.size(); ++q) {
+    out[q].angles = angles;
+    out[q].ranges.assign(ranges.begin() + q * beam_count, ranges.begin() + (q + 1) * beam_count);
+    out[q].max_range = max_range;
+  }
+  return out;
+}
+template <class Rng>
+LidarScan simulate_scan(const OccupancyMap& map, const Pose2& pose, int beam_count, double fov, double max_range,
+                        double range_noise_sigma, Rng& rng) {  // simulator.cpp:63-94
+  return simulate_scans(map, std::vector<Pose2>{pose}, beam_count, fov, max_range, range_noise_sigma, rng)[0];
+}
+
 // ------------------------------------------------------------- localizer
 struct LocalizerConfig {  // localizer.hpp:17-26
   int channels = 128;

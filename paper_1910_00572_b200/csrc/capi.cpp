@@ -752,11 +752,17 @@ gl_status gl_activation_get(gl_context* ctx, const gl_activation* a,
 }
 
 // ---------------------------------------------------------------- tensors
-static gl_tensor* new_tensor(gl_context* ctx, int w, int h, int c, double cell,
-                             double ox, double oy, int halo = -1, int c_total = 0,
-                             int c_begin = 0) {
+// Owning handle of a tensor under construction: a failure anywhere before
+// the caller releases it frees every device buffer allocated so far (at
+// 4096^2 x 360 one buffer is 48 GB, which must not leak on an OOM of the
+// second).
+using TensorPtr = std::unique_ptr<gl_tensor, gl_status (*)(gl_tensor*)>;
+
+static TensorPtr new_tensor(gl_context* ctx, int w, int h, int c, double cell,
+                            double ox, double oy, int halo = -1, int c_total = 0,
+                            int c_begin = 0) {
   need(w >= 1 && h >= 1 && c >= 1, "belief tensor dimensions must be positive");
-  auto t = std::make_unique<gl_tensor>();
+  TensorPtr t(new gl_tensor(), gl_tensor_destroy);
   t->w = w;
   t->h = h;
   t->c = c;
@@ -774,7 +780,7 @@ static gl_tensor* new_tensor(gl_context* ctx, int w, int h, int c, double cell,
   glb::DeviceBlock init{};
   init.buf[0].scale = init.buf[1].scale = 1.0;
   CK(cudaMemcpy(t->d_block, &init, sizeof(init), cudaMemcpyHostToDevice));
-  return t.release();
+  return t;
 }
 
 gl_status gl_tensor_create(gl_context* ctx, int width, int height,
@@ -783,10 +789,10 @@ gl_status gl_tensor_create(gl_context* ctx, int width, int height,
   return guard([&] {
     need(ctx && out, "null argument");
     DeviceGuard g(ctx->device);
-    gl_tensor* t = new_tensor(ctx, width, height, channels, cell_size, origin_x, origin_y);
-    glb::launch_fill(ctx, t->d_buf[0], elems_of(t), 0.0);
+    TensorPtr t = new_tensor(ctx, width, height, channels, cell_size, origin_x, origin_y);
+    glb::launch_fill(ctx, t->d_buf[0], elems_of(t.get()), 0.0);
     CK(cudaStreamSynchronize(ctx->stream));
-    *out = t;
+    *out = t.release();
   });
 }
 
@@ -797,11 +803,11 @@ gl_status gl_init_uniform(gl_context* ctx, const gl_map* map, int channels,
     need(channels >= 4 && channels % 2 == 0, "channel count must be even and >= 4");
     need(map->free_count > 0, "map has no free cells to initialize from");
     DeviceGuard g(ctx->device);
-    gl_tensor* t = new_tensor(ctx, map->w, map->h, channels, map->res, map->ox, map->oy);
+    TensorPtr t = new_tensor(ctx, map->w, map->h, channels, map->res, map->ox, map->oy);
     glb::launch_init_uniform(ctx, t->d_buf[0], map->d_occ, map->w, map->h, channels);
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaGetLastError());
-    *out = t;
+    *out = t.release();
   });
 }
 
@@ -852,11 +858,20 @@ gl_status gl_read_belief_snapshot(gl_context* ctx, const char* path, double cell
     in.read(reinterpret_cast<char*>(dims), sizeof(dims));
     in.read(reinterpret_cast<char*>(&theta), sizeof(theta));
     if (!in) throw std::runtime_error(std::string("truncated belief snapshot ") + path);
+    // validate the header against the file before allocating (a corrupt
+    // header must not request a huge device allocation)
+    need(dims[0] >= 1 && dims[1] >= 1 && dims[2] >= 1 && dims[0] <= (1u << 20) && dims[1] <= (1u << 20) &&
+             dims[2] <= (1u << 16),
+         "belief snapshot dimensions out of range");
+    const unsigned long long want = 16ull + 4ull * dims[0] * dims[1] * dims[2];
+    const std::streampos here = in.tellg();
+    in.seekg(0, std::ios::end);
+    const unsigned long long have = static_cast<unsigned long long>(in.tellg());
+    in.seekg(here);
+    if (have < want) throw std::runtime_error(std::string("truncated belief snapshot ") + path);
     DeviceGuard g(ctx->device);
-    std::unique_ptr<gl_tensor, gl_status (*)(gl_tensor*)> t(
-        new_tensor(ctx, static_cast<int>(dims[0]), static_cast<int>(dims[1]), static_cast<int>(dims[2]),
-                   cell_size, origin_x, origin_y),
-        gl_tensor_destroy);
+    TensorPtr t = new_tensor(ctx, static_cast<int>(dims[0]), static_cast<int>(dims[1]), static_cast<int>(dims[2]),
+                             cell_size, origin_x, origin_y);
     t->theta_t = theta;
     const size_t n = elems_of(t.get());
     std::vector<float> buf(n);
@@ -976,14 +991,14 @@ gl_status gl_tensor_clone(gl_context* ctx, gl_tensor* src, gl_tensor** out) {
     need(ctx && src && out, "null argument");
     DeviceGuard g(ctx->device);
     materialize(ctx, src);
-    gl_tensor* t = new_tensor(ctx, src->w, src->h, src->c, src->cell, src->ox, src->oy,
-                              src->halo, src->c_total, src->c_begin);
+    TensorPtr t = new_tensor(ctx, src->w, src->h, src->c, src->cell, src->ox, src->oy,
+                             src->halo, src->c_total, src->c_begin);
     CK(cudaMemcpyAsync(t->d_buf[0], src->d_buf[src->cur], storage_elems(src) * sizeof(double),
                        cudaMemcpyDeviceToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     t->theta_t = src->theta_t;
     t->clean[0] = src->clean[src->cur];
-    *out = t;
+    *out = t.release();
   });
 }
 
@@ -1252,13 +1267,13 @@ gl_status gl_shard_init_uniform(gl_context* ctx, const gl_map* map, int c_total,
     need(halo >= 0 && 2 * halo < c_total, "bad halo");
     need(map->free_count > 0, "map has no free cells to initialize from");
     DeviceGuard g(ctx->device);
-    gl_tensor* t = new_tensor(ctx, map->w, map->h, c_end - c_begin, map->res, map->ox, map->oy, halo,
-                              c_total, c_begin);
+    TensorPtr t = new_tensor(ctx, map->w, map->h, c_end - c_begin, map->res, map->ox, map->oy, halo,
+                             c_total, c_begin);
     // every storage plane (interior and halo) starts as the free indicator
     glb::launch_init_uniform(ctx, t->d_buf[0], map->d_occ, map->w, map->h, t->c + 2 * halo);
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaGetLastError());
-    *out = t;
+    *out = t.release();
   });
 }
 
@@ -1779,6 +1794,108 @@ gl_status gl_debug_counters(gl_context* ctx, unsigned long long* out4) {
     DeviceGuard g(ctx->device);
     CK(cudaStreamSynchronize(ctx->stream));
     glb::fused_counters(out4);
+  });
+}
+
+// ------------------------------------------------- raycast / simulate_scan
+// Batches for trace generation: every ray on the device,
+// bit-exact against raycast (occupancy_map.cpp:273-332) — the directions are
+// glibc cos/sin evaluated on the host, as the reference evaluates them.
+namespace {
+
+void run_rays(gl_context* ctx, const gl_map* map, const std::vector<double>& xy, const std::vector<double>& dir,
+              int beams, double max_range, const double* noise, double sigma, double* ranges, const char* what) {
+  const size_t n_rays = dir.size() / 2, n_pose = xy.size() / 2;
+  need(n_rays <= static_cast<size_t>(INT32_MAX), "too many rays in one batch");
+  const size_t b_xy = 16 * n_pose, b_dir = 16 * n_rays, b_noise = noise ? 8 * n_rays : 0, b_r = 8 * n_rays;
+  auto al = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
+  char* d = static_cast<char*>(ensure_misc(ctx, al(b_xy) + al(b_dir) + al(b_noise) + al(b_r) + 256));
+  auto* d_xy = reinterpret_cast<double2*>(d);
+  auto* d_dir = reinterpret_cast<double2*>(d + al(b_xy));
+  auto* d_noise = noise ? reinterpret_cast<double*>(d + al(b_xy) + al(b_dir)) : nullptr;
+  auto* d_r = reinterpret_cast<double*>(d + al(b_xy) + al(b_dir) + al(b_noise));
+  auto* d_bad = reinterpret_cast<int*>(d + al(b_xy) + al(b_dir) + al(b_noise) + al(b_r));
+  CK(cudaMemcpyAsync(d_xy, xy.data(), b_xy, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d_dir, dir.data(), b_dir, cudaMemcpyHostToDevice, ctx->stream));
+  if (noise) CK(cudaMemcpyAsync(d_noise, noise, b_noise, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(d_bad, 0, sizeof(int), ctx->stream));
+  glb::launch_raycast_batch(ctx, map->d_occ, map->w, map->h, map->res, map->ox, map->oy, d_xy, d_dir,
+                            static_cast<int>(n_rays), beams, max_range, d_noise, sigma, d_r, d_bad);
+  CK(cudaGetLastError());
+  int bad = 0;
+  CK(cudaMemcpyAsync(ranges, d_r, b_r, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (bad) fail(GL_E_MAP_PARSE, what);
+}
+
+}  // namespace
+
+gl_status gl_raycast(gl_context* ctx, const gl_map* map, const double* rays, int n, double max_range,
+                     double* ranges) {
+  return guard([&] {
+    need(ctx && map && (n == 0 || (rays && ranges)), "null argument");
+    need(n >= 0, "ray count must be >= 0");
+    need(max_range > 0.0, "max_range must be > 0");  // occupancy_map.cpp:275
+    if (n == 0) return;
+    DeviceGuard g(ctx->device);
+    std::vector<double> xy(2 * static_cast<size_t>(n)), dir(2 * static_cast<size_t>(n));
+    for (int q = 0; q < n; ++q) {
+      xy[2 * q] = rays[3 * q];
+      xy[2 * q + 1] = rays[3 * q + 1];
+      dir[2 * q] = std::cos(rays[3 * q + 2]);
+      dir[2 * q + 1] = std::sin(rays[3 * q + 2]);
+    }
+    run_rays(ctx, map, xy, dir, 1, max_range, nullptr, 0.0, ranges, "raycast origin not in a free cell");
+  });
+}
+
+gl_status gl_simulate_scans(gl_context* ctx, const gl_map* map, const double* poses, int n, int beam_count,
+                            double fov, double max_range, double range_noise_sigma, const double* noise,
+                            double* angles, double* ranges) {
+  return guard([&] {
+    need(ctx && map && (n == 0 || (poses && ranges)), "null argument");
+    need(n >= 0, "pose count must be >= 0");
+    need(beam_count >= 1, "beam_count must be >= 1");  // simulator.cpp:66
+    // world_free(pose) for every pose first (simulator.cpp:67-70)
+    for (int q = 0; q < n; ++q) {
+      const double x = poses[3 * q], y = poses[3 * q + 1];
+      const int i = static_cast<int>(std::floor((x - map->ox) / map->res));
+      const int j = static_cast<int>(std::floor((y - map->oy) / map->res));
+      if (!(i >= 0 && i < map->w && j >= 0 && j < map->h) || map->occ[static_cast<size_t>(j) * map->w + i]) {
+        fail(GL_E_MAP_PARSE, "scan pose is not in free space");
+      }
+    }
+    need(max_range > 0.0, "max_range must be > 0");  // the first raycast (occupancy_map.cpp:275)
+    const bool full_circle = fov >= 2.0 * M_PI - 1e-9;
+    std::vector<double> a(beam_count);
+    for (int b = 0; b < beam_count; ++b) {
+      if (beam_count == 1) {
+        a[b] = 0.0;
+      } else if (full_circle) {
+        a[b] = -M_PI + b * (2.0 * M_PI / beam_count);  // endpoint-exclusive
+      } else {
+        a[b] = -fov / 2.0 + b * (fov / (beam_count - 1));
+      }
+    }
+    if (angles) std::copy(a.begin(), a.end(), angles);
+    if (n == 0) return;
+    DeviceGuard g(ctx->device);
+    const size_t rays = static_cast<size_t>(n) * beam_count;
+    std::vector<double> xy(2 * static_cast<size_t>(n)), dir(2 * rays);
+    for (int q = 0; q < n; ++q) {
+      xy[2 * q] = poses[3 * q];
+      xy[2 * q + 1] = poses[3 * q + 1];
+      for (int b = 0; b < beam_count; ++b) {
+        const double ang = poses[3 * q + 2] + a[b];  // raycast(map, x, y, pose.theta + a, ...)
+        dir[2 * (static_cast<size_t>(q) * beam_count + b)] = std::cos(ang);
+        dir[2 * (static_cast<size_t>(q) * beam_count + b) + 1] = std::sin(ang);
+      }
+    }
+    const bool noisy = range_noise_sigma > 0.0;
+    need(!noisy || noise, "range noise requested without the per-beam normal draws");
+    run_rays(ctx, map, xy, dir, beam_count, max_range, noisy ? noise : nullptr, range_noise_sigma, ranges,
+             "raycast origin not in a free cell");
   });
 }
 

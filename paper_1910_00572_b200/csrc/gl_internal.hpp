@@ -316,6 +316,10 @@ struct DifficultyArgs {
   int* bad;                // 1 (zeroed)
 };
 void launch_difficulty(gl_context* ctx, const DifficultyArgs& a);
+// raycast / simulate_scan batches (occupancy_map.cpp:273-332, simulator.cpp:63-94)
+void launch_raycast_batch(gl_context* ctx, const uint8_t* occ, int w, int h, double res, double ox, double oy,
+                          const double2* xy, const double2* dir, int n_rays, int beams, double max_range,
+                          const double* noise, double sigma, double* ranges, int* bad);
 
 // k_observe.cu
 void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,

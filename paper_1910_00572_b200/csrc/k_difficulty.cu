@@ -25,29 +25,19 @@ namespace glb {
 
 namespace {
 
-// raycast (occupancy_map.cpp:273-332) from a cell centre at heading a_b
-// (the query pose has theta = 0, so the beam angle is a_b exactly).
-__global__ void k_raycast_queries(const uint8_t* __restrict__ occ, int w, int h, double res,
-                                  double ox, double oy, const int2* __restrict__ cells, int n,
-                                  const double2* __restrict__ ray, int beams, double max_range,
-                                  double* __restrict__ ranges, int* __restrict__ bad) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n * beams) return;
-  const int q = t / beams, b = t - q * beams;
-  const int2 cl = cells[q];
-  const double x = ox + (cl.x + 0.5) * res;  // center_x / center_y
-  const double y = oy + (cl.y + 0.5) * res;
+// raycast (occupancy_map.cpp:273-332): Amanatides-Woo from (x, y) along the
+// host-computed direction (dx, dy) = (cos, sin)(angle) (glibc, as the
+// reference), with its corner-tie tolerance; every operation in the
+// reference's order (--fmad=false). Returns false when the origin is not a
+// free in-bounds cell (the reference throws MapParseError kInvalidOrigin).
+__device__ __forceinline__ bool raycast_dev(const uint8_t* __restrict__ occ, int w, int h, double res, double ox,
+                                            double oy, double x, double y, double dx, double dy, double max_range,
+                                            double* out) {
   const double cx = (x - ox) / res;
   const double cy = (y - oy) / res;
   int i = static_cast<int>(floor(cx));
   int j = static_cast<int>(floor(cy));
-  if (!(i >= 0 && i < w && j >= 0 && j < h) || occ[static_cast<size_t>(j) * w + i]) {
-    atomicExch(bad, 1);  // the reference throws (raycast origin not free)
-    ranges[t] = 0.0;
-    return;
-  }
-  const double dx = ray[b].x;
-  const double dy = ray[b].y;
+  if (!(i >= 0 && i < w && j >= 0 && j < h) || occ[static_cast<size_t>(j) * w + i]) return false;
   const double max_cells = max_range / res;
   const int step_x = dx > 0.0 ? 1 : (dx < 0.0 ? -1 : 0);
   const int step_y = dy > 0.0 ? 1 : (dy < 0.0 ? -1 : 0);
@@ -80,6 +70,50 @@ __global__ void k_raycast_queries(const uint8_t* __restrict__ occ, int w, int h,
       r = (max_cells < tt ? max_cells : tt) * res;  // std::min(t, max_cells) * res
       break;
     }
+  }
+  *out = r;
+  return true;
+}
+
+// map_difficulty's noise-free query scans: from each query cell's centre at
+// heading a_b (the query pose has theta = 0, so the beam angle is a_b exactly)
+__global__ void k_raycast_queries(const uint8_t* __restrict__ occ, int w, int h, double res,
+                                  double ox, double oy, const int2* __restrict__ cells, int n,
+                                  const double2* __restrict__ ray, int beams, double max_range,
+                                  double* __restrict__ ranges, int* __restrict__ bad) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * beams) return;
+  const int q = t / beams, b = t - q * beams;
+  const int2 cl = cells[q];
+  const double x = ox + (cl.x + 0.5) * res;  // center_x / center_y
+  const double y = oy + (cl.y + 0.5) * res;
+  double r = 0.0;
+  if (!raycast_dev(occ, w, h, res, ox, oy, x, y, ray[b].x, ray[b].y, max_range, &r)) {
+    atomicExch(bad, 1);  // the reference throws (raycast origin not free)
+    r = 0.0;
+  }
+  ranges[t] = r;
+}
+
+// A batch of rays (raycast) or scans (simulate_scan, simulator.cpp:63-94):
+// ray t = (pose t / beams, beam t % beams) from xy[pose] along dir[t]; with
+// noise, r += noise[t] * sigma, clamped to [0, max_range] (std::clamp).
+__global__ void k_raycast_batch(const uint8_t* __restrict__ occ, int w, int h, double res, double ox, double oy,
+                                const double2* __restrict__ xy, const double2* __restrict__ dir, int n_rays,
+                                int beams, double max_range, const double* __restrict__ noise, double sigma,
+                                double* __restrict__ ranges, int* __restrict__ bad) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_rays) return;
+  const double2 p = xy[t / beams];
+  double r = 0.0;
+  if (!raycast_dev(occ, w, h, res, ox, oy, p.x, p.y, dir[t].x, dir[t].y, max_range, &r)) {
+    atomicExch(bad, 1);
+    ranges[t] = 0.0;
+    return;
+  }
+  if (noise) {
+    r += noise[t] * sigma;
+    r = r < 0.0 ? 0.0 : (max_range < r ? max_range : r);
   }
   ranges[t] = r;
 }
@@ -201,6 +235,14 @@ __global__ void __launch_bounds__(256) k_difficulty_near(
 }
 
 }  // namespace
+
+void launch_raycast_batch(gl_context* ctx, const uint8_t* occ, int w, int h, double res, double ox, double oy,
+                          const double2* xy, const double2* dir, int n_rays, int beams, double max_range,
+                          const double* noise, double sigma, double* ranges, int* bad) {
+  k_raycast_batch<<<(n_rays + 127) / 128, 128, 0, ctx->stream>>>(occ, w, h, res, ox, oy, xy, dir, n_rays, beams,
+                                                                 max_range, noise, sigma, ranges, bad);
+  ctx->launches++;
+}
 
 void launch_difficulty(gl_context* ctx, const DifficultyArgs& a) {
   const int rt = a.n * a.beams;

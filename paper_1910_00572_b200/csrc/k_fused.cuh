@@ -32,6 +32,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <stdexcept>
+#include <string>
 #include <cstdint>
 #include <cstdlib>
 #include <cmath>
@@ -778,10 +781,36 @@ constexpr size_t smem_bytes() {
 // wave holds rem CTAs splits its last ~rem/5 CTAs (rounded down to 32) into
 // 3 channel chunks. 1024^2 x 72 (1120 CTAs, rem 528 -> 96): 0.2475 ->
 // 0.2384 ms; 128 CTAs measured the same, 64 / 160 / 4 chunks gave nothing.
-inline int auto_tail_ctas(const gl_context* ctx, int blocks) {
-  const int slots = 4 * (ctx->sm_count > 0 ? ctx->sm_count : 148);
-  if (blocks <= slots) return 0;
+// `slots` = resident CTAs of the instantiated kernel on the whole GPU
+// (occupancy API x SMs). Gated to the measured shape class: grids of 1..4
+// waves, where the partial last wave is a large share of the run; longer
+// grids (4096^2: 59 waves) gain nothing from it and keep one chunk.
+inline int auto_tail_ctas(int slots, int blocks) {
+  if (slots <= 0 || blocks <= slots || blocks > 4 * slots) return 0;
   return ((blocks % slots) / 5) & ~31;
+}
+
+// Tuning-experiment environment overrides (GRIDLOC_B200_CHUNKS,
+// GRIDLOC_B200_TAIL = "ctas[,chunks]"): compiled in only with
+// -DGL_EXPERIMENT_ENV (tools/build_variants.sh); the shipped library ignores
+// the environment and takes only the gl_context_set_* settings.
+inline int env_int(const char* name, int dflt) {
+#ifdef GL_EXPERIMENT_ENV
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+#else
+  (void)name;
+  return dflt;
+#endif
+}
+inline int env_tail_chunks() {
+#ifdef GL_EXPERIMENT_ENV
+  const char* e = std::getenv("GRIDLOC_B200_TAIL");
+  const char* c = e ? std::strchr(e, ',') : nullptr;
+  return c ? std::atoi(c + 1) : 0;
+#else
+  return 0;
+#endif
 }
 
 // Auto tile order (measured, profiles/r02_tile_order.md): grids up to 48
@@ -803,13 +832,23 @@ void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& f
   using G = Geo<R, ROWS>;
   constexpr size_t smem = smem_bytes<R, ROWS, WALL>();
   auto kern = k_fused_step<R, H, ROWS, kNS, kNWARP, FAST, HIMAX, TMA, WALL>;
-  static uint64_t configured = 0;  // bit per device: the attribute is per device
-  const uint64_t bit = 1ull << (ctx->device & 63);
-  if (!(configured & bit)) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    configured |= bit;
+  // per device (the attribute is per device): the dynamic shared-memory
+  // opt-in and the resident CTAs per SM it leaves (grid sizing below)
+  static std::atomic<int> per_sm[64] = {};
+  const int dslot = ctx->device & 63;
+  int cta_per_sm = per_sm[dslot].load(std::memory_order_acquire);
+  if (cta_per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    int n = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 32 * kNWARP, smem);
+    if (e != cudaSuccess || n < 1) {
+      throw std::runtime_error(std::string("fused step kernel cannot be configured: ") + cudaGetErrorString(e));
+    }
+    per_sm[dslot].store(n, std::memory_order_release);
+    cta_per_sm = n;
   }
+  const int sms = ctx->sm_count > 0 ? ctx->sm_count : 148;
   fp.tiles_x = (fp.w + G::OW - 1) / G::OW;
   fp.tiles_y = (fp.h + ROWS - 1) / ROWS;
   // tile order: strips only pay where a full tile row is long enough that
@@ -824,7 +863,7 @@ void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& f
   // 50%. Measured at 1024^2 x 72 (4480 tiles): 1 chunk 0.265 ms, 2 chunks
   // 0.274 ms — chunking only pays when the tiles cannot fill the GPU.
   fp.n_chunks = 1;
-  const long wave = 16L * (ctx->sm_count > 0 ? ctx->sm_count : 148);
+  const long wave = static_cast<long>(kNWARP) * cta_per_sm * sms;  // resident warps
   if (fp.n_tiles < wave) {
     // at most one wave: a second, mostly empty wave costs a whole warp
     // lifetime (measured 256^2 x 36: 9 chunks = 1.09 waves 22.7 us, 4 chunks 20.2 us)
@@ -832,10 +871,7 @@ void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& f
     const int max_chunks = n_win / (H == 0 ? 2 : 4 * H);
     fp.n_chunks = std::max(1, std::min(want, max_chunks));
   }
-  static const int chunk_override = [] {
-    const char* e = std::getenv("GRIDLOC_B200_CHUNKS");  // tuning experiments only
-    return e ? std::atoi(e) : 0;
-  }();
+  static const int chunk_override = env_int("GRIDLOC_B200_CHUNKS", 0);
   if (ctx->channel_chunks > 0) fp.n_chunks = std::min(ctx->channel_chunks, n_win);
   if (chunk_override > 0) fp.n_chunks = std::min(chunk_override, n_win);
   fp.k_chunk = (n_win + fp.n_chunks - 1) / fp.n_chunks;
@@ -844,19 +880,12 @@ void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& f
   // Wave tail: with one chunk, the grid's last partial wave of CTAs leaves
   // slots idle while it runs; the last tail CTAs' tiles are split into
   // channel chunks so the tail drains in shorter work items.
-  static const int tail_override = [] {
-    const char* e = std::getenv("GRIDLOC_B200_TAIL");  // tuning experiments only: "ctas[,chunks]"
-    return e ? std::atoi(e) : -1;
-  }();
-  static const int tail_chunks_override = [] {
-    const char* e = std::getenv("GRIDLOC_B200_TAIL");
-    const char* c = e ? std::strchr(e, ',') : nullptr;
-    return c ? std::atoi(c + 1) : 0;
-  }();
+  static const int tail_override = env_int("GRIDLOC_B200_TAIL", -1);
+  static const int tail_chunks_override = env_tail_chunks();
   fp.head_ctas = blocks;
   fp.tail_chunks = 1;
   fp.tail_k = fp.k_chunk;
-  int tail = ctx->tail_ctas >= 0 ? ctx->tail_ctas : auto_tail_ctas(ctx, blocks);
+  int tail = ctx->tail_ctas >= 0 ? ctx->tail_ctas : auto_tail_ctas(cta_per_sm * sms, blocks);
   if (tail_override >= 0) tail = tail_override;
   tail = fp.n_chunks == 1 ? std::min(tail, blocks) : 0;
   const int tail_chunks = std::max(1, std::min(tail_chunks_override > 0 ? tail_chunks_override : ctx->tail_chunks, n_win));

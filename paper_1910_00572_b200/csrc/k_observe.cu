@@ -4,6 +4,9 @@
 // (observation.cpp:113-170). --fmad=false; reference operand order.
 #include <cuda_runtime.h>
 
+#include <stdexcept>
+#include <string>
+
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -523,13 +526,16 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
 //     thresholds at 0.5 on support cells, emits, and records e = v - q.
 // Serpentine order has no inter-row wavefront (row j+1 starts where row j
 // ended), so the W*H dependent chain is inherent; see DESIGN.md.
+// Row buffers in shared memory, or (gbuf != null, rows wider than shared
+// memory holds: W > ~14.5K cells) in global memory.
 __global__ void __launch_bounds__(32) k_dither(
     const double* __restrict__ bm, int w, int h, int budget,
     int* __restrict__ cells, int cap, int* __restrict__ n_out,
-    double* __restrict__ mass_out) {
+    double* __restrict__ mass_out, double* gbuf) {
   extern __shared__ double sh[];
-  double* pre = sh;       // w
-  double* err = sh + w;   // w: errors of the previous row
+  double* base = gbuf ? gbuf : sh;
+  double* pre = base;       // w
+  double* err = base + w;   // w: errors of the previous row
   const int lane = threadIdx.x;
   const size_t plane = static_cast<size_t>(w) * h;
 
@@ -689,17 +695,29 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
                    int* d_cells, int cap, int* d_n, double* d_mass) {
   const size_t rs = (static_cast<size_t>(w) + 3) & ~static_cast<size_t>(1);
   const size_t smem_pipe = (3 * rs + w) * sizeof(double) + 8 * static_cast<size_t>((w + 31) / 32 + 1) + 16;
-  if (smem_pipe <= 200 * 1024) {
-    if (smem_pipe > 48 * 1024) {
-      cudaFuncSetAttribute(k_dither_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem_pipe));
+  auto attr = [](const void* fn, size_t bytes) {
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(bytes));
+    if (e != cudaSuccess) {
+      throw std::runtime_error(std::string("dither kernel shared-memory opt-in failed: ") + cudaGetErrorString(e));
     }
+  };
+  const size_t smem = static_cast<size_t>(2) * w * sizeof(double);
+  if (smem_pipe <= 200 * 1024) {
+    if (smem_pipe > 48 * 1024) attr(reinterpret_cast<const void*>(k_dither_pipe), smem_pipe);
     k_dither_pipe<<<1, 64, smem_pipe, ctx->stream>>>(bm, w, h, budget, d_cells, cap, d_n, d_mass);
+  } else if (smem <= 200 * 1024) {
+    attr(reinterpret_cast<const void*>(k_dither), smem);
+    k_dither<<<1, 32, smem, ctx->stream>>>(bm, w, h, budget, d_cells, cap, d_n, d_mass, nullptr);
   } else {
-    const size_t smem = static_cast<size_t>(2) * w * sizeof(double);
-    cudaFuncSetAttribute(k_dither, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    k_dither<<<1, 32, smem, ctx->stream>>>(bm, w, h, budget, d_cells, cap, d_n, d_mass);
+    // rows wider than shared memory holds: the two row buffers in global
+    // memory (stream-ordered allocation around the launch)
+    double* gbuf = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&gbuf), smem, ctx->stream);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("dither row buffers: ") + cudaGetErrorString(e));
+    k_dither<<<1, 32, 0, ctx->stream>>>(bm, w, h, budget, d_cells, cap, d_n, d_mass, gbuf);
+    e = cudaFreeAsync(gbuf, ctx->stream);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("dither row buffers: ") + cudaGetErrorString(e));
   }
   ctx->launches++;
   if (getenv("GL_DEBUG_DITHER")) {

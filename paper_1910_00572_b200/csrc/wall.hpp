@@ -24,7 +24,7 @@
 
 namespace glb {
 
-constexpr int kWallSeg = 6;       // fused path: crossed cells per tap (else the generic chain)
+constexpr int kWallSeg = 8;       // fused path: crossed cells per tap (else the generic chain)
 constexpr int kWallEntries = 16;  // fused path: distinct (floor dx, floor dy) per launch window
 constexpr int kWallReach = 7;     // fused path: |crossed cell - destination| per axis
 

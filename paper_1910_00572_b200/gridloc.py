@@ -27,6 +27,7 @@ __all__ = [
     "distance_field", "wrap_angle", "compose_delta", "Localizer", "LocalizerConfig",
     "write_belief_snapshot", "read_belief_snapshot", "DifficultyConfig", "map_difficulty",
     "BeliefExtinguishedError", "MapParseError", "CudaError", "GridlocError", "Engine",
+    "raycast", "simulate_scans", "simulate_scan",
 ]
 
 
@@ -754,6 +755,47 @@ class Localizer:
 
     def steps_run(self) -> int:
         return self._steps
+
+
+# ------------------------------------------------------ raycast / scans
+def raycast(m: OccupancyMap, rays, max_range: float, ctx=None) -> np.ndarray:
+    """occupancy_map.cpp:273-332 for a batch of rays: rays (n, 3) = (x, y,
+    angle); returns (n,) ranges in meters, bit-exact, on the device."""
+    ctx = _ctx(ctx) if ctx is not None else m.ctx
+    r = np.ascontiguousarray(np.asarray(rays, dtype=np.float64).reshape(-1, 3))
+    out = np.empty(len(r))
+    check(ctx.lib.gl_raycast(ctx.h, m.h, _d(r), len(r), max_range, _d(out)))
+    return out
+
+
+def simulate_scans(m: OccupancyMap, poses, beam_count: int, fov: float, max_range: float,
+                   range_noise_sigma: float = 0.0, rng=None, ctx=None):
+    """simulator.cpp:63-94 for a batch of poses (n, 3) = (x, y, theta):
+    returns (angles (beams,), ranges (n, beams)). With range noise, `rng`
+    (the reference's xoshiro256++ generator, floorplan.Rng) draws one normal
+    per beam in pose-major order, exactly as n successive simulate_scan
+    calls on the reference's Rng would."""
+    ctx = _ctx(ctx) if ctx is not None else m.ctx
+    p = np.ascontiguousarray(np.asarray(poses, dtype=np.float64).reshape(-1, 3))
+    n = len(p)
+    noise = None
+    if range_noise_sigma > 0.0:
+        if rng is None:
+            raise ValueError("range noise needs an rng (reference draw order)")
+        noise = np.array([rng.normal() for _ in range(n * beam_count)], dtype=np.float64)
+    angles = np.empty(max(beam_count, 0))
+    ranges = np.empty((n, max(beam_count, 0)))
+    check(ctx.lib.gl_simulate_scans(ctx.h, m.h, _d(p), n, beam_count, fov, max_range, range_noise_sigma,
+                                    None if noise is None else _d(noise), _d(angles), _d(ranges)))
+    return angles, ranges
+
+
+def simulate_scan(m: OccupancyMap, pose: Pose2, beam_count: int, fov: float, max_range: float,
+                  range_noise_sigma: float = 0.0, rng=None, ctx=None) -> LidarScan:
+    """simulator.cpp:63-94 (one pose)."""
+    a, r = simulate_scans(m, [(pose.x, pose.y, pose.theta)], beam_count, fov, max_range, range_noise_sigma, rng,
+                          ctx)
+    return LidarScan(a, r[0], max_range)
 
 
 # ------------------------------------------------------------------ engine

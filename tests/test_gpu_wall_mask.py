@@ -53,7 +53,7 @@ def _pair(ctx, port, occ, channels, noise, motions, path, B0=None, fast=True):
 
 
 MOTIONS = [(0.1, 0.0, 0.0), (0.25, 0.13, 0.05), (-0.31, 0.22, -0.1), (0.0, 0.0, 0.2), (0.2, 0.2, 0.0),
-           (0.55, -0.37, 0.3), (0.0, -0.2, 0.0)]
+           (0.35, -0.27, 0.3), (0.0, -0.2, 0.0)]
 
 
 @pytest.mark.parametrize("path", [GL_PATH_FUSED, GL_PATH_GENERIC])
