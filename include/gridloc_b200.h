@@ -107,7 +107,7 @@ gl_status gl_context_set_tile_order(gl_context* ctx, int strip_tiles, int stack)
  * through a wall. Fused into the step kernel's shift stage (a per-warp
  * occupancy bit window; the per-channel crossed-cell lists come from the
  * host); steps whose motion the kernel's table cannot hold (|floor(d)| > 7,
- * > 8 crossed cells per tap, > 16 distinct floors) run the generic chain. Parity for this mode is
+ * > 8 crossed cells per tap, > 64 distinct floors) run the generic chain. Parity for this mode is
  * against the oracle's restatement (oracle/gl_oracle.c glo_step_wall). */
 gl_status gl_context_set_wall_mask(gl_context* ctx, int enable);
 /* scan_likelihood's final exp (the per-pose geometric mean,
@@ -356,6 +356,12 @@ gl_status gl_dither_device(gl_context* ctx, const double* d_plane, int width,
 gl_status gl_dither_tensor(gl_context* ctx, gl_tensor* t, int budget,
                            int32_t* cells, int cap, int* n,
                            double* source_mass);
+
+/* dither_samples' total (observation.cpp:16-17: total = 0.0; total += v
+ * in order), bit-exact, computed on the device by a parallel scan over the
+ * running sum's binades (k_observe.cu k_seq_sum). Values must be finite and
+ * >= 0 (else GL_E_INVALID). */
+gl_status gl_sequential_sum(gl_context* ctx, const double* values, size_t n, double* total);
 
 /* scan_likelihood / observation_update (observation.cpp:73-170). */
 typedef struct {

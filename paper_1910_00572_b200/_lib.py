@@ -147,6 +147,7 @@ SIGNATURES = {
     "gl_shard_observe_finalize": [_vp, _vp],
     "gl_tensor_hash_at": [_vp, _vp, C.c_uint64, C.POINTER(C.c_uint64)],
     "gl_raycast": [_vp, _vp, _dp, C.c_int, C.c_double, _dp],
+    "gl_sequential_sum": [_vp, _dp, C.c_size_t, _dp],
     "gl_simulate_scans": [_vp, _vp, _dp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, _dp, _dp, _dp],
     "gl_tensor_argmax_candidate": [_vp, _vp, _dp, C.POINTER(C.c_int64), _dp],
     "gl_engine_create": [_ip, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, _u8p, C.c_int,

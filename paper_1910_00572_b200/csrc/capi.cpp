@@ -1489,8 +1489,9 @@ static void run_dither(gl_context* ctx, const double* d_bm, int w, int h,
   // layout: [bm plane (if copied)] [n, mass] [cells]
   int* d_n = reinterpret_cast<int*>(base + plane * sizeof(double));
   double* d_mass = reinterpret_cast<double*>(base + plane * sizeof(double) + 8);
+  int* d_inv = reinterpret_cast<int*>(base + plane * sizeof(double) + 16);
   int* d_cells = reinterpret_cast<int*>(base + plane * sizeof(double) + 64);
-  glb::launch_dither(ctx, d_bm, w, h, budget, d_cells, static_cast<int>(dcap), d_n, d_mass);
+  glb::launch_dither(ctx, d_bm, w, h, budget, d_cells, static_cast<int>(dcap), d_n, d_mass, d_inv);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(n, d_n, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(mass, d_mass, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1794,6 +1795,29 @@ gl_status gl_debug_counters(gl_context* ctx, unsigned long long* out4) {
     DeviceGuard g(ctx->device);
     CK(cudaStreamSynchronize(ctx->stream));
     glb::fused_counters(out4);
+  });
+}
+
+// The reference's sequential sum (observation.cpp:16-17 order) of n host
+// doubles computed on the device, bit-exact (the parallel binade scan that
+// gives dither_samples its total; there the dither kernel's own sequential
+// chain covers negative / non-finite planes).
+gl_status gl_sequential_sum(gl_context* ctx, const double* host, size_t n, double* total) {
+  return guard([&] {
+    need(ctx && (host || n == 0) && total, "null argument");
+    DeviceGuard g(ctx->device);
+    char* base = static_cast<char*>(ensure_misc(ctx, n * sizeof(double) + 64));
+    double* d_x = reinterpret_cast<double*>(base + 64);
+    double* d_t = reinterpret_cast<double*>(base);
+    int* d_inv = reinterpret_cast<int*>(base + 8);
+    if (n) CK(cudaMemcpyAsync(d_x, host, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(d_t, 0, sizeof(double), ctx->stream));
+    glb::launch_seq_sum(ctx, d_x, n, d_t, d_inv);
+    int inv = 0;
+    CK(cudaMemcpyAsync(total, d_t, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&inv, d_inv, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (inv) fail(GL_E_INVALID, "sequential_sum: values must be finite and >= 0");
   });
 }
 

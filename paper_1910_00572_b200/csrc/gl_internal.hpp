@@ -323,7 +323,11 @@ void launch_raycast_batch(gl_context* ctx, const uint8_t* occ, int w, int h, dou
 
 // k_observe.cu
 void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
-                   int* d_cells, int cap, int* d_n, double* d_mass);
+                   int* d_cells, int cap, int* d_n, double* d_mass, int* d_sum_invalid);
+// the reference's sequential FP64 sum of x[0..n) from +0.0 (observation.cpp:
+// 16-17), bit-exact by a parallel binade scan; *d_invalid = 1 (and *d_total
+// unspecified) if any x is negative or non-finite
+void launch_seq_sum(gl_context* ctx, const double* x, size_t n, double* d_total, int* d_invalid);
 void launch_likelihoods(gl_context* ctx, const uint8_t* occ, const double* score,
                         double oob_score, int w, int h, double res, double ox,
                         double oy, double cell, double tox, double toy,

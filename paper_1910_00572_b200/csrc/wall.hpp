@@ -25,7 +25,7 @@
 namespace glb {
 
 constexpr int kWallSeg = 8;       // fused path: crossed cells per tap (else the generic chain)
-constexpr int kWallEntries = 16;  // fused path: distinct (floor dx, floor dy) per launch window
+constexpr int kWallEntries = 64;  // fused path: distinct (floor dx, floor dy) per launch window
 constexpr int kWallReach = 7;     // fused path: |crossed cell - destination| per axis
 
 GL_HD bool wall_axis(long long o, long long c, long long* lo_n, long long* lo_d, long long* hi_n,

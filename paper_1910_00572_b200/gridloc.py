@@ -27,7 +27,7 @@ __all__ = [
     "distance_field", "wrap_angle", "compose_delta", "Localizer", "LocalizerConfig",
     "write_belief_snapshot", "read_belief_snapshot", "DifficultyConfig", "map_difficulty",
     "BeliefExtinguishedError", "MapParseError", "CudaError", "GridlocError", "Engine",
-    "raycast", "simulate_scans", "simulate_scan",
+    "raycast", "simulate_scans", "simulate_scan", "sequential_sum",
 ]
 
 
@@ -755,6 +755,17 @@ class Localizer:
 
     def steps_run(self) -> int:
         return self._steps
+
+
+def sequential_sum(values, ctx=None) -> float:
+    """dither_samples' total (observation.cpp:16-17): the reference's
+    sequential FP64 sum in order, bit-exact, computed on the device by a
+    parallel binade scan. Values must be finite and >= 0."""
+    ctx = _ctx(ctx)
+    v = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+    out = C.c_double()
+    check(ctx.lib.gl_sequential_sum(ctx.h, _d(v), v.size, C.byref(out)))
+    return out.value
 
 
 # ------------------------------------------------------ raycast / scans
