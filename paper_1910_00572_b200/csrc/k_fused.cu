@@ -1,20 +1,21 @@
 // Fused Algorithm-1 step, host side: launch_fused_step (shift records,
 // channel windows, the wall table, the HIMAX epilogue) over the kernel
-// templates of k_fused.cuh, whose (R, H) instantiations are compiled in
-// k_fused_inst_r*_h*.cu.
+// templates of k_fused.cuh, whose (R, H, params) instantiations are compiled
+// in k_fused_inst_r*_h*_{s,l}.cu.
 #include "k_fused.cuh"
 
 namespace glb {
 namespace fk {
-template <int R, int H>
-void launch_rh(gl_context* ctx, const CUtensorMap* const* tmap, FusedParams& fp, bool fast, bool himax,
-               bool wall);
-#define GL_FUSED_EXTERN(R, H) \
-  extern template void launch_rh<R, H>(gl_context*, const CUtensorMap* const*, FusedParams&, bool, bool, bool);
+template <int R, int H, class P>
+void launch_rh(gl_context* ctx, const CUtensorMap* const* tmap, P& fp, bool fast, bool himax, bool wall);
+#define GL_FUSED_EXTERN2(R, H, P) \
+  extern template void launch_rh<R, H, P>(gl_context*, const CUtensorMap* const*, P&, bool, bool, bool);
+#define GL_FUSED_EXTERN(R, H) GL_FUSED_EXTERN2(R, H, FusedParams) GL_FUSED_EXTERN2(R, H, FusedParamsSmall)
 GL_FUSED_EXTERN(0, 0) GL_FUSED_EXTERN(0, 1) GL_FUSED_EXTERN(0, 2) GL_FUSED_EXTERN(0, 3)
 GL_FUSED_EXTERN(1, 0) GL_FUSED_EXTERN(1, 1) GL_FUSED_EXTERN(1, 2) GL_FUSED_EXTERN(1, 3)
 GL_FUSED_EXTERN(2, 0) GL_FUSED_EXTERN(2, 1) GL_FUSED_EXTERN(2, 2) GL_FUSED_EXTERN(2, 3)
 #undef GL_FUSED_EXTERN
+#undef GL_FUSED_EXTERN2
 }  // namespace fk
 
 using namespace fk;
@@ -76,14 +77,14 @@ __global__ void __launch_bounds__(1024) k_himax_epilogue(const double* __restric
   }
 }
 
-template <int R>
-void launch_r(gl_context* ctx, const CUtensorMap* const* tmap, FusedParams& fp, int H,
+template <int R, class P>
+void launch_r(gl_context* ctx, const CUtensorMap* const* tmap, P& fp, int H,
               bool fast, bool himax, bool wall) {
   switch (H) {
-    case 0: launch_rh<R, 0>(ctx, tmap, fp, fast, himax, wall); break;
-    case 1: launch_rh<R, 1>(ctx, tmap, fp, fast, himax, wall); break;
-    case 2: launch_rh<R, 2>(ctx, tmap, fp, fast, himax, wall); break;
-    default: launch_rh<R, 3>(ctx, tmap, fp, fast, himax, wall); break;
+    case 0: launch_rh<R, 0, P>(ctx, tmap, fp, fast, himax, wall); break;
+    case 1: launch_rh<R, 1, P>(ctx, tmap, fp, fast, himax, wall); break;
+    case 2: launch_rh<R, 2, P>(ctx, tmap, fp, fast, himax, wall); break;
+    default: launch_rh<R, 3, P>(ctx, tmap, fp, fast, himax, wall); break;
   }
 }
 
@@ -177,12 +178,16 @@ void fused_counters(unsigned long long* out4) {
   cudaMemcpyFromSymbol(out4, g_fused_counters, sizeof(unsigned long long) * 4);
 }
 
-void launch_fused_step(gl_context* ctx, const StepArgs& a,
-                       const CUtensorMap* tmap, const double* sep, int r,
-                       const AngTaps& ang, bool fast) {
-  // ~19 KB: kept off the stack and not re-zeroed per step (every field the
-  // kernel reads is assigned below; unused record slots are never read)
-  static thread_local FusedParams fp;
+namespace {
+
+// One step's launches with parameter block P (see FusedHeader): records,
+// channel windows of P::kRec - 2H output channels, the wall table.
+template <class P>
+void fused_step_with(gl_context* ctx, const StepArgs& a, const CUtensorMap* tmap, const double* sep, int r,
+                     const AngTaps& ang, bool fast) {
+  // kept off the stack and not re-zeroed per step (every field the kernel
+  // reads is assigned below; unused record slots are never read)
+  static thread_local P fp;
   const int H = ang.n / 2;
   fp.dst = a.dst;
   fp.occ = a.occ;
@@ -212,7 +217,7 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
   for (int t = 0; t < 2 * r + 1; ++t) fp.sep[t] = sep[t];
   for (int t = 0; t < ang.n; ++t) fp.ang[t] = ang.w[t];
   // The shift records ride in the launch parameters; more than
-  // kParamChannels - 2H output channels take several launches over channel
+  // P::kRec - 2H output channels take several launches over channel
   // windows. Only the last one finalises the max (a shard never does: its
   // max goes to the cross-rank all-reduce first).
   // high-word max for clean buffers whose step finalises on this device
@@ -222,7 +227,7 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
   const size_t elems = static_cast<size_t>(a.w) * a.h * a.c;
   const bool himax = GL_FUSED_HIMAX && fast && tmap != nullptr && !a.wall && (!fp.shard || a.full_shard) &&
                      (ctx->himax_mode == 1 || (ctx->himax_mode == 0 && elems >= (size_t(1) << 27)));
-  const int win = kParamChannels - 2 * H;
+  const int win = P::kRec - 2 * H;
   for (int kb = 0; kb < a.c; kb += win) {
     const int ke = std::min(a.c, kb + win);
     fp.k_base = kb;
@@ -251,7 +256,9 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
       fp.rec[q].z = z;
       fp.rec[q].map = map;
     }
-    if (a.wall) wall_table(fp, ke - kb + 2 * H);
+    if constexpr (P::kWall > 0) {
+      if (a.wall) wall_table(fp, ke - kb + 2 * H);
+    }
     switch (r) {
       case 0: launch_r<0>(ctx, maps, fp, H, fast, himax, a.wall); break;
       case 1: launch_r<1>(ctx, maps, fp, H, fast, himax, a.wall); break;
@@ -263,6 +270,22 @@ void launch_fused_step(gl_context* ctx, const StepArgs& a,
     k_himax_epilogue<<<ctx->sm_count > 0 ? ctx->sm_count : 148, 1024, 0, ctx->stream>>>(
         a.dst + plane * fp.out_off, plane * a.c, a.step_state, a.dst_state, a.host_status);
     ctx->launches++;
+  }
+}
+
+}  // namespace
+
+void launch_fused_step(gl_context* ctx, const StepArgs& a,
+                       const CUtensorMap* tmap, const double* sep, int r,
+                       const AngTaps& ang, bool fast) {
+  // the ~5 KB parameter block when one launch holds every record and no
+  // wall table is needed (Theta <= 90: configs[0..2] and [4]); launching it
+  // costs less host time per step than the ~21 KB block
+  const int H = ang.n / 2;
+  if (!a.wall && a.c + 2 * H <= kSmallRec) {
+    fused_step_with<FusedParamsSmall>(ctx, a, tmap, sep, r, ang, fast);
+  } else {
+    fused_step_with<FusedParams>(ctx, a, tmap, sep, r, ang, fast);
   }
 }
 

@@ -144,7 +144,12 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map,
       : "memory");
 }
 
-struct FusedParams {
+// The launch parameters: a fixed header, then the step's per-channel shift
+// records and (WALL variants) the wall table. Kernel parameters are copied
+// per launch, so their size is host time on every step: windows of up to
+// kSmallRec records (Theta <= 90) launch with the ~5 KB FusedParamsSmall,
+// larger ones with the ~21 KB FusedParams (384 records + the wall table).
+struct FusedHeader {
   double* dst;
   const uint8_t* occ;
   const double* inv;
@@ -175,13 +180,22 @@ struct FusedParams {
   const double* src_base[3];
   double sep[2 * kFusedMaxRadius + 1];
   double ang[2 * kFusedMaxHalf + 1];
+};
+
+template <int NREC, int NWALL>
+struct FusedParamsT : FusedHeader {
+  static constexpr int kRec = NREC;
+  static constexpr int kWall = NWALL;
   // the step's shift records (host) for the window's input planes: output
   // channels k_base-H .. k_end-1+H (shard: storage planes from plane_off + k_base)
-  ChanRec rec[kParamChannels];
+  ChanRec rec[NREC];
   // wall-crossing mask (WALL variants): the crossed cells of each distinct
   // (floor dx, floor dy) of the window, indexed by ChanRec::wall
-  WallEntry wall[kWallEntries];
+  WallEntry wall[NWALL > 0 ? NWALL : 1];
 };
+constexpr int kSmallRec = 96;
+using FusedParams = FusedParamsT<kParamChannels, kWallEntries>;
+using FusedParamsSmall = FusedParamsT<kSmallRec, 0>;
 
 template <int R, int ROWS>
 struct Geo {
@@ -292,7 +306,7 @@ __device__ __forceinline__ double dot_seq(const double* w, const double* x) {
 // products instead of S values (R+1 DMUL per S instead of 2R+1; same values,
 // same addition order).
 template <int R, bool FAST>
-__device__ __forceinline__ double row_pass(const FusedParams& p, double s) {
+__device__ __forceinline__ double row_pass(const FusedHeader& p, double s) {
   double q[R + 1];
 #pragma unroll
   for (int j = 0; j <= R; ++j) q[j] = p.sep[j] * s;
@@ -313,11 +327,11 @@ __device__ __forceinline__ double row_pass(const FusedParams& p, double s) {
   return acc;
 }
 
-template <int R, int H, int ROWS, int NS, bool FAST, bool HIMAX, bool TMA, bool WALL>
+template <int R, int H, int ROWS, int NS, bool FAST, bool HIMAX, bool TMA, bool WALL, class P>
 __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
                                             const CUtensorMap* tmap_lo,
                                             const CUtensorMap* tmap_hi,
-                                            const FusedParams& p, double* Bs,
+                                            const P& p, double* Bs,
                                             uint64_t* mbar, int lane, int x0,
                                             int y0, int k0, int n_out,
                                             bool active, double* invs,
@@ -626,7 +640,7 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
 // neighbours run at nearly the same time and the halo rows they share are
 // re-read from L2, not DRAM (gl_context_set_tile_order). A tile row past the
 // grid (stack padding) comes back >= tiles_y.
-__device__ __forceinline__ void tile_coords(const FusedParams& p, int tile, int* tx, int* ty) {
+__device__ __forceinline__ void tile_coords(const FusedHeader& p, int tile, int* tx, int* ty) {
   int cell = tile, w = 0;
   if (p.stack > 1) {
     cell = tile / p.stack;
@@ -656,12 +670,12 @@ __device__ __forceinline__ void tile_coords(const FusedParams& p, int tile, int*
   *ty = cy * (p.stack > 1 ? p.stack : 1) + w;
 }
 
-template <int R, int H, int ROWS, int NS, int NWARP, bool FAST, bool HIMAX, bool TMA, bool WALL>
+template <int R, int H, int ROWS, int NS, int NWARP, bool FAST, bool HIMAX, bool TMA, bool WALL, class P>
 __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_MINB_H3)
     k_fused_step(const __grid_constant__ CUtensorMap tmap,
                  const __grid_constant__ CUtensorMap tmap_lo,
                  const __grid_constant__ CUtensorMap tmap_hi,
-                 const FusedParams p) {
+                 const P p) {
   using G = Geo<R, ROWS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // TMA destinations must be 128-B aligned. Pad by an offset computed from
@@ -713,7 +727,7 @@ __global__ void __launch_bounds__(32 * NWARP, H <= 1 ? GL_FUSED_MINB : GL_FUSED_
   }
   const int x0 = tx * G::OW;
   const int y0 = ty * ROWS;
-  double vmax = warp_tile<R, H, ROWS, NS, FAST, HIMAX, TMA, WALL>(&tmap, &tmap_lo, &tmap_hi, p, Bs, mbar, lane, x0,
+  double vmax = warp_tile<R, H, ROWS, NS, FAST, HIMAX, TMA, WALL, P>(&tmap, &tmap_lo, &tmap_hi, p, Bs, mbar, lane, x0,
                                                              y0, k0, n_out, active, invs, colbits);
 
   // global max -> the last CTA finalises status and the pending rescale
@@ -825,13 +839,13 @@ inline int auto_strip_tiles(int tiles_x) {
   return (tiles_x + n - 1) / n;
 }
 
-template <int R, int H, bool FAST, bool HIMAX, bool TMA, bool WALL = false>
-void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& fp) {
+template <int R, int H, bool FAST, bool HIMAX, bool TMA, bool WALL, class P>
+void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, P& fp) {
   const int n_win = fp.k_end - fp.k_base;
   constexpr int ROWS = rows_for<H>();
   using G = Geo<R, ROWS>;
   constexpr size_t smem = smem_bytes<R, ROWS, WALL>();
-  auto kern = k_fused_step<R, H, ROWS, kNS, kNWARP, FAST, HIMAX, TMA, WALL>;
+  auto kern = k_fused_step<R, H, ROWS, kNS, kNWARP, FAST, HIMAX, TMA, WALL, P>;
   // per device (the attribute is per device): the dynamic shared-memory
   // opt-in and the resident CTAs per SM it leaves (grid sizing below)
   static std::atomic<int> per_sm[64] = {};
@@ -902,30 +916,32 @@ void launch_rhf(gl_context* ctx, const CUtensorMap* const* tmaps, FusedParams& f
   ctx->launches++;
 }
 
-template <int R, int H>
-void launch_rh(gl_context* ctx, const CUtensorMap* const* tmap, FusedParams& fp, bool fast, bool himax,
-               bool wall) {
-  if (wall) {  // TMA only (odd widths take the generic chain), exact max
-    if (fast) {
-      launch_rhf<R, H, true, false, true, true>(ctx, tmap, fp);
+template <int R, int H, class P>
+void launch_rh(gl_context* ctx, const CUtensorMap* const* tmap, P& fp, bool fast, bool himax, bool wall) {
+  if (wall) {  // TMA only (odd widths take the generic chain), exact max; the big params carry the table
+    if constexpr (P::kWall > 0) {
+      if (fast) {
+        launch_rhf<R, H, true, false, true, true>(ctx, tmap, fp);
+      } else {
+        launch_rhf<R, H, false, false, true, true>(ctx, tmap, fp);
+      }
     } else {
-      launch_rhf<R, H, false, false, true, true>(ctx, tmap, fp);
+      throw std::logic_error("wall-mask step routed to parameters without a wall table");
     }
   } else if (tmap[0] == nullptr) {  // cp.async loads (odd widths); no high-word max variant
     if (fast) {
-      launch_rhf<R, H, true, false, false>(ctx, tmap, fp);
+      launch_rhf<R, H, true, false, false, false>(ctx, tmap, fp);
     } else {
-      launch_rhf<R, H, false, false, false>(ctx, tmap, fp);
+      launch_rhf<R, H, false, false, false, false>(ctx, tmap, fp);
     }
   } else if (fast && himax) {
-    launch_rhf<R, H, true, true, true>(ctx, tmap, fp);
+    launch_rhf<R, H, true, true, true, false>(ctx, tmap, fp);
   } else if (fast) {
-    launch_rhf<R, H, true, false, true>(ctx, tmap, fp);
+    launch_rhf<R, H, true, false, true, false>(ctx, tmap, fp);
   } else {
-    launch_rhf<R, H, false, false, true>(ctx, tmap, fp);
+    launch_rhf<R, H, false, false, true, false>(ctx, tmap, fp);
   }
 }
-
 
 }  // namespace fk
 }  // namespace glb
