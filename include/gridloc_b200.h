@@ -221,10 +221,12 @@ gl_status gl_tensor_hash(gl_context* ctx, gl_tensor* t, uint64_t* hash);
 gl_status gl_tensor_hash_at(gl_context* ctx, gl_tensor* t, uint64_t p0, uint64_t* hash);
 /* argmax_state's building block (belief_tensor.cpp:512-541): the first
  * strict maximum of the (interior) tensor in [k][j][i] order, its flat
- * index and the pairwise device sum of all values (multi-shard argmax
- * combines these; value <= 0 means no positive mass). */
-gl_status gl_tensor_argmax_candidate(gl_context* ctx, gl_tensor* t, double* value, int64_t* flat,
-                                     double* sum);
+ * index, and the reference's sequential total continued from sum_in over
+ * this tensor's values (bit-exact: sum_in = 0.0 gives argmax_state's total;
+ * theta shards chain their totals in channel order). value <= 0 means no
+ * positive mass. */
+gl_status gl_tensor_argmax_candidate(gl_context* ctx, gl_tensor* t, double sum_in, double* value, int64_t* flat,
+                                     double* sum_out);
 /* Raw device pointer of the current buffer (for NCCL halo exchange). */
 gl_status gl_tensor_device_ptr(gl_context* ctx, gl_tensor* t, double** dptr);
 

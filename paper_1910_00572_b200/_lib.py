@@ -149,7 +149,7 @@ SIGNATURES = {
     "gl_raycast": [_vp, _vp, _dp, C.c_int, C.c_double, _dp],
     "gl_sequential_sum": [_vp, _dp, C.c_size_t, _dp],
     "gl_simulate_scans": [_vp, _vp, _dp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, _dp, _dp, _dp],
-    "gl_tensor_argmax_candidate": [_vp, _vp, _dp, C.POINTER(C.c_int64), _dp],
+    "gl_tensor_argmax_candidate": [_vp, _vp, C.c_double, _dp, C.POINTER(C.c_int64), _dp],
     "gl_engine_create": [_ip, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, _u8p, C.c_int,
                          C.c_int, _pvp],
     "gl_engine_destroy": [_vp],

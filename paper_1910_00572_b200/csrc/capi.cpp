@@ -1030,25 +1030,51 @@ gl_status gl_tensor_hash_at(gl_context* ctx, gl_tensor* t, uint64_t p0, uint64_t
   });
 }
 
-gl_status gl_tensor_argmax_candidate(gl_context* ctx, gl_tensor* t, double* value, int64_t* flat, double* sum) {
+// argmax_state's scan (belief_tensor.cpp:512-541): the first strict maximum
+// and its flat index (per-block candidates, lowest-index tie rule) and the
+// reference's SEQUENTIAL total in [k][j][i] order, bit-exact (k_seqsum.cu:
+// parallel binade scan; the literal one-thread chain for tensors holding
+// negative / non-finite values). s0: the running total the scan enters with
+// (a theta shard continues its left neighbours' sum).
+struct ArgmaxExact {
+  double v;
+  long long idx;
+  double total;
+};
+
+static ArgmaxExact argmax_exact(gl_context* ctx, gl_tensor* t, double s0) {
+  materialize(ctx, t);
+  const size_t n = elems_of(t);
+  auto al = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
+  const size_t sb = al(glb::argmax_scratch_bytes(n));
+  char* d = static_cast<char*>(ensure_misc(ctx, sb + 256 + glb::seq_sum_scratch_bytes(n)));
+  glb::launch_argmax(ctx, interior(t), n, d, sb, d + sb);  // {v, idx, pairwise sum} at d + sb
+  double* d_total = reinterpret_cast<double*>(d + sb + 64);
+  int* d_inv = reinterpret_cast<int*>(d + sb + 72);
+  glb::launch_seq_sum_big(ctx, interior(t), n, d_total, d_inv, d + sb + 256, s0);
+  glb::launch_seq_sum_chain(ctx, interior(t), n, d_total, d_inv, s0);  // runs only if the scan flagged
+  struct {
+    double v;
+    long long idx;
+    double sum;
+  } res{};
+  double total = 0.0;
+  CK(cudaMemcpyAsync(&res, d + sb, sizeof(res), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&total, d_total, sizeof(total), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaGetLastError());
+  return ArgmaxExact{res.v, res.idx, total};
+}
+
+gl_status gl_tensor_argmax_candidate(gl_context* ctx, gl_tensor* t, double sum_in, double* value, int64_t* flat,
+                                     double* sum_out) {
   return guard([&] {
-    need(ctx && t && value && flat && sum, "null argument");
+    need(ctx && t && value && flat && sum_out, "null argument");
     DeviceGuard g(ctx->device);
-    materialize(ctx, t);
-    const size_t n = elems_of(t);
-    const size_t sb = glb::argmax_scratch_bytes(n);
-    char* d = static_cast<char*>(ensure_misc(ctx, sb + 256));
-    glb::launch_argmax(ctx, interior(t), n, d, sb, d + sb);
-    struct {
-      double v;
-      long long idx;
-      double sum;
-    } res{};
-    CK(cudaMemcpyAsync(&res, d + sb, sizeof(res), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    const ArgmaxExact res = argmax_exact(ctx, t, sum_in);
     *value = res.v;
     *flat = res.idx;
-    *sum = res.sum;
+    *sum_out = res.total;
   });
 }
 
@@ -1452,18 +1478,7 @@ gl_status gl_argmax(gl_context* ctx, gl_tensor* t, gl_pose_estimate* out) {
   return guard([&] {
     need(ctx && t && out, "null argument");
     DeviceGuard g(ctx->device);
-    materialize(ctx, t);
-    const size_t n = elems_of(t);
-    const size_t sb = glb::argmax_scratch_bytes(n);
-    char* d = static_cast<char*>(ensure_misc(ctx, sb + 256));
-    glb::launch_argmax(ctx, interior(t), n, d, sb, d + sb);
-    struct {
-      double v;
-      long long idx;
-      double sum;
-    } res{};
-    CK(cudaMemcpyAsync(&res, d + sb, sizeof(res), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    const ArgmaxExact res = argmax_exact(ctx, t, 0.0);
     if (!(res.v > 0.0)) fail(GL_E_EXTINGUISHED, "argmax on an all-zero belief tensor");
     const size_t plane = plane_of(t);
     const size_t p = static_cast<size_t>(res.idx) % plane;
@@ -1473,7 +1488,7 @@ gl_status gl_argmax(gl_context* ctx, gl_tensor* t, gl_pose_estimate* out) {
     out->x = t->ox + (out->i + 0.5) * t->cell;
     out->y = t->oy + (out->j + 0.5) * t->cell;
     out->theta = wrap_angle(out->k * (2.0 * M_PI / t->c) + t->theta_t);
-    out->confidence = res.sum > 0.0 ? res.v / res.sum : 0.0;
+    out->confidence = res.total > 0.0 ? res.v / res.total : 0.0;  // belief_tensor.cpp:539
   });
 }
 
@@ -1485,13 +1500,16 @@ static void run_dither(gl_context* ctx, const double* d_bm, int w, int h,
   const size_t plane = static_cast<size_t>(w) * h;
   // device capacity: every cell could emit at most once
   const size_t dcap = std::min<size_t>(plane, static_cast<size_t>(std::max(cap, 1)));
-  char* base = static_cast<char*>(ensure_misc(ctx, plane * sizeof(double) + 64 + dcap * 8));
-  // layout: [bm plane (if copied)] [n, mass] [cells]
+  const size_t cells_bytes = (dcap * 8 + 255) & ~static_cast<size_t>(255);
+  char* base = static_cast<char*>(ensure_misc(ctx, plane * sizeof(double) + 64 + cells_bytes +
+                                                       glb::seq_sum_scratch_bytes(plane)));
+  // layout: [bm plane (if copied)] [n, mass, flag] [cells] [sequential-sum scratch]
   int* d_n = reinterpret_cast<int*>(base + plane * sizeof(double));
   double* d_mass = reinterpret_cast<double*>(base + plane * sizeof(double) + 8);
   int* d_inv = reinterpret_cast<int*>(base + plane * sizeof(double) + 16);
   int* d_cells = reinterpret_cast<int*>(base + plane * sizeof(double) + 64);
-  glb::launch_dither(ctx, d_bm, w, h, budget, d_cells, static_cast<int>(dcap), d_n, d_mass, d_inv);
+  void* d_sum = base + plane * sizeof(double) + 64 + cells_bytes;
+  glb::launch_dither(ctx, d_bm, w, h, budget, d_cells, static_cast<int>(dcap), d_n, d_mass, d_inv, d_sum);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(n, d_n, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(mass, d_mass, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1806,13 +1824,14 @@ gl_status gl_sequential_sum(gl_context* ctx, const double* host, size_t n, doubl
   return guard([&] {
     need(ctx && (host || n == 0) && total, "null argument");
     DeviceGuard g(ctx->device);
-    char* base = static_cast<char*>(ensure_misc(ctx, n * sizeof(double) + 64));
-    double* d_x = reinterpret_cast<double*>(base + 64);
+    const size_t xb = (n * sizeof(double) + 255) & ~static_cast<size_t>(255);
+    char* base = static_cast<char*>(ensure_misc(ctx, 256 + xb + glb::seq_sum_scratch_bytes(n)));
     double* d_t = reinterpret_cast<double*>(base);
     int* d_inv = reinterpret_cast<int*>(base + 8);
+    double* d_x = reinterpret_cast<double*>(base + 256);
     if (n) CK(cudaMemcpyAsync(d_x, host, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemsetAsync(d_t, 0, sizeof(double), ctx->stream));
-    glb::launch_seq_sum(ctx, d_x, n, d_t, d_inv);
+    glb::launch_seq_sum_big(ctx, d_x, n, d_t, d_inv, base + 256 + xb);
     int inv = 0;
     CK(cudaMemcpyAsync(total, d_t, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(&inv, d_inv, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));

@@ -442,10 +442,11 @@ gl_status gl_engine_argmax(gl_engine* e, gl_pose_estimate* out) {
     double best = -1.0, total = 0.0;
     long long best_idx = 0;
     for (int s = 0; s < e->n; ++s) {
-      double v = 0.0, sum = 0.0;
+      double v = 0.0;
       int64_t flat = 0;
-      ecall(gl_tensor_argmax_candidate(e->ctx[s], e->t[s], &v, &flat, &sum));
-      total += sum;
+      // the reference's sequential total runs through the shards in channel
+      // order: each continues the previous one's running sum (bit-exact)
+      ecall(gl_tensor_argmax_candidate(e->ctx[s], e->t[s], total, &v, &flat, &total));
       // shards are in channel order: a later shard's equal value has a
       // higher global flat index, so only a strictly larger one wins
       const long long g = static_cast<long long>(e->c0[s]) * static_cast<long long>(plane) + flat;

@@ -323,11 +323,22 @@ void launch_raycast_batch(gl_context* ctx, const uint8_t* occ, int w, int h, dou
 
 // k_observe.cu
 void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
-                   int* d_cells, int cap, int* d_n, double* d_mass, int* d_sum_invalid);
-// the reference's sequential FP64 sum of x[0..n) from +0.0 (observation.cpp:
-// 16-17), bit-exact by a parallel binade scan; *d_invalid = 1 (and *d_total
-// unspecified) if any x is negative or non-finite
-void launch_seq_sum(gl_context* ctx, const double* x, size_t n, double* d_total, int* d_invalid);
+                   int* d_cells, int cap, int* d_n, double* d_mass, int* d_sum_invalid,
+                   void* sum_scratch);
+// k_seqsum.cu: the reference's sequential FP64 sum of x[0..n) from +0.0
+// (observation.cpp:16-17, belief_tensor.cpp:517-522), bit-exact by a
+// parallel binade scan; *d_invalid = 1 (and *d_total unspecified) if any x is
+// negative or non-finite. _big runs the chunk passes on every SM first
+// (scratch: seq_sum_scratch_bytes(n), 16-byte aligned).
+// s0: the running sum the chain enters with (0.0; a previous shard's total).
+void launch_seq_sum(gl_context* ctx, const double* x, size_t n, double* d_total, int* d_invalid, double s0 = 0.0);
+size_t seq_sum_scratch_bytes(size_t n);
+void launch_seq_sum_big(gl_context* ctx, const double* x, size_t n, double* d_total, int* d_invalid,
+                        void* scratch, double s0 = 0.0);
+// the literal chain on one thread (inputs outside the scan's domain); runs
+// only when *when != 0 (when == null: always)
+void launch_seq_sum_chain(gl_context* ctx, const double* x, size_t n, double* d_total, const int* when,
+                          double s0 = 0.0);
 void launch_likelihoods(gl_context* ctx, const uint8_t* occ, const double* score,
                         double oob_score, int w, int h, double res, double ox,
                         double oy, double cell, double tox, double toy,

@@ -63,6 +63,17 @@
 #ifndef GL_FUSED_INVSMEM
 #define GL_FUSED_INVSMEM 1      // the tile's inverse in shared memory (frees 16 registers; measured +2-4% at 1024^2x72)
 #endif
+#ifndef GL_FUSED_ROT_H
+// angular half-widths from which the channel loop is ROLLED with a rotating
+// ring of running sums (one channel body of code instead of 2H+1 unrolled
+// ones: at H = 3 the unrolled loop is ~4400 SASS instructions and the warps
+// stall on instruction fetch); below it the ring slots are indexed at
+// compile time in a loop unrolled by 2H+1
+#define GL_FUSED_ROT_H 99
+#endif
+#ifndef GL_FUSED_ROT_UNROLL
+#define GL_FUSED_ROT_UNROLL 1   // unroll factor of the rolled channel loop
+#endif
 #ifndef GL_FUSED_ROWS_H3
 #define GL_FUSED_ROWS_H3 4      // tile rows for H >= 2 (Theta = 360: H = 3)
 #endif
@@ -467,10 +478,18 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
   // D[k+H] first (belief_tensor.cpp:449-463), so a descending walk turns the
   // angular stencil into running sums whose symmetric taps (w_t == w_{2H-t}
   // bitwise, host-checked) need H+1 products per D value, not 2H+1.
-  auto channel = [&](const int it, auto Ut, auto Et, auto Pt) {
+  // ROT: a rolled channel loop whose ring is rotated instead of indexed:
+  // after input channel m, P[i] holds the running sum of output m - H + i
+  // (terms 0..i), i = 0..2H-1; the next channel's D finishes P[2H-1] (its
+  // last term, emitted), moves every P[i-1] + w_i D into P[i] (in place, top
+  // down: no register moves) and starts P[0] = w_0 D. Slots that do not
+  // hold a real output yet (the first 2H channels) are never emitted.
+  constexpr bool ROT = H >= GL_FUSED_ROT_H;
+  auto channel = [&](const int it, auto Ut, auto Et, auto Pt, const bool emit_rt) {
     constexpr int u = decltype(Ut)::value;
-    constexpr bool emit = decltype(Et)::value;
+    constexpr bool emit_ct = decltype(Et)::value;
     constexpr int tmax = decltype(Pt)::value;  // terms t <= tmax exist (prologue)
+    const bool emit = ROT ? emit_rt : emit_ct;
     const int stage = it % NS;
     const int q_in = n_iter - 1 - it;  // relative input channel
     const ChanShift cs = chan_shift(p.rec[rec0 + q_in]);
@@ -557,20 +576,31 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
 #pragma unroll
         for (int j = 0; j <= H; ++j) aq[j] = p.ang[j] * d;
         double o = 0.0;
-#pragma unroll
-        for (int t = 0; t <= 2 * H; ++t) {
-          if (t > tmax) continue;
-          const double v = aq[t <= H ? t : 2 * H - t];
-          const int slot = (u + 2 * H - t) % NG;
-          if (t == 2 * H) {
-            o = (H == 0) ? v : aacc[slot][r] + v;
-          } else if (t == 0) {
-            aacc[slot][r] = v;
+        if constexpr (ROT) {
+          if constexpr (H == 0) {
+            o = aq[0];
           } else {
-            aacc[slot][r] += v;
+            o = aacc[2 * H - 1][r] + aq[0];  // term 2H (w_2H == w_0)
+#pragma unroll
+            for (int i = 2 * H - 1; i >= 1; --i) aacc[i][r] = aacc[i - 1][r] + aq[i <= H ? i : 2 * H - i];
+            aacc[0][r] = aq[0];  // term 0 starts an output (no 0.0 seed: belief_tensor.cpp:454)
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t <= 2 * H; ++t) {
+            if (t > tmax) continue;
+            const double v = aq[t <= H ? t : 2 * H - t];
+            const int slot = (u + 2 * H - t) % NG;
+            if (t == 2 * H) {
+              o = (H == 0) ? v : aacc[slot][r] + v;
+            } else if (t == 0) {
+              aacc[slot][r] = v;
+            } else {
+              aacc[slot][r] += v;
+            }
           }
         }
-        if constexpr (emit) {
+        if (emit) {
           // mask, x inverse, max (belief_tensor.cpp:464-474)
           double iv;
           if constexpr (INVREG) {
@@ -612,19 +642,32 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
     }
   };
 
-  // channels m = -H .. H-1 only fill the ring (slots 0 .. 2H-1) ...
-  static_for<0, 2 * H>([&](auto U) {
-    channel(decltype(U)::value, U, std::false_type{}, U);
-  });
-  // ... then every channel emits output channel it - 2H; slot = it % NG
-  for (int base = 2 * H; base < n_iter; base += NG) {
-    static_for<0, NG>([&](auto V) {
-      constexpr int v = decltype(V)::value;
-      const int it = base + v;
-      if (it < n_iter)
-        channel(it, std::integral_constant<int, (2 * H + v) % NG>{}, std::true_type{},
-                std::integral_constant<int, 2 * H>{});
+  if constexpr (ROT) {
+#pragma unroll
+    for (int i = 0; i < NG - 1; ++i)
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) aacc[i][r] = 0.0;  // never emitted; keeps the prologue's reads defined
+    constexpr int kRotUnroll = GL_FUSED_ROT_UNROLL;
+#pragma unroll kRotUnroll
+    for (int it = 0; it < n_iter; ++it) {
+      channel(it, std::integral_constant<int, 0>{}, std::false_type{}, std::integral_constant<int, 2 * H>{},
+              it >= 2 * H);
+    }
+  } else {
+    // channels m = -H .. H-1 only fill the ring (slots 0 .. 2H-1) ...
+    static_for<0, 2 * H>([&](auto U) {
+      channel(decltype(U)::value, U, std::false_type{}, U, false);
     });
+    // ... then every channel emits output channel it - 2H; slot = it % NG
+    for (int base = 2 * H; base < n_iter; base += NG) {
+      static_for<0, NG>([&](auto V) {
+        constexpr int v = decltype(V)::value;
+        const int it = base + v;
+        if (it < n_iter)
+          channel(it, std::integral_constant<int, (2 * H + v) % NG>{}, std::true_type{},
+                  std::integral_constant<int, 2 * H>{}, true);
+      });
+    }
   }
   if constexpr (HIMAX) vmax = __hiloint2double(static_cast<int>(hmax), 0);
   return vmax;

@@ -40,206 +40,6 @@ __device__ __forceinline__ double fs_carry_coef(int i, int j, int w, int h, int 
   return ws > 0.0 ? (7.0 / 16.0) / ws : 0.0;
 }
 
-// ---------------------------------------------------------------------------
-// The reference's sequential total (observation.cpp:16-17: total = 0.0;
-// total += v in row-major order) — one dependent DADD per cell, 8+ M cycles
-// at 1024^2 on one thread — reproduced BIT-EXACTLY by a parallel scan.
-//
-// While the running sum s stays inside one binade [2^e, 2^(e+1)) its ulp U
-// is fixed and s = M*U with an integer M < 2^53. For x >= 0, fl(s + x) then
-// equals (M + r)*U where r = x/U rounded to nearest, ties to the r that
-// makes M + r even (IEEE round-half-even on the result). So inside a binade
-// the sequential sum is an INTEGER prefix sum of per-element increments r_i,
-// except that a tie's r depends on the parity of the running M: each element
-// is a map M -> M + a_{M & 1} with two increments (a_0, a_1) (equal unless
-// x/U is exactly half-odd), and such maps compose associatively:
-// (f then g)_p = f_p + g_{p ^ (f_p & 1)}. A block-wide scan of these pairs
-// gives every element's exact running M; the first element whose M reaches
-// 2^53 (the sum leaves the binade) is redone as a real DADD from the exact
-// predecessor, and the scan restarts in the new binade. The sum only grows
-// (x >= 0), so there are few restarts (one per binade crossed, ~20 at
-// 1024^2). Elements that are negative, infinite or NaN set *invalid: the
-// caller then takes the sequential chain.
-constexpr int kSumT = 1024, kSumK = 8, kSumChunk = kSumT * kSumK;
-constexpr long long kSumSat = 1ll << 60;
-
-struct IncPair {
-  long long a0, a1;  // increment when the running M is even / odd
-};
-
-__device__ __forceinline__ long long sat_add(long long a, long long b) {
-  const long long c = a + b;
-  return c > kSumSat ? kSumSat : c;
-}
-
-__device__ __forceinline__ IncPair compose(IncPair f, IncPair g) {  // f, then g
-  IncPair c;
-  c.a0 = sat_add(f.a0, (f.a0 & 1) ? g.a1 : g.a0);
-  c.a1 = sat_add(f.a1, (f.a1 & 1) ? g.a0 : g.a1);
-  return c;
-}
-
-// x / U rounded: floor rf, and whether the remainder is above / exactly half
-__device__ __forceinline__ IncPair inc_of(double x, int ulog, int* bad) {
-  const long long xb = __double_as_longlong(x);
-  if (xb < 0 || ((xb >> 52) & 0x7ff) == 0x7ff) {  // negative (incl. -0.0), inf, NaN
-    if (xb != static_cast<long long>(0x8000000000000000ull)) *bad = 1;  // -0.0 adds nothing from +0 sums
-    return IncPair{0, 0};
-  }
-  const int xe = static_cast<int>((xb >> 52) & 0x7ff);
-  const long long mx = xe == 0 ? (xb & 0xfffffffffffffll) : ((xb & 0xfffffffffffffll) | (1ll << 52));
-  if (mx == 0) return IncPair{0, 0};
-  const int xlog = xe == 0 ? -1074 : xe - 1075;  // x = mx * 2^xlog
-  const int d = ulog - xlog;                        // x / U = mx * 2^-d
-  if (d <= 0) {
-    const long long r = (-d >= 8) ? kSumSat : (mx << (-d));
-    return IncPair{r, r};
-  }
-  if (d >= 55) return IncPair{0, 0};  // below half an ulp: no change, never a tie
-  const long long rf = mx >> d;
-  const long long rem = mx & ((1ll << d) - 1);
-  const long long half = 1ll << (d - 1);
-  if (rem != half) {
-    const long long r = rf + (rem > half ? 1 : 0);
-    return IncPair{r, r};
-  }
-  // tie: round to the even result
-  return IncPair{rf + (rf & 1), rf + ((1 + rf) & 1)};
-}
-
-__device__ __forceinline__ long long apply(IncPair f, long long m) { return m + ((m & 1) ? f.a1 : f.a0); }
-
-__global__ void __launch_bounds__(kSumT) k_seq_sum(const double* __restrict__ x, size_t n, double* __restrict__ total,
-                                                   int* __restrict__ invalid) {
-  __shared__ IncPair s_warp[32];
-  __shared__ unsigned long long s_cross;  // first element whose running M leaves the binade
-  __shared__ long long s_mprev;            // its predecessor's M
-  __shared__ long long s_mend;             // M after the chunk (no crossing)
-  __shared__ unsigned long long s_first;   // first nonzero element (while s == 0)
-  __shared__ int s_bad;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_bad = 0;
-  double s = 0.0;  // block-uniform running sum
-  size_t pos = 0;
-  while (pos < n) {
-    if (s == 0.0) {
-      // 0.0 + x == x exactly: the sum starts at the first nonzero element
-      if (tid == 0) s_first = ~0ull;
-      __syncthreads();
-      for (int k = 0; k < kSumK; ++k) {
-        const size_t q = pos + static_cast<size_t>(k) * kSumT + tid;
-        if (q < n && x[q] != 0.0) atomicMin(&s_first, static_cast<unsigned long long>(q));
-      }
-      __syncthreads();
-      const unsigned long long f = s_first;
-      __syncthreads();
-      if (f == ~0ull) {
-        pos += kSumChunk;
-        continue;
-      }
-      s = 0.0 + x[f];  // the reference's first effective add (NaN / negative: flagged below)
-      if (!(s >= 0.0) || s == __longlong_as_double(0x7ff0000000000000ll)) {
-        if (tid == 0) *invalid = 1;
-        return;
-      }
-      pos = f + 1;
-      continue;
-    }
-    const long long sb = __double_as_longlong(s);
-    const int se = static_cast<int>((sb >> 52) & 0x7ff);
-    const int ulog = se == 0 ? -1074 : se - 1075;
-    const long long mmax = se == 0 ? (1ll << 52) : (1ll << 53);
-    const long long m0 = se == 0 ? (sb & 0xfffffffffffffll) : ((sb & 0xfffffffffffffll) | (1ll << 52));
-    // U = 2^ulog as a double (subnormal below 2^-1022); M * U is exact for M < 2^53
-    const double u = __longlong_as_double(ulog >= -1022 ? (static_cast<long long>(ulog + 1023) << 52)
-                                                         : (1ll << (ulog + 1074)));
-    // this thread's K consecutive elements
-    const size_t base = pos + static_cast<size_t>(tid) * kSumK;
-    IncPair inc[kSumK];
-    int bad = 0;
-    IncPair mine{0, 0};
-#pragma unroll
-    for (int k = 0; k < kSumK; ++k) {
-      const size_t q = base + k;
-      inc[k] = q < n ? inc_of(x[q], ulog, &bad) : IncPair{0, 0};
-      mine = compose(mine, inc[k]);
-    }
-    if (bad) s_bad = 1;
-    // block exclusive scan of the composed maps
-    IncPair incl = mine;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      IncPair y;
-      y.a0 = __shfl_up_sync(0xffffffffu, incl.a0, o);
-      y.a1 = __shfl_up_sync(0xffffffffu, incl.a1, o);
-      if (lane >= o) incl = compose(y, incl);
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    if (tid == 0) {
-      s_cross = ~0ull;
-      s_mend = -1;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      IncPair wv = s_warp[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        IncPair y;
-        y.a0 = __shfl_up_sync(0xffffffffu, wv.a0, o);
-        y.a1 = __shfl_up_sync(0xffffffffu, wv.a1, o);
-        if (lane >= o) wv = compose(y, wv);
-      }
-      s_warp[lane] = wv;  // inclusive over warps
-    }
-    __syncthreads();
-    if (s_bad) {
-      if (tid == 0) *invalid = 1;
-      return;
-    }
-    // exclusive prefix of this thread = (warps before) then (lanes before)
-    IncPair excl_lane;
-    excl_lane.a0 = __shfl_up_sync(0xffffffffu, incl.a0, 1);
-    excl_lane.a1 = __shfl_up_sync(0xffffffffu, incl.a1, 1);
-    if (lane == 0) excl_lane = IncPair{0, 0};
-    const IncPair before = warp > 0 ? compose(s_warp[warp - 1], excl_lane) : excl_lane;
-    long long m = apply(before, m0);
-    // walk this thread's elements; the first crossing in the block wins
-    if (m < mmax) {
-#pragma unroll
-      for (int k = 0; k < kSumK; ++k) {
-        const long long nm = apply(inc[k], m);
-        if (nm >= mmax) {
-          atomicMin(&s_cross, static_cast<unsigned long long>(base + k));
-          break;
-        }
-        m = nm;
-      }
-    }
-    __syncthreads();
-    const unsigned long long cross = s_cross;
-    if (cross == ~0ull) {
-      if (tid == kSumT - 1) s_mend = m;  // the block's last thread holds the chunk's end
-      __syncthreads();
-      s = static_cast<double>(s_mend) * u;
-      pos += kSumChunk;
-      __syncthreads();
-      continue;
-    }
-    // the crossing element's thread knows its predecessor's exact M
-    if (base <= cross && cross < base + kSumK) {
-      long long mp = apply(before, m0);
-      for (size_t q = base; q < cross; ++q) mp = apply(inc[q - base], mp);
-      s_mprev = mp;
-    }
-    __syncthreads();
-    const double sprev = static_cast<double>(s_mprev) * u;  // exact: M < 2^53
-    s = sprev + x[cross];                                     // the real DADD across the binade edge
-    pos = cross + 1;
-    __syncthreads();
-  }
-  if (tid == 0) *total = s;
-}
-
 // Pipelined serpentine Floyd-Steinberg (observation.cpp:11-71), bit-identical
 // to the reference's serial sweep:
 //   warp 0, lane 0: the sequential total (observation.cpp:16-17), then the
@@ -902,7 +702,8 @@ __global__ void k_observe_finalize(StepState* st, BufState* buf) {
 }  // namespace
 
 void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
-                   int* d_cells, int cap, int* d_n, double* d_mass, int* d_sum_invalid) {
+                   int* d_cells, int cap, int* d_n, double* d_mass, int* d_sum_invalid,
+                   void* sum_scratch) {
   const size_t rs = (static_cast<size_t>(w) + 3) & ~static_cast<size_t>(1);
   const size_t smem_pipe = (3 * rs + w) * sizeof(double) + 8 * static_cast<size_t>((w + 31) / 32 + 1) + 16;
   auto attr = [](const void* fn, size_t bytes) {
@@ -917,8 +718,7 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
     if (smem_pipe > 48 * 1024) attr(reinterpret_cast<const void*>(k_dither_pipe), smem_pipe);
     // the total first, as a parallel bit-exact scan (falls back to the
     // pipeline's sequential chain on negative / non-finite planes)
-    cudaMemsetAsync(d_sum_invalid, 0, sizeof(int), ctx->stream);
-    k_seq_sum<<<1, kSumT, 0, ctx->stream>>>(bm, static_cast<size_t>(w) * h, d_mass, d_sum_invalid);
+    launch_seq_sum_big(ctx, bm, static_cast<size_t>(w) * h, d_mass, d_sum_invalid, sum_scratch);
     k_dither_pipe<<<1, 64, smem_pipe, ctx->stream>>>(bm, w, h, budget, d_cells, cap, d_n, d_mass, d_sum_invalid);
     ctx->launches++;
   } else if (smem <= 200 * 1024) {
@@ -941,12 +741,6 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
     cudaMemcpyFromSymbol(clk, g_dither_clk, sizeof(clk));
     fprintf(stderr, "dither clocks: total-sum %lld, sweep %lld (chain waited %lld at row starts, %lld at row ends) cycles (%d x %d)\n", clk[1], clk[2], clk[3], clk[0], w, h);
   }
-}
-
-void launch_seq_sum(gl_context* ctx, const double* x, size_t n, double* d_total, int* d_invalid) {
-  cudaMemsetAsync(d_invalid, 0, sizeof(int), ctx->stream);
-  k_seq_sum<<<1, kSumT, 0, ctx->stream>>>(x, n, d_total, d_invalid);
-  ctx->launches++;
 }
 
 void launch_likelihoods(gl_context* ctx, const uint8_t* occ, const double* score,
