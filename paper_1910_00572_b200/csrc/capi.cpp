@@ -144,14 +144,18 @@ int halo_of(const gl_tensor* t) { return t->halo > 0 ? t->halo : 0; }
 size_t storage_elems(const gl_tensor* t) { return plane_of(t) * (t->c + 2 * halo_of(t)); }
 double* interior(const gl_tensor* t) { return t->d_buf[t->cur] + plane_of(t) * halo_of(t); }
 
+// The context's reusable device scratch. Growing it keeps its contents (an
+// operation may place data in it and then ask for more room).
 void* ensure_misc(gl_context* ctx, size_t bytes) {
   if (ctx->misc_bytes < bytes) {
+    void* fresh = nullptr;
+    CK(cudaMalloc(&fresh, bytes));
     if (ctx->d_misc) {
+      CK(cudaMemcpyAsync(fresh, ctx->d_misc, ctx->misc_bytes, cudaMemcpyDeviceToDevice, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
       CK(cudaFree(ctx->d_misc));
     }
-    ctx->d_misc = nullptr;
-    CK(cudaMalloc(&ctx->d_misc, bytes));
+    ctx->d_misc = fresh;
     ctx->misc_bytes = bytes;
   }
   return ctx->d_misc;
@@ -1492,17 +1496,28 @@ gl_status gl_argmax(gl_context* ctx, gl_tensor* t, gl_pose_estimate* out) {
   });
 }
 
+// misc scratch of a dither call: [bm plane] [n, mass, flag] [cells]
+// [sequential-sum scratch]. Callers size it with this BEFORE placing the
+// plane in it (ensure_misc reallocates, and a reallocation loses contents).
+static size_t dither_cells_bytes(size_t plane, int cap) {
+  // device capacity: every cell could emit at most once
+  const size_t dcap = std::min<size_t>(plane, static_cast<size_t>(std::max(cap, 1)));
+  return (dcap * 8 + 255) & ~static_cast<size_t>(255);
+}
+static size_t dither_misc_bytes(size_t plane, int cap) {
+  return plane * sizeof(double) + 64 + dither_cells_bytes(plane, cap) + glb::seq_sum_scratch_bytes(plane);
+}
+
 static void run_dither(gl_context* ctx, const double* d_bm, int w, int h,
                        int budget, int32_t* cells, int cap, int* n,
                        double* mass) {
   need(budget >= 1, "sample budget must be >= 1");
   need(cap >= 0 && n && mass, "bad output arguments");
   const size_t plane = static_cast<size_t>(w) * h;
-  // device capacity: every cell could emit at most once
   const size_t dcap = std::min<size_t>(plane, static_cast<size_t>(std::max(cap, 1)));
-  const size_t cells_bytes = (dcap * 8 + 255) & ~static_cast<size_t>(255);
-  char* base = static_cast<char*>(ensure_misc(ctx, plane * sizeof(double) + 64 + cells_bytes +
-                                                       glb::seq_sum_scratch_bytes(plane)));
+  const size_t cells_bytes = dither_cells_bytes(plane, cap);
+  need(ctx->misc_bytes >= dither_misc_bytes(plane, cap), "internal: dither scratch not sized by the caller");
+  char* base = static_cast<char*>(ctx->d_misc);
   // layout: [bm plane (if copied)] [n, mass, flag] [cells] [sequential-sum scratch]
   int* d_n = reinterpret_cast<int*>(base + plane * sizeof(double));
   double* d_mass = reinterpret_cast<double*>(base + plane * sizeof(double) + 8);
@@ -1530,8 +1545,7 @@ gl_status gl_dither(gl_context* ctx, const double* belief_map, int width,
     need(width >= 1 && height >= 1, "bad belief map size");
     DeviceGuard g(ctx->device);
     const size_t plane = static_cast<size_t>(width) * height;
-    double* d = static_cast<double*>(
-        ensure_misc(ctx, plane * sizeof(double) + 64 + std::min<size_t>(plane, std::max(cap, 1)) * 8));
+    double* d = static_cast<double*>(ensure_misc(ctx, dither_misc_bytes(plane, cap)));
     CK(cudaMemcpyAsync(d, belief_map, plane * sizeof(double),
                        cudaMemcpyHostToDevice, ctx->stream));
     run_dither(ctx, d, width, height, budget, cells, cap, n, source_mass);
@@ -1545,6 +1559,7 @@ gl_status gl_dither_device(gl_context* ctx, const double* d_plane, int width,
     need(ctx && d_plane, "null argument");
     need(width >= 1 && height >= 1, "bad belief map size");
     DeviceGuard g(ctx->device);
+    ensure_misc(ctx, dither_misc_bytes(static_cast<size_t>(width) * height, cap));
     run_dither(ctx, d_plane, width, height, budget, cells, cap, n, source_mass);
   });
 }
@@ -1557,8 +1572,7 @@ gl_status gl_dither_tensor(gl_context* ctx, gl_tensor* t, int budget,
     DeviceGuard g(ctx->device);
     materialize(ctx, t);
     const size_t plane = plane_of(t);
-    double* d = static_cast<double*>(
-        ensure_misc(ctx, plane * sizeof(double) + 64 + std::min<size_t>(plane, std::max(cap, 1)) * 8));
+    double* d = static_cast<double*>(ensure_misc(ctx, dither_misc_bytes(plane, cap)));
     glb::launch_belief_map(ctx, interior(t), t->w, t->h, t->c, d);
     run_dither(ctx, d, t->w, t->h, budget, cells, cap, n, source_mass);
   });
