@@ -12,8 +12,8 @@
 //     write back with set_values(). at(i,j,k) reads/writes one element.
 //   * StepScratch::t_motion receives the whole step's device time (the fused
 //     kernel has no phase boundaries); t_diffusion = t_masking = 0.
-//   * argmax_state().confidence uses a pairwise device sum (the reference's
-//     is a sequential host sum): equal to ~1e-15 relative, not bitwise.
+//   (argmax_state().confidence is bit-exact: the reference's sequential
+//   total is reproduced by a parallel binade scan.)
 #pragma once
 
 #include <cmath>

@@ -96,7 +96,7 @@ static void check_steps(const ref::OccupancyMap& rmap, b2::ThreadPool& pool, ref
   const b2::PoseEstimate be = b2::argmax_state(bt);
   EXPECT(re.i == be.i && re.j == be.j && re.k == be.k, "argmax differs");
   EXPECT(re.pose.x == be.pose.x && re.pose.y == be.pose.y && re.pose.theta == be.pose.theta, "pose differs");
-  EXPECT(std::fabs(re.confidence - be.confidence) <= 1e-12 * re.confidence, "confidence differs");
+  EXPECT(re.confidence == be.confidence, "confidence differs");
   const ref::Grid2d rbm = ref::belief_map(rt);
   const b2::Grid2d bbm = b2::belief_map(bt);
   EXPECT(bit_mismatches(bbm.data, rbm.data) == 0, "belief_map differs");
