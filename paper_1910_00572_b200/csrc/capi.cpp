@@ -8,8 +8,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
 #include <deque>
+#include <functional>
+#include <thread>
 #include <fstream>
 #include <memory>
 #include <mutex>
@@ -1602,16 +1605,89 @@ void* ensure_kind(gl_context* ctx, size_t n) {
 
 // The geometric mean's final exp with the host's glibc, like the reference
 // (observation.cpp:110): the kernel left the exponent and a case code.
+// A few persistent host workers for the glibc exp of an observation's
+// likelihoods (<= 512 * Theta values; one thread takes ~0.6 ms for 37K):
+// every worker calls the same glibc exp on the same CPU, so the results are
+// the single-threaded ones bit for bit.
+class HostPool {
+ public:
+  static HostPool& get() {
+    // never destroyed: its detached workers block on its condition variable
+    // for the life of the process (destroying it at exit could wait on them)
+    static HostPool* pool = new HostPool;
+    return *pool;
+  }
+  // run f(begin, end) over [0, n) in `parts` slices; the caller takes slice 0
+  void run(size_t n, int parts, const std::function<void(size_t, size_t)>& f) {
+    parts = std::max(1, std::min<int>(parts, static_cast<int>(workers_.size()) + 1));
+    if (parts == 1) {
+      f(0, n);
+      return;
+    }
+    std::unique_lock<std::mutex> lk(call_mu_);  // one parallel call at a time
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      job_ = &f;
+      n_ = n;
+      parts_ = parts;
+      next_ = 1;
+      pending_ = parts - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    f(0, n / parts);
+    std::unique_lock<std::mutex> g(mu_);
+    done_cv_.wait(g, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int k = static_cast<int>(std::min<unsigned>(hw > 1 ? hw - 1 : 0, 15));
+    for (int i = 0; i < k; ++i) workers_.emplace_back([this] { loop(); });
+    for (auto& t : workers_) t.detach();  // live for the process
+  }
+  void loop() {
+    unsigned long long seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> g(mu_);
+      cv_.wait(g, [&] { return gen_ != seen && next_ < parts_; });
+      seen = gen_;
+      const int part = next_++;
+      const auto* f = job_;
+      const size_t n = n_;
+      const int parts = parts_;
+      g.unlock();
+      (*f)(n * part / parts, n * (part + 1) / parts);
+      g.lock();
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, call_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(size_t, size_t)>* job_ = nullptr;
+  size_t n_ = 0;
+  int parts_ = 0, next_ = 0, pending_ = 0;
+  unsigned long long gen_ = 0;
+};
+
 void finish_likelihoods_on_host(gl_context* ctx, double* d_L, const uint8_t* d_kind, size_t n,
                                 double floor_w) {
-  std::vector<double> L(n);
-  std::vector<uint8_t> kind(n);
+  thread_local std::vector<double> L;
+  thread_local std::vector<uint8_t> kind;
+  L.resize(n);
+  kind.resize(n);
   CK(cudaMemcpyAsync(L.data(), d_L, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(kind.data(), d_kind, n, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  for (size_t q = 0; q < n; ++q) {
-    L[q] = kind[q] == 0 ? std::exp(L[q]) : (kind[q] == 1 ? floor_w : 1.0);
-  }
+  double* l = L.data();
+  const uint8_t* kd = kind.data();
+  const std::function<void(size_t, size_t)> fin = [=](size_t b, size_t e) {
+    for (size_t q = b; q < e; ++q) l[q] = kd[q] == 0 ? std::exp(l[q]) : (kd[q] == 1 ? floor_w : 1.0);
+  };
+  HostPool::get().run(n, static_cast<int>(n / 4096), fin);
   CK(cudaMemcpyAsync(d_L, L.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
 }

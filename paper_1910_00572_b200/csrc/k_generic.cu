@@ -367,21 +367,68 @@ __global__ void k_edt_rows(const double* __restrict__ sq, double* __restrict__ o
 }
 
 // belief_map (belief_tensor.cpp:500-510).
+// belief_map (belief_tensor.cpp:500-510): out = std::max over channels from
+// 0.0. The max of {0.0, v_k} does not depend on the combining order (NaN
+// never replaces a value, -0.0 never replaces +0.0), so each thread keeps 4
+// independent partial maxima over 2 cells (16-byte loads, 8 loads in flight)
+// and merges them: one HBM-speed pass.
 __global__ void k_belief_map(const double* __restrict__ B,
                              double* __restrict__ out, size_t plane, int c) {
-  for (size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-       p < plane; p += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    double m = 0.0;
-    for (int k = 0; k < c; ++k) m = dmax_ref(m, B[plane * k + p]);
-    out[p] = m;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  if ((plane & 1) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0) {
+    const size_t p2n = plane / 2;
+    const double2* B2 = reinterpret_cast<const double2*>(B);
+    double2* out2 = reinterpret_cast<double2*>(out);
+    for (size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; p < p2n; p += stride) {
+      double2 m[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) m[j] = make_double2(0.0, 0.0);
+      int k = 0;
+      for (; k + 4 <= c; k += 4) {
+        double2 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = B2[p2n * (k + j) + p];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          m[j].x = dmax_ref(m[j].x, v[j].x);
+          m[j].y = dmax_ref(m[j].y, v[j].y);
+        }
+      }
+      for (; k < c; ++k) {
+        const double2 v = B2[p2n * k + p];
+        m[0].x = dmax_ref(m[0].x, v.x);
+        m[0].y = dmax_ref(m[0].y, v.y);
+      }
+      double2 r = m[0];
+#pragma unroll
+      for (int j = 1; j < 4; ++j) {
+        r.x = dmax_ref(r.x, m[j].x);
+        r.y = dmax_ref(r.y, m[j].y);
+      }
+      out2[p] = r;
+    }
+    return;
+  }
+  for (size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; p < plane; p += stride) {
+    double m[4] = {0.0, 0.0, 0.0, 0.0};
+    int k = 0;
+    for (; k + 4 <= c; k += 4) {
+      double v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = B[plane * (k + j) + p];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) m[j] = dmax_ref(m[j], v[j]);
+    }
+    for (; k < c; ++k) m[0] = dmax_ref(m[0], B[plane * k + p]);
+    out[p] = dmax_ref(dmax_ref(m[0], m[1]), dmax_ref(m[2], m[3]));
   }
 }
 
 // argmax_state (belief_tensor.cpp:512-541): the first strictly-greater scan
 // in (k, j, i) order == the lowest flat index among the maxima (NaN never
 // wins, values must exceed -1). Two passes: per-block candidates, then one
-// block. The confidence's total is a fixed-order pairwise sum (the
-// reference's is sequential).
+// block. (The confidence's total is the reference's sequential sum,
+// k_seqsum.cu; the per-block sums here are not used for it.)
 struct ArgCand {
   double v;
   long long idx;
@@ -663,7 +710,7 @@ size_t distance_field_scratch_bytes(int w, int h) {
 void launch_belief_map(gl_context* ctx, const double* buf, int w, int h,
                        int c, double* out) {
   const size_t plane = static_cast<size_t>(w) * h;
-  k_belief_map<<<grid_for(plane, kThreads), kThreads, 0, ctx->stream>>>(
+  k_belief_map<<<grid_for((plane + 1) / 2, kThreads), kThreads, 0, ctx->stream>>>(
       buf, out, plane, c);
   ctx->launches++;
 }
