@@ -1673,22 +1673,36 @@ class HostPool {
   unsigned long long gen_ = 0;
 };
 
+// the context's pinned host scratch (grown on demand; contents not kept)
+void* ensure_host_misc(gl_context* ctx, size_t bytes) {
+  if (ctx->h_misc_bytes < bytes) {
+    if (ctx->h_misc) {
+      CK(cudaStreamSynchronize(ctx->stream));
+      CK(cudaFreeHost(ctx->h_misc));
+      ctx->h_misc = nullptr;
+      ctx->h_misc_bytes = 0;
+    }
+    CK(cudaMallocHost(&ctx->h_misc, bytes));
+    ctx->h_misc_bytes = bytes;
+  }
+  return ctx->h_misc;
+}
+
 void finish_likelihoods_on_host(gl_context* ctx, double* d_L, const uint8_t* d_kind, size_t n,
                                 double floor_w) {
-  thread_local std::vector<double> L;
-  thread_local std::vector<uint8_t> kind;
-  L.resize(n);
-  kind.resize(n);
-  CK(cudaMemcpyAsync(L.data(), d_L, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(kind.data(), d_kind, n, cudaMemcpyDeviceToHost, ctx->stream));
+  // pinned staging: the two copies each way run at full PCIe speed
+  char* h = static_cast<char*>(ensure_host_misc(ctx, n * sizeof(double) + n + 64));
+  double* l = reinterpret_cast<double*>(h);
+  uint8_t* kind = reinterpret_cast<uint8_t*>(h + n * sizeof(double));
+  CK(cudaMemcpyAsync(l, d_L, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(kind, d_kind, n, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  double* l = L.data();
-  const uint8_t* kd = kind.data();
+  const uint8_t* kd = kind;
   const std::function<void(size_t, size_t)> fin = [=](size_t b, size_t e) {
     for (size_t q = b; q < e; ++q) l[q] = kd[q] == 0 ? std::exp(l[q]) : (kd[q] == 1 ? floor_w : 1.0);
   };
   HostPool::get().run(n, static_cast<int>(n / 4096), fin);
-  CK(cudaMemcpyAsync(d_L, L.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d_L, l, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
 }
 

@@ -664,19 +664,15 @@ __global__ void k_likelihoods(const uint8_t* __restrict__ occ,
 }
 
 // Sequential mean over all sampled states (observation.cpp:139-141).
-__global__ void k_mean(const double* __restrict__ L, int total,
-                       double* __restrict__ mean) {
-  double m = 0.0;
-#pragma unroll 8
-  for (int q = 0; q < total; ++q) m += L[q];
-  *mean = m / static_cast<double>(total);
-}
-
-// B[i,j,k] *= L / mean, quotient first (observation.cpp:145-150).
+// B[i,j,k] *= L / mean, quotient first (observation.cpp:145-150); mean =
+// the sequential sum of all likelihoods (k_seqsum.cu, bit-exact) divided by
+// their count (:139-141), formed identically by every thread.
 __global__ void k_observe_apply(double* __restrict__ B, int w, int h, int c_local,
                                 int k_off, int c_total, const int* __restrict__ samples, int n,
                                 const double* __restrict__ L,
-                                const double* __restrict__ mean) {
+                                const double* __restrict__ lsum) {
+  const double mean_v = *lsum / static_cast<double>(n * c_total);
+  const double* mean = &mean_v;
   // (sample, local channel) pairs; a theta-slab shard holds global channels
   // k_off .. k_off + c_local - 1 of c_total, L is indexed s * c_total + k
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -735,12 +731,15 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
     if (e != cudaSuccess) throw std::runtime_error(std::string("dither row buffers: ") + cudaGetErrorString(e));
   }
   ctx->launches++;
+#ifdef GL_EXPERIMENT_ENV
   if (getenv("GL_DEBUG_DITHER")) {
     long long clk[4];
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpyFromSymbol(clk, g_dither_clk, sizeof(clk));
     fprintf(stderr, "dither clocks: total-sum %lld, sweep %lld (chain waited %lld at row starts, %lld at row ends) cycles (%d x %d)\n", clk[1], clk[2], clk[3], clk[0], w, h);
   }
+#endif
+
 }
 
 void launch_likelihoods(gl_context* ctx, const uint8_t* occ, const double* score,
@@ -760,11 +759,14 @@ void launch_likelihoods(gl_context* ctx, const uint8_t* occ, const double* score
 void launch_observe_apply(gl_context* ctx, double* buf, int w, int h, int c_local,
                           int k_off, int c_total, const int* d_samples, int n,
                           const double* d_L, double* d_mean) {
-  k_mean<<<1, 1, 0, ctx->stream>>>(d_L, n * c_total, d_mean);
+  // d_mean[0]: the likelihoods' sequential sum; d_mean[1]: scan-domain flag
+  int* flag = reinterpret_cast<int*>(d_mean + 1);
+  launch_seq_sum(ctx, d_L, static_cast<size_t>(n) * c_total, d_mean, flag);
+  launch_seq_sum_chain(ctx, d_L, static_cast<size_t>(n) * c_total, d_mean, flag);  // only if flagged
   const int total = n * c_local;
   k_observe_apply<<<(total + 127) / 128, 128, 0, ctx->stream>>>(
       buf, w, h, c_local, k_off, c_total, d_samples, n, d_L, d_mean);
-  ctx->launches += 2;
+  ctx->launches++;
 }
 
 void launch_observe_finalize(gl_context* ctx, StepState* st, BufState* buf) {
