@@ -660,8 +660,28 @@ def run_sharded(args, cfg, world, rank, local):
     ks = g.build_kernels(g.MotionNoise(), C, m.resolution(), 2.0 * math.pi / C)
     act = g.make_activation(m, ks, C, ctx)
     halo = max(1, len(ks.angular) // 2)
-    shard = ThetaShard(m, C, halo, rank, world, ctx, exchange=args.exchange)
     u = g.OdometryDelta(m.resolution(), 0.0, 0.0)
+    single = None
+    if world > 1:
+        # the same workload on ONE GPU in the same run (rank 0, before its
+        # shard exists, the other ranks wait): the N = 1 point of this
+        # config's strong-scaling curve, measured on this box
+        if rank == 0:
+            t1 = g.init_uniform(m, C, ctx)
+            for _ in range(3):
+                g.step_async(t1, u, m, ks, act, ctx)
+            ctx.synchronize()
+            n1 = max(5, min(args.steps, 50))
+            ctx.mark(0)
+            for _ in range(n1):
+                g.step_async(t1, u, m, ks, act, ctx)
+            ctx.mark(1)
+            single = {"value": n1 / (ctx.marks_ms(0, 1) / 1e3), "unit": "Hz", "steps": n1,
+                      "how": "the unsharded step of the same belief on rank 0's GPU alone, before sharding"}
+            g.tensor_status(t1)
+            del t1
+        dist_barrier(world)
+    shard = ThetaShard(m, C, halo, rank, world, ctx, exchange=args.exchange)
     for _ in range(args.warmup):
         shard.step(u, ks, act)
     ctx.synchronize()
@@ -727,6 +747,8 @@ def run_sharded(args, cfg, world, rank, local):
                      "note": "rank 0's fused kernel on its slab (per-GPU roofline)"},
         "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
     }
+    if single:
+        line["extras"] = {"single_gpu_same_config": single}
     print(json.dumps(line))
     return 0
 
