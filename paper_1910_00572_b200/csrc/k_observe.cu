@@ -235,115 +235,6 @@ __device__ __forceinline__ bool fs_spec_pipe(const double* __restrict__ pre, dou
   }
 }
 
-#ifndef GL_FS_PREFETCH3
-#define GL_FS_PREFETCH3 1
-#endif
-// fs_spec_pipe with three register buffers: group g runs its chain on buffer
-// g % 3 while it screens and stores group g-1 (buffer (g+2) % 3) and loads
-// group g+1's pre-accumulated values into buffer (g+1) % 3, so no group
-// starts by waiting for its own shared-memory loads. Same values, same
-// verification and replay as fs_spec_pipe.
-template <bool kConstC>
-__device__ __forceinline__ bool fs_spec_pipe3(const double* __restrict__ pre, double* __restrict__ err,
-                                              const unsigned int* __restrict__ sup, int& q,
-                                              double& carry, double c_reg, int w,
-                                              volatile int* progress) {
-  constexpr int G = 32;
-  const double c = kConstC ? 7.0 / 16.0 : c_reg;
-  if (q + G > w - 1) return false;
-  double2 pb[3][G / 2];
-  {
-    const double2* p2 = reinterpret_cast<const double2*>(pre + q + 1);
-#pragma unroll
-    for (int k = 0; k < G / 2; ++k) pb[0][k] = p2[k];
-  }
-  int q_p = 0;
-  double carry_p = 0.0;
-  int npub = 0;
-  auto emits = [&](auto Pt) -> bool {
-    constexpr int P = decltype(Pt)::value;
-    const unsigned long long sw = static_cast<unsigned long long>(sup[q_p >> 5]) |
-                                  (static_cast<unsigned long long>(sup[(q_p >> 5) + 1]) << 32);
-    const unsigned int swq = static_cast<unsigned int>(sw >> (q_p & 31));
-    int ms = 0;
-#pragma unroll
-    for (int k = 0; k < G / 2; ++k) {
-      ms = max(ms, __double2hiint(pb[P][k].x) & -static_cast<int>((swq >> (2 * k)) & 1u));
-      ms = max(ms, __double2hiint(pb[P][k].y) & -static_cast<int>((swq >> (2 * k + 1)) & 1u));
-    }
-    return ms >= 0x3FE00000;
-  };
-  // 0 = continue, 1 = replay (q, carry set), 2 = tail reached
-  auto group = [&](auto Bt, auto Pendt) -> int {
-    constexpr int B = decltype(Bt)::value;
-    constexpr int P = (B + 2) % 3;
-    constexpr int N = (B + 1) % 3;
-    constexpr bool pend = decltype(Pendt)::value;
-    const int qn = q + G;
-    const bool more = qn + G <= w - 1;
-    const double2* pn2 = reinterpret_cast<const double2*>(pre + qn + 1);
-    double2* ep = reinterpret_cast<double2*>(err + q_p + 1);
-    double cr = carry;
-    int hm = 0;
-#pragma unroll
-    for (int k = 0; k < G / 2; ++k) {
-      const double2 in = pb[B][k];
-      const double v0 = in.x + cr;
-      cr = v0 * c;
-      const double v1 = in.y + cr;
-      cr = v1 * c;
-      pb[B][k] = make_double2(v0, v1);
-      if constexpr (pend) {  // the previous group: long-ready registers, off the chain
-        hm = max(hm, max(__double2hiint(pb[P][k].x), __double2hiint(pb[P][k].y)));
-        ep[k] = pb[P][k];
-      }
-      if (more) pb[N][k] = pn2[k];  // the next group's values, long before it needs them
-    }
-    if constexpr (pend) {
-      if (__builtin_expect(hm >= 0x3FE00000, 0) && emits(std::integral_constant<int, P>{})) {
-        q = q_p;  // replay the pending group; this group's values are dropped
-        carry = carry_p;
-        return 1;
-      }
-      if (++npub == GL_FS_PUBN) {
-        npub = 0;
-        fence_cta();
-        *progress = q;
-      }
-    }
-    q_p = q;
-    carry_p = carry;
-    carry = cr;
-    q = qn;
-    if (more) return 0;
-    int hl = 0;
-    double2* el = reinterpret_cast<double2*>(err + q_p + 1);
-#pragma unroll
-    for (int k = 0; k < G / 2; ++k) {
-      hl = max(hl, max(__double2hiint(pb[B][k].x), __double2hiint(pb[B][k].y)));
-      el[k] = pb[B][k];
-    }
-    if (__builtin_expect(hl >= 0x3FE00000, 0) && emits(std::integral_constant<int, B>{})) {
-      q = q_p;
-      carry = carry_p;
-      return 1;
-    }
-    fence_cta();
-    *progress = q;
-    return 2;
-  };
-  int r = group(std::integral_constant<int, 0>{}, std::false_type{});
-  if (r) return r == 1;
-  for (;;) {
-    r = group(std::integral_constant<int, 1>{}, std::true_type{});
-    if (r) return r == 1;
-    r = group(std::integral_constant<int, 2>{}, std::true_type{});
-    if (r) return r == 1;
-    r = group(std::integral_constant<int, 0>{}, std::true_type{});
-    if (r) return r == 1;
-  }
-}
-
 __device__ long long g_dither_clk[4];  // phase timestamps (debug read-out)
 
 __global__ void __launch_bounds__(64) k_dither_pipe(
@@ -527,10 +418,7 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
       auto sweep = [&](auto gsize) {
         constexpr int G = decltype(gsize)::value;
         auto spec = [&]() {
-          if constexpr (G == 32 && GL_FS_PREFETCH3) {
-            return c_mid == 7.0 / 16.0 ? fs_spec_pipe3<true>(pre, err, sup, q, carry, c_mid, w, &progress)
-                                       : fs_spec_pipe3<false>(pre, err, sup, q, carry, c_mid, w, &progress);
-          } else if constexpr (G == 32) {
+          if constexpr (G == 32) {
             return c_mid == 7.0 / 16.0 ? fs_spec_pipe<true>(pre, err, sup, q, carry, c_mid, w, &progress)
                                        : fs_spec_pipe<false>(pre, err, sup, q, carry, c_mid, w, &progress);
           } else {
