@@ -722,7 +722,7 @@ def run_sharded(args, cfg, world, rank, local):
     achieved = bytes_launch / (avg_kern_ms / 1e3) / 1e9
     peak, peak_src = measured_peak()
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the CPU baseline is an N = 1 figure
         cpu = sharded_cpu_baseline(cfg, args.cpu_budget_s) if W * H * C * 40 > 40e9 else \
             cpu_baseline(make_map_bytes(W, H), cfg, budget_s=args.cpu_budget_s)
     shard.close()
