@@ -140,6 +140,9 @@ class ThreadPool {
   }
   int thread_count() const { return 1; }
   gl_context* get() const { return ctx_.get(); }
+  // the wall-crossing mask extension for every step on this device context
+  // (off by default: the reference masks destination cells only)
+  void set_wall_mask(bool enable) { check(gl_context_set_wall_mask(ctx_.get(), enable ? 1 : 0)); }
   static ThreadPool& default_pool() {
     static ThreadPool pool(0, 0);
     return pool;
