@@ -240,8 +240,9 @@ __device__ long long g_dither_clk[4];  // phase timestamps (debug read-out)
 __global__ void __launch_bounds__(64) k_dither_pipe(
     const double* __restrict__ bm, int w, int h, int budget,
     int* __restrict__ cells, int cap, int* __restrict__ n_out,
-    double* __restrict__ mass_out, const int* __restrict__ sum_invalid) {
+    double* __restrict__ mass_out, const int* __restrict__ sum_invalid, const int* __restrict__ seg_done) {
   extern __shared__ double sh2[];
+  if (seg_done != nullptr && *seg_done) return;  // k_dither_seg swept this plane
   // rows of RS doubles (scan order at index q + 1; RS even keeps 16-byte
   // alignment)
   const int RS = (w + 3) & ~1;
@@ -526,6 +527,224 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Segment-parallel serpentine Floyd-Steinberg (round 2). Inside a row the
+// reference's carry chain e_q -> v_{q+1} = pre + e_q * (7/16) CONTRACTS: two
+// chains started from different carries meet bitwise after ~45-60 pixels
+// (the difference shrinks by 7/16 per pixel until one rounding merges them,
+// and from then on the same state gives the same future — emissions
+// included). So every row is cut into P <= 32 segments run by the lanes of
+// one warp at once: lane l starts kSegWU pixels before its segment with a
+// guessed carry 0 (a warm-up over the previous segment's tail, recording
+// nothing), then runs its own segment exactly as the reference would from
+// that state. Lane 0 starts at the row's first pixel, exactly. Afterwards
+// lane 0 verifies the segments in order: lane l is exact iff its warm-up's
+// last error equals, bit for bit, the true error lane l-1 left at that pixel
+// (then both carries into the segment are equal). If not, lane 0 reruns
+// lane l's segment exactly from the true carry until its error coincides
+// bitwise with lane l's, taking the true emissions up to that pixel and lane
+// l's after it. Emissions are gathered per lane and written in scan order.
+// Every value and every emission is the reference's; the sequential work per
+// row drops from W pixels to ~W/P + kSegWU. Rows whose lane lists overflow,
+// the last row (no row below: carry coefficient 1, no contraction) and
+// narrow rows run the exact sequential chain on lane 0. The next row's
+// pre-accumulation runs on all warps between rows.
+#ifndef GL_FS_SEG
+#define GL_FS_SEG 1  // the segment-parallel sweep (0: the pipelined chain only)
+#endif
+constexpr int kSegT = 128;     // threads (4 warps: warp 0 runs the chains; all warps the pre pass)
+constexpr int kSegWU = 64;     // warm-up pixels of lanes 1..P-1
+constexpr int kSegEMax = 8;    // emissions per lane per row before the row falls back
+__host__ __device__ __forceinline__ int seg_pidx(int q) { return q + (q >> 5); }  // 64-bit bank spread
+
+__global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__ bm, int w, int h, int budget,
+                                                      int* __restrict__ cells, int cap, int* __restrict__ n_out,
+                                                      const double* __restrict__ total_in,
+                                                      const int* __restrict__ sum_invalid, int* __restrict__ done) {
+  extern __shared__ double segsh[];
+  const int WP = seg_pidx(w) + 2;
+  double* pre = segsh;                 // row j's pre-accumulated work, scan order, padded index
+  double* err = segsh + WP;            // row j's errors, scan order, padded index
+  double* nrow = segsh + 2 * WP;       // row j+1 of bm (staged by warps 1..3)
+  unsigned int* sup = reinterpret_cast<unsigned int*>(segsh + 3 * WP);  // support bits, scan order
+  int* elist = reinterpret_cast<int*>(sup + (w + 31) / 32 + 1);          // [32][kSegEMax] lane emissions
+  __shared__ double s_wu[32];  // lane l's warm-up error at its segment's first pixel - 1
+  __shared__ int s_ne[32];     // lane l's emission count (> kSegEMax: overflow)
+  __shared__ int s_count;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (*sum_invalid) {  // negative / non-finite plane: k_dither_pipe's sequential total takes it
+    if (tid == 0) *done = 0;
+    return;
+  }
+  const double total = *total_in;
+  if (!(total > 0.0)) {
+    if (tid == 0) {
+      *n_out = 0;
+      *done = 1;
+    }
+    return;
+  }
+  const double scale = budget / total;
+  if (tid == 0) s_count = 0;
+  // segments: P lanes of S pixels (P = 1 for narrow rows)
+  const int P = w >= 2 * kSegWU ? min(32, w / 32) : 1;
+  const int S = (w + P - 1) / P;
+  auto seg_start = [&](int l) { return min(w, l * S); };
+
+  // row 0: pre = work, no error inflow (observation.cpp:23-25)
+  for (int pos = tid; pos < w; pos += kSegT) pre[seg_pidx(pos)] = bm[pos] * scale;  // dir = +1
+  for (int wd = warp; wd <= w / 32; wd += kSegT / 32) {
+    const int q = wd * 32 + lane;
+    const unsigned int bits = __ballot_sync(0xffffffffu, q < w && bm[q] > 0.0);
+    if (lane == 0) sup[wd] = bits;
+  }
+  __syncthreads();
+
+  for (int j = 0; j < h; ++j) {
+    const int dir = (j % 2 == 0) ? 1 : -1;
+    const int start = dir == 1 ? 0 : w - 1;
+    const double c_first = fs_carry_coef(start, j, w, h, dir);
+    const double c_mid = (w > 2) ? fs_carry_coef(start + dir, j, w, h, dir) : 0.0;
+    auto supp = [&](int q) { return (sup[q >> 5] >> (q & 31)) & 1u; };
+    auto emit_out = [&](int q) {  // lane 0 only, in scan order
+      const int c = s_count;
+      if (c < cap) {
+        cells[2 * c] = start + q * dir;
+        cells[2 * c + 1] = j;
+      }
+      s_count = c + 1;
+    };
+    // the reference's exact sweep of scan positions [q0, q1) from `carry`,
+    // writing err and emitting; returns the carry after q1 - 1
+    auto exact = [&](int q0, int q1, double carry) {
+      for (int q = q0; q < q1; ++q) {
+        const double v = q == 0 ? pre[seg_pidx(0)] : pre[seg_pidx(q)] + carry;
+        double e = v;
+        if (v >= 0.5 && supp(q)) {
+          e = v - 1.0;
+          emit_out(q);
+        }
+        err[seg_pidx(q)] = e;
+        carry = e * (q == 0 ? c_first : c_mid);
+      }
+      return carry;
+    };
+    const bool seq = (j == h - 1) || P == 1;
+    if (warp == 0) {
+      if (seq) {
+        if (lane == 0) exact(0, w, 0.0);
+      } else {
+        // ---- every lane's segment at once (lanes >= P idle) ----
+        const int qs = seg_start(lane), qe = seg_start(lane + 1);
+        const bool act = lane < P;
+        int q = lane == 0 ? 0 : max(1, qs - kSegWU);
+        double carry = 0.0;  // the guess (exact for lane 0: the row's first pixel has no carry in)
+        int ne = 0;
+        double wu = 0.0;
+        const int n_steps = (lane == 0 ? qe : qe - q);
+        for (int it = 0; it < S + kSegWU; ++it, ++q) {
+          if (!act || it >= n_steps) continue;
+          const double v = q == 0 ? pre[seg_pidx(0)] : pre[seg_pidx(q)] + carry;
+          const bool em = v >= 0.5 && supp(q);
+          const double e = em ? v - 1.0 : v;
+          if (q >= qs) {
+            err[seg_pidx(q)] = e;
+            if (em) {
+              if (ne < kSegEMax) elist[lane * kSegEMax + ne] = q;
+              ++ne;
+            }
+          } else if (q == qs - 1) {
+            wu = e;
+          }
+          carry = e * (q == 0 ? c_first : c_mid);
+        }
+        if (act) {
+          s_wu[lane] = wu;
+          s_ne[lane] = ne;
+        }
+        __syncwarp();
+        // ---- lane 0: verify in order, fix up, emit in scan order ----
+        if (lane == 0) {
+          bool overflow = false;
+          for (int l = 0; l < P; ++l) overflow = overflow || s_ne[l] > kSegEMax;
+          if (overflow) {
+            exact(0, w, 0.0);  // redo the row exactly
+          } else {
+            for (int l = 0; l < P; ++l) {
+              const int ls = seg_start(l), le = seg_start(l + 1);
+              int from = ls;  // lane l's own emissions at positions >= from are valid
+              if (l > 0) {
+                const double et = err[seg_pidx(ls - 1)];
+                if (__double_as_longlong(et) != __double_as_longlong(s_wu[l])) {
+                  // rerun lane l's segment exactly until it meets lane l's errors
+                  double carry = et * (ls - 1 == 0 ? c_first : c_mid);
+                  from = le;
+                  for (int qq = ls; qq < le; ++qq) {
+                    const double v = pre[seg_pidx(qq)] + carry;
+                    double e = v;
+                    if (v >= 0.5 && supp(qq)) {
+                      e = v - 1.0;
+                      emit_out(qq);
+                    }
+                    const double spec = err[seg_pidx(qq)];
+                    err[seg_pidx(qq)] = e;
+                    carry = e * c_mid;
+                    if (__double_as_longlong(e) == __double_as_longlong(spec)) {
+                      from = qq + 1;
+                      break;
+                    }
+                  }
+                }
+              }
+              for (int k = 0; k < s_ne[l]; ++k) {
+                const int qk = elist[l * kSegEMax + k];
+                if (qk >= from) emit_out(qk);
+              }
+            }
+          }
+        }
+      }
+    } else if (j + 1 < h) {
+      // warps 1..3 stage row j+1 of bm while warp 0 sweeps row j
+      const double* brow = bm + static_cast<size_t>(j + 1) * w;
+      for (int t = tid - 32; t < w; t += kSegT - 32) nrow[t] = brow[t];
+    }
+    __syncthreads();
+    if (j + 1 < h) {
+      // ---- row j+1's pre-accumulation (all warps), the helper's arithmetic ----
+      const int pd = dir, dn = -pd;
+      const int start_n = dn == 1 ? 0 : w - 1;
+      const double w_lo = fs_wsum(0, j, w, h, pd), w_hi = fs_wsum(w - 1, j, w, h, pd);
+      const double e1[2] = {(1.0 / 16.0) / w_lo, (1.0 / 16.0) / w_hi};
+      const double e5[2] = {(5.0 / 16.0) / w_lo, (5.0 / 16.0) / w_hi};
+      const double e3[2] = {(3.0 / 16.0) / w_lo, (3.0 / 16.0) / w_hi};
+      auto coef = [&](int sc, double wt, const double* edge) {
+        return sc == 0 ? edge[0] : (sc == w - 1 ? edge[1] : wt);
+      };
+      // pre (row j) is dead once row j is swept: overwrite it in place
+      for (int pos = tid; pos < w; pos += kSegT) {
+        const int t = pd == 1 ? pos : w - 1 - pos;
+        double v = nrow[t] * scale;
+        if (pos >= 1) v += err[seg_pidx(pos - 1)] * coef(t - pd, 1.0 / 16.0, e1);
+        v += err[seg_pidx(pos)] * coef(t, 5.0 / 16.0, e5);
+        if (pos + 1 < w) v += err[seg_pidx(pos + 1)] * coef(t + pd, 3.0 / 16.0, e3);
+        pre[seg_pidx(w - 1 - pos)] = v;  // row j+1 scans the other way
+      }
+      // support bits of row j+1 in its scan order
+      for (int wd = warp; wd <= w / 32; wd += kSegT / 32) {
+        const int qn = wd * 32 + lane;
+        const unsigned int bits = __ballot_sync(0xffffffffu, qn < w && nrow[start_n + qn * dn] > 0.0);
+        if (lane == 0) sup[wd] = bits;
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    *n_out = s_count;
+    *done = 1;
+  }
+}
+
 // dither_samples as a row decomposition that is bit-identical to the
 // reference's serial sweep (probe P2):
 //   * total: one sequential sum (observation.cpp:16-17), lane 0;
@@ -710,12 +929,25 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
     }
   };
   const size_t smem = static_cast<size_t>(2) * w * sizeof(double);
+  const size_t smem_seg = (3 * static_cast<size_t>(seg_pidx(w) + 2)) * sizeof(double) +
+                          4 * static_cast<size_t>((w + 31) / 32 + 1) + 32 * kSegEMax * 4 + 64;
   if (smem_pipe <= 200 * 1024) {
     if (smem_pipe > 48 * 1024) attr(reinterpret_cast<const void*>(k_dither_pipe), smem_pipe);
     // the total first, as a parallel bit-exact scan (falls back to the
     // pipeline's sequential chain on negative / non-finite planes)
     launch_seq_sum_big(ctx, bm, static_cast<size_t>(w) * h, d_mass, d_sum_invalid, sum_scratch);
-    k_dither_pipe<<<1, 64, smem_pipe, ctx->stream>>>(bm, w, h, budget, d_cells, cap, d_n, d_mass, d_sum_invalid);
+    // the segment-parallel sweep where the plane is in the scan's domain;
+    // the pipelined kernel then only runs if it could not (a device flag)
+    int* d_done = d_sum_invalid + 1;
+    const bool seg = GL_FS_SEG && w >= 2 * kSegWU && smem_seg <= 200 * 1024;
+    if (seg) {
+      if (smem_seg > 48 * 1024) attr(reinterpret_cast<const void*>(k_dither_seg), smem_seg);
+      k_dither_seg<<<1, kSegT, smem_seg, ctx->stream>>>(bm, w, h, budget, d_cells, cap, d_n, d_mass, d_sum_invalid,
+                                                        d_done);
+      ctx->launches++;
+    }
+    k_dither_pipe<<<1, 64, smem_pipe, ctx->stream>>>(bm, w, h, budget, d_cells, cap, d_n, d_mass, d_sum_invalid,
+                                                     seg ? d_done : nullptr);
     ctx->launches++;
   } else if (smem <= 200 * 1024) {
     attr(reinterpret_cast<const void*>(k_dither), smem);
