@@ -634,65 +634,127 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
       if (seq) {
         if (lane == 0) exact(0, w, 0.0);
       } else {
-        // ---- every lane's segment at once (lanes >= P idle) ----
+        // ---- every lane's segment at once (lanes >= P idle), 16-pixel
+        // groups: the group's pre values and support bits are loaded up
+        // front, the chain runs assuming no emission (one DADD and one DMUL
+        // per pixel) and is replayed exactly, by the lanes that need it,
+        // when any lane's group holds a supported v >= 0.5 ----
         const int qs = seg_start(lane), qe = seg_start(lane + 1);
         const bool act = lane < P;
-        int q = lane == 0 ? 0 : max(1, qs - kSegWU);
+        const int q0 = lane == 0 ? 0 : max(1, qs - kSegWU);
         double carry = 0.0;  // the guess (exact for lane 0: the row's first pixel has no carry in)
         int ne = 0;
         double wu = 0.0;
-        const int n_steps = (lane == 0 ? qe : qe - q);
-        for (int it = 0; it < S + kSegWU; ++it, ++q) {
-          if (!act || it >= n_steps) continue;
-          const double v = q == 0 ? pre[seg_pidx(0)] : pre[seg_pidx(q)] + carry;
-          const bool em = v >= 0.5 && supp(q);
-          const double e = em ? v - 1.0 : v;
-          if (q >= qs) {
-            err[seg_pidx(q)] = e;
-            if (em) {
-              if (ne < kSegEMax) elist[lane * kSegEMax + ne] = q;
-              ++ne;
-            }
-          } else if (q == qs - 1) {
-            wu = e;
+        const int n_grp = (S + kSegWU + 15) / 16;
+        for (int gi = 0; gi < n_grp; ++gi) {
+          const int base = q0 + 16 * gi;
+          const int valid = act ? max(0, min(16, qe - base)) : 0;
+          if (!__any_sync(0xffffffffu, valid > 0)) break;
+          double p[16], v[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) p[k] = k < valid ? pre[seg_pidx(base + k)] : 0.0;
+          const int wd = base >> 5, sh = base & 31;
+          const unsigned long long sw2 = valid > 0 ? (static_cast<unsigned long long>(sup[wd]) |
+                                                      (static_cast<unsigned long long>(sup[wd + 1]) << 32))
+                                                   : 0ull;
+          const unsigned int sb = static_cast<unsigned int>(sw2 >> sh) & ((valid >= 16) ? 0xffffu : ((1u << valid) - 1u));
+          const double c0 = carry;
+          double c = c0;
+          int hm = 0;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const double vk = (base + k == 0) ? p[k] : p[k] + c;  // pixel 0: no carry in
+            v[k] = vk;
+            asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(vk), "d"(base + k == 0 ? c_first : c_mid));
+            hm = max(hm, __double2hiint(vk) & -static_cast<int>((sb >> k) & 1u));
           }
-          carry = e * (q == 0 ? c_first : c_mid);
+          const bool need = hm >= 0x3FE00000;
+          unsigned int emask = 0;
+          if (__any_sync(0xffffffffu, need)) {
+            if (need) {  // the exact sweep of this group
+              c = c0;
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                const double vk = (base + k == 0) ? p[k] : p[k] + c;
+                const bool em = vk >= 0.5 && ((sb >> k) & 1u);
+                const double e = em ? vk - 1.0 : vk;
+                emask |= static_cast<unsigned int>(em) << k;
+                v[k] = e;
+                asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(e), "d"(base + k == 0 ? c_first : c_mid));
+              }
+            }
+          }
+          carry = c;
+          // errors of the own segment, the warm-up's last error, emissions
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int q = base + k;
+            if (k < valid && q >= qs) err[seg_pidx(q)] = v[k];
+            if (k < valid && q == qs - 1) wu = v[k];
+          }
+          emask &= ~((qs > base) ? ((qs - base >= 32) ? 0xffffffffu : ((1u << (qs - base)) - 1u)) : 0u);
+          while (emask) {
+            const int k = __ffs(emask) - 1;
+            emask &= emask - 1;
+            if (ne < kSegEMax) elist[lane * kSegEMax + ne] = base + k;
+            ++ne;
+          }
         }
         if (act) {
           s_wu[lane] = wu;
           s_ne[lane] = ne;
         }
         __syncwarp();
-        // ---- lane 0: verify in order, fix up, emit in scan order ----
+        // ---- verify: lane l is exact iff its warm-up's last error equals
+        // lane l-1's error at that pixel and lane l-1 is exact ----
+        const bool ovf = __any_sync(0xffffffffu, act && ne > kSegEMax);
+        const bool ok_l = !act || lane == 0 || (__double_as_longlong(err[seg_pidx(qs - 1)]) == __double_as_longlong(wu));
+        const unsigned int bad = __ballot_sync(0xffffffffu, !ok_l);
+        const int first_bad = bad ? __ffs(bad) - 1 : P;  // lanes below it are exact
+        const int c_base = s_count;
+        // emissions of the exact lanes, in scan order (a warp prefix sum)
+        const int mine = (act && lane < first_bad && !ovf) ? ne : 0;
+        int incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        for (int k = 0; k < mine; ++k) {
+          const int c = c_base + incl - mine + k;
+          if (c < cap) {
+            cells[2 * c] = start + elist[lane * kSegEMax + k] * dir;
+            cells[2 * c + 1] = j;
+          }
+        }
+        __syncwarp();
         if (lane == 0) {
-          bool overflow = false;
-          for (int l = 0; l < P; ++l) overflow = overflow || s_ne[l] > kSegEMax;
-          if (overflow) {
-            exact(0, w, 0.0);  // redo the row exactly
+          if (ovf) {
+            exact(0, w, 0.0);  // a lane's list overflowed: redo the row exactly
           } else {
-            for (int l = 0; l < P; ++l) {
+            s_count = c_base + tot;
+            // the remaining lanes in order (rare): fix up, then emit
+            for (int l = first_bad; l < P; ++l) {
               const int ls = seg_start(l), le = seg_start(l + 1);
-              int from = ls;  // lane l's own emissions at positions >= from are valid
-              if (l > 0) {
-                const double et = err[seg_pidx(ls - 1)];
-                if (__double_as_longlong(et) != __double_as_longlong(s_wu[l])) {
-                  // rerun lane l's segment exactly until it meets lane l's errors
-                  double carry = et * (ls - 1 == 0 ? c_first : c_mid);
-                  from = le;
-                  for (int qq = ls; qq < le; ++qq) {
-                    const double v = pre[seg_pidx(qq)] + carry;
-                    double e = v;
-                    if (v >= 0.5 && supp(qq)) {
-                      e = v - 1.0;
-                      emit_out(qq);
-                    }
-                    const double spec = err[seg_pidx(qq)];
-                    err[seg_pidx(qq)] = e;
-                    carry = e * c_mid;
-                    if (__double_as_longlong(e) == __double_as_longlong(spec)) {
-                      from = qq + 1;
-                      break;
-                    }
+              int from = ls;
+              const double et = err[seg_pidx(ls - 1)];
+              if (__double_as_longlong(et) != __double_as_longlong(s_wu[l])) {
+                double cr = et * (ls - 1 == 0 ? c_first : c_mid);
+                from = le;
+                for (int qq = ls; qq < le; ++qq) {
+                  const double vv = pre[seg_pidx(qq)] + cr;
+                  double e = vv;
+                  if (vv >= 0.5 && supp(qq)) {
+                    e = vv - 1.0;
+                    emit_out(qq);
+                  }
+                  const double spec = err[seg_pidx(qq)];
+                  err[seg_pidx(qq)] = e;
+                  cr = e * c_mid;
+                  if (__double_as_longlong(e) == __double_as_longlong(spec)) {
+                    from = qq + 1;
+                    break;
                   }
                 }
               }
