@@ -533,41 +533,66 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
 // chains started from different carries meet bitwise after ~45-60 pixels
 // (the difference shrinks by 7/16 per pixel until one rounding merges them,
 // and from then on the same state gives the same future — emissions
-// included). So every row is cut into P <= 32 segments run by the lanes of
-// one warp at once: lane l starts kSegWU pixels before its segment with a
-// guessed carry 0 (a warm-up over the previous segment's tail, recording
-// nothing), then runs its own segment exactly as the reference would from
-// that state. Lane 0 starts at the row's first pixel, exactly. Afterwards
-// lane 0 verifies the segments in order: lane l is exact iff its warm-up's
-// last error equals, bit for bit, the true error lane l-1 left at that pixel
-// (then both carries into the segment are equal). If not, lane 0 reruns
-// lane l's segment exactly from the true carry until its error coincides
-// bitwise with lane l's, taking the true emissions up to that pixel and lane
-// l's after it. Emissions are gathered per lane and written in scan order.
-// Every value and every emission is the reference's; the sequential work per
-// row drops from W pixels to ~W/P + kSegWU. Rows whose lane lists overflow,
-// the last row (no row below: carry coefficient 1, no contraction) and
-// narrow rows run the exact sequential chain on lane 0. The next row's
-// pre-accumulation runs on all warps between rows.
+// included). So every row is cut into segments run by the lanes of one warp
+// at once. Lane 0 runs [0, F) exactly from the row's first pixel; lane l >= 1
+// runs segment [s_l, s_l + S) but starts kSegWU pixels early with a guessed
+// carry 0 (a warm-up over the previous segment's tail that records
+// nothing). Segments are S pixels apart with S odd, so the lanes' shared-
+// memory accesses fall in distinct banks. Each lane works in 16-pixel
+// groups: values loaded up front, the chain run assuming no emission (one
+// DADD and one DMUL per pixel), the group replayed exactly by the lanes that
+// need it when any lane's group holds a supported v >= 0.5. Then: lane l is
+// exact iff its warm-up's last error equals, bit for bit, the error at that
+// pixel of an exact lane l-1 (the carries into the segment are then equal).
+// The exact lanes' emissions go out in scan order through a warp prefix
+// sum; from the first lane that fails, lane 0 reruns segments exactly from
+// the true carry until they meet the lanes' own errors, taking the true
+// emissions up to that pixel and the lane's after it. Every value and every
+// emission is the reference's. Rows whose lane lists overflow, the last row
+// (no row below: carry coefficient 1, no contraction) and narrow rows run
+// the exact sequential chain on lane 0. The next row's pre-accumulation runs
+// on all warps between rows, from the row's errors in shared memory.
 #ifndef GL_FS_SEG
 #define GL_FS_SEG 1  // the segment-parallel sweep (0: the pipelined chain only)
 #endif
 constexpr int kSegT = 128;     // threads (4 warps: warp 0 runs the chains; all warps the pre pass)
-constexpr int kSegWU = 64;     // warm-up pixels of lanes 1..P-1
+constexpr int kSegWU = 64;     // warm-up pixels of lanes 1..31
 constexpr int kSegEMax = 8;    // emissions per lane per row before the row falls back
-__host__ __device__ __forceinline__ int seg_pidx(int q) { return q + (q >> 5); }  // 64-bit bank spread
+
+struct SegLayout {
+  int P, F, S;  // lanes in use, lane 0's length, segment stride (odd)
+  __host__ __device__ int start(int l) const { return l == 0 ? 0 : min(w_, F + (l - 1) * S); }
+  int w_;
+};
+
+__host__ __device__ inline SegLayout seg_layout(int w) {
+  SegLayout L{};
+  L.w_ = w;
+  if (w < 4 * kSegWU) {
+    L.P = 1;
+    L.F = w;
+    L.S = w;
+    return L;
+  }
+  int S = (w - kSegWU + 31) / 32;  // 32 lanes, lane 0 takes S + kSegWU (every lane runs ~S + kSegWU pixels)
+  S |= 1;
+  L.S = S;
+  L.F = min(w, S + kSegWU);
+  L.P = 1 + (w - L.F + S - 1) / S;
+  return L;
+}
 
 __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__ bm, int w, int h, int budget,
                                                       int* __restrict__ cells, int cap, int* __restrict__ n_out,
                                                       const double* __restrict__ total_in,
                                                       const int* __restrict__ sum_invalid, int* __restrict__ done) {
   extern __shared__ double segsh[];
-  const int WP = seg_pidx(w) + 2;
-  double* pre = segsh;                 // row j's pre-accumulated work, scan order, padded index
-  double* err = segsh + WP;            // row j's errors, scan order, padded index
-  double* nrow = segsh + 2 * WP;       // row j+1 of bm (staged by warps 1..3)
-  unsigned int* sup = reinterpret_cast<unsigned int*>(segsh + 3 * WP);  // support bits, scan order
-  int* elist = reinterpret_cast<int*>(sup + (w + 31) / 32 + 1);          // [32][kSegEMax] lane emissions
+  const int WR = (w + 1) & ~1;
+  double* pre = segsh;                 // row j's pre-accumulated work, scan order
+  double* err = segsh + WR;            // row j's errors, scan order
+  double* nrow = segsh + 2 * WR;       // row j+1 of bm (staged by warps 1..3)
+  unsigned int* sup = reinterpret_cast<unsigned int*>(segsh + 3 * WR);  // support bits, scan order
+  int* elist = reinterpret_cast<int*>(sup + (w + 31) / 32 + 2);          // [32][kSegEMax] lane emissions
   __shared__ double s_wu[32];  // lane l's warm-up error at its segment's first pixel - 1
   __shared__ int s_ne[32];     // lane l's emission count (> kSegEMax: overflow)
   __shared__ int s_count;
@@ -586,25 +611,42 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
   }
   const double scale = budget / total;
   if (tid == 0) s_count = 0;
-  // segments: P lanes of S pixels (P = 1 for narrow rows)
-  const int P = w >= 2 * kSegWU ? min(32, w / 32) : 1;
-  const int S = (w + P - 1) / P;
-  auto seg_start = [&](int l) { return min(w, l * S); };
+  const SegLayout L = seg_layout(w);
+  // per-direction constants of every row but the last (fs_wsum with a row
+  // below; index 0: dir +1, 1: dir -1): carry coefficients and the diffusion
+  // quotients of the row-end sources
+  double cf[2], cm[2], e1[2][2], e5[2][2], e3[2][2];
+#pragma unroll
+  for (int d = 0; d < 2; ++d) {
+    const int dir = d == 0 ? 1 : -1, st = d == 0 ? 0 : w - 1;
+    cf[d] = fs_carry_coef(st, 0, w, 2, dir);
+    cm[d] = (w > 2) ? fs_carry_coef(st + dir, 0, w, 2, dir) : 0.0;
+    const double w_lo = fs_wsum(0, 0, w, 2, dir), w_hi = fs_wsum(w - 1, 0, w, 2, dir);
+    e1[d][0] = (1.0 / 16.0) / w_lo;
+    e1[d][1] = (1.0 / 16.0) / w_hi;
+    e5[d][0] = (5.0 / 16.0) / w_lo;
+    e5[d][1] = (5.0 / 16.0) / w_hi;
+    e3[d][0] = (3.0 / 16.0) / w_lo;
+    e3[d][1] = (3.0 / 16.0) / w_hi;
+  }
 
   // row 0: pre = work, no error inflow (observation.cpp:23-25)
-  for (int pos = tid; pos < w; pos += kSegT) pre[seg_pidx(pos)] = bm[pos] * scale;  // dir = +1
+  for (int pos = tid; pos < w; pos += kSegT) pre[pos] = bm[pos] * scale;  // dir = +1
   for (int wd = warp; wd <= w / 32; wd += kSegT / 32) {
     const int q = wd * 32 + lane;
     const unsigned int bits = __ballot_sync(0xffffffffu, q < w && bm[q] > 0.0);
     if (lane == 0) sup[wd] = bits;
   }
+  if (tid == 0) sup[w / 32 + 1] = 0u;
   __syncthreads();
 
   for (int j = 0; j < h; ++j) {
     const int dir = (j % 2 == 0) ? 1 : -1;
+    const int d = j % 2;
     const int start = dir == 1 ? 0 : w - 1;
-    const double c_first = fs_carry_coef(start, j, w, h, dir);
-    const double c_mid = (w > 2) ? fs_carry_coef(start + dir, j, w, h, dir) : 0.0;
+    const bool last = j == h - 1;
+    const double c_first = last ? fs_carry_coef(start, j, w, h, dir) : cf[d];
+    const double c_mid = last ? ((w > 2) ? fs_carry_coef(start + dir, j, w, h, dir) : 0.0) : cm[d];
     auto supp = [&](int q) { return (sup[q >> 5] >> (q & 31)) & 1u; };
     auto emit_out = [&](int q) {  // lane 0 only, in scan order
       const int c = s_count;
@@ -614,85 +656,81 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
       }
       s_count = c + 1;
     };
-    // the reference's exact sweep of scan positions [q0, q1) from `carry`,
-    // writing err and emitting; returns the carry after q1 - 1
-    auto exact = [&](int q0, int q1, double carry) {
-      for (int q = q0; q < q1; ++q) {
-        const double v = q == 0 ? pre[seg_pidx(0)] : pre[seg_pidx(q)] + carry;
+    // the reference's exact sweep of scan positions [0, w) (lane 0)
+    auto exact_row = [&]() {
+      double carry = 0.0;
+      for (int q = 0; q < w; ++q) {
+        const double v = q == 0 ? pre[0] : pre[q] + carry;
         double e = v;
         if (v >= 0.5 && supp(q)) {
           e = v - 1.0;
           emit_out(q);
         }
-        err[seg_pidx(q)] = e;
+        err[q] = e;
         carry = e * (q == 0 ? c_first : c_mid);
       }
-      return carry;
     };
-    const bool seq = (j == h - 1) || P == 1;
     if (warp == 0) {
-      if (seq) {
-        if (lane == 0) exact(0, w, 0.0);
+      if (last || L.P == 1) {
+        if (lane == 0) exact_row();
       } else {
-        // ---- every lane's segment at once (lanes >= P idle), 16-pixel
-        // groups: the group's pre values and support bits are loaded up
-        // front, the chain runs assuming no emission (one DADD and one DMUL
-        // per pixel) and is replayed exactly, by the lanes that need it,
-        // when any lane's group holds a supported v >= 0.5 ----
-        const int qs = seg_start(lane), qe = seg_start(lane + 1);
-        const bool act = lane < P;
-        const int q0 = lane == 0 ? 0 : max(1, qs - kSegWU);
+        const bool act = lane < L.P;
+        const int qs = L.start(lane), qe = L.start(lane + 1);
+        const int q0 = lane == 0 ? 0 : qs - kSegWU;  // F > kSegWU: warm-ups start inside the row
         double carry = 0.0;  // the guess (exact for lane 0: the row's first pixel has no carry in)
         int ne = 0;
         double wu = 0.0;
-        const int n_grp = (S + kSegWU + 15) / 16;
+        const int n_grp = (L.S + kSegWU + 15) / 16;
         for (int gi = 0; gi < n_grp; ++gi) {
           const int base = q0 + 16 * gi;
           const int valid = act ? max(0, min(16, qe - base)) : 0;
           if (!__any_sync(0xffffffffu, valid > 0)) break;
+          const double* pb = pre + (valid > 0 ? base : 0);
           double p[16], v[16];
 #pragma unroll
-          for (int k = 0; k < 16; ++k) p[k] = k < valid ? pre[seg_pidx(base + k)] : 0.0;
-          const int wd = base >> 5, sh = base & 31;
-          const unsigned long long sw2 = valid > 0 ? (static_cast<unsigned long long>(sup[wd]) |
-                                                      (static_cast<unsigned long long>(sup[wd + 1]) << 32))
-                                                   : 0ull;
-          const unsigned int sb = static_cast<unsigned int>(sw2 >> sh) & ((valid >= 16) ? 0xffffu : ((1u << valid) - 1u));
+          for (int k = 0; k < 16; ++k) p[k] = k < valid ? pb[k] : 0.0;
+          const unsigned long long sw2 = static_cast<unsigned long long>(sup[valid > 0 ? (base >> 5) : 0]) |
+                                         (static_cast<unsigned long long>(sup[valid > 0 ? (base >> 5) + 1 : 0]) << 32);
+          const unsigned int sb = valid > 0 ? (static_cast<unsigned int>(sw2 >> (base & 31)) &
+                                               (valid >= 16 ? 0xffffu : ((1u << valid) - 1u)))
+                                            : 0u;
+          const bool first = base == 0;  // lane 0's first group: pixel 0 has no carry in, coefficient c_first
           const double c0 = carry;
           double c = c0;
           int hm = 0;
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
-            const double vk = (base + k == 0) ? p[k] : p[k] + c;  // pixel 0: no carry in
+            const double vk = (k == 0 && first) ? p[0] : p[k] + c;
             v[k] = vk;
-            asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(vk), "d"(base + k == 0 ? c_first : c_mid));
+            asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(vk), "d"((k == 0 && first) ? c_first : c_mid));
             hm = max(hm, __double2hiint(vk) & -static_cast<int>((sb >> k) & 1u));
           }
-          const bool need = hm >= 0x3FE00000;
           unsigned int emask = 0;
+          const bool need = hm >= 0x3FE00000;
           if (__any_sync(0xffffffffu, need)) {
             if (need) {  // the exact sweep of this group
               c = c0;
 #pragma unroll
               for (int k = 0; k < 16; ++k) {
-                const double vk = (base + k == 0) ? p[k] : p[k] + c;
+                const double vk = (k == 0 && first) ? p[0] : p[k] + c;
                 const bool em = vk >= 0.5 && ((sb >> k) & 1u);
                 const double e = em ? vk - 1.0 : vk;
                 emask |= static_cast<unsigned int>(em) << k;
                 v[k] = e;
-                asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(e), "d"(base + k == 0 ? c_first : c_mid));
+                asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(e), "d"((k == 0 && first) ? c_first : c_mid));
               }
             }
           }
           carry = c;
-          // errors of the own segment, the warm-up's last error, emissions
+          // own-segment errors, the warm-up's last error, emissions
+          const int own = base - qs;  // pixels k >= -own are the lane's own
+          double* eb = err + (valid > 0 ? base : 0);
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
-            const int q = base + k;
-            if (k < valid && q >= qs) err[seg_pidx(q)] = v[k];
-            if (k < valid && q == qs - 1) wu = v[k];
+            if (k < valid && k >= -own) eb[k] = v[k];
+            if (k == -own - 1) wu = v[k];
           }
-          emask &= ~((qs > base) ? ((qs - base >= 32) ? 0xffffffffu : ((1u << (qs - base)) - 1u)) : 0u);
+          if (own < 0) emask &= (-own >= 16) ? 0u : ~((1u << (-own)) - 1u);
           while (emask) {
             const int k = __ffs(emask) - 1;
             emask &= emask - 1;
@@ -705,14 +743,12 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
           s_ne[lane] = ne;
         }
         __syncwarp();
-        // ---- verify: lane l is exact iff its warm-up's last error equals
-        // lane l-1's error at that pixel and lane l-1 is exact ----
+        // ---- verify in parallel: lanes below the first mismatch are exact ----
         const bool ovf = __any_sync(0xffffffffu, act && ne > kSegEMax);
-        const bool ok_l = !act || lane == 0 || (__double_as_longlong(err[seg_pidx(qs - 1)]) == __double_as_longlong(wu));
+        const bool ok_l = !act || lane == 0 || (__double_as_longlong(err[qs - 1]) == __double_as_longlong(wu));
         const unsigned int bad = __ballot_sync(0xffffffffu, !ok_l);
-        const int first_bad = bad ? __ffs(bad) - 1 : P;  // lanes below it are exact
+        const int first_bad = bad ? __ffs(bad) - 1 : L.P;
         const int c_base = s_count;
-        // emissions of the exact lanes, in scan order (a warp prefix sum)
         const int mine = (act && lane < first_bad && !ovf) ? ne : 0;
         int incl = mine;
 #pragma unroll
@@ -722,35 +758,37 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
         }
         const int tot = __shfl_sync(0xffffffffu, incl, 31);
         for (int k = 0; k < mine; ++k) {
-          const int c = c_base + incl - mine + k;
-          if (c < cap) {
-            cells[2 * c] = start + elist[lane * kSegEMax + k] * dir;
-            cells[2 * c + 1] = j;
+          const int cc = c_base + incl - mine + k;
+          if (cc < cap) {
+            cells[2 * cc] = start + elist[lane * kSegEMax + k] * dir;
+            cells[2 * cc + 1] = j;
           }
         }
         __syncwarp();
         if (lane == 0) {
           if (ovf) {
-            exact(0, w, 0.0);  // a lane's list overflowed: redo the row exactly
+            exact_row();  // a lane's list overflowed: redo the row exactly
           } else {
             s_count = c_base + tot;
-            // the remaining lanes in order (rare): fix up, then emit
-            for (int l = first_bad; l < P; ++l) {
-              const int ls = seg_start(l), le = seg_start(l + 1);
+            // from the first mismatching lane on, in order (rare): a lane is
+            // exact if its warm-up met the (final) error before it; else
+            // rerun it exactly until it meets its own errors
+            for (int l = first_bad; l < L.P; ++l) {
+              const int ls = L.start(l), le = L.start(l + 1);
               int from = ls;
-              const double et = err[seg_pidx(ls - 1)];
+              const double et = err[ls - 1];
               if (__double_as_longlong(et) != __double_as_longlong(s_wu[l])) {
-                double cr = et * (ls - 1 == 0 ? c_first : c_mid);
+                double cr = et * c_mid;  // ls - 1 >= kSegWU: an interior pixel
                 from = le;
                 for (int qq = ls; qq < le; ++qq) {
-                  const double vv = pre[seg_pidx(qq)] + cr;
+                  const double vv = pre[qq] + cr;
                   double e = vv;
                   if (vv >= 0.5 && supp(qq)) {
                     e = vv - 1.0;
                     emit_out(qq);
                   }
-                  const double spec = err[seg_pidx(qq)];
-                  err[seg_pidx(qq)] = e;
+                  const double spec = err[qq];
+                  err[qq] = e;
                   cr = e * c_mid;
                   if (__double_as_longlong(e) == __double_as_longlong(spec)) {
                     from = qq + 1;
@@ -773,24 +811,20 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
     }
     __syncthreads();
     if (j + 1 < h) {
-      // ---- row j+1's pre-accumulation (all warps), the helper's arithmetic ----
+      // ---- row j+1's pre-accumulation (all warps), the reference's
+      // arrival order: upstream, centre, downstream source of row j ----
       const int pd = dir, dn = -pd;
       const int start_n = dn == 1 ? 0 : w - 1;
-      const double w_lo = fs_wsum(0, j, w, h, pd), w_hi = fs_wsum(w - 1, j, w, h, pd);
-      const double e1[2] = {(1.0 / 16.0) / w_lo, (1.0 / 16.0) / w_hi};
-      const double e5[2] = {(5.0 / 16.0) / w_lo, (5.0 / 16.0) / w_hi};
-      const double e3[2] = {(3.0 / 16.0) / w_lo, (3.0 / 16.0) / w_hi};
-      auto coef = [&](int sc, double wt, const double* edge) {
-        return sc == 0 ? edge[0] : (sc == w - 1 ? edge[1] : wt);
-      };
-      // pre (row j) is dead once row j is swept: overwrite it in place
+      const double* E1 = e1[d];
+      const double* E5 = e5[d];
+      const double* E3 = e3[d];
       for (int pos = tid; pos < w; pos += kSegT) {
-        const int t = pd == 1 ? pos : w - 1 - pos;
+        const int t = pd == 1 ? pos : w - 1 - pos;  // column of row j at scan position pos
         double v = nrow[t] * scale;
-        if (pos >= 1) v += err[seg_pidx(pos - 1)] * coef(t - pd, 1.0 / 16.0, e1);
-        v += err[seg_pidx(pos)] * coef(t, 5.0 / 16.0, e5);
-        if (pos + 1 < w) v += err[seg_pidx(pos + 1)] * coef(t + pd, 3.0 / 16.0, e3);
-        pre[seg_pidx(w - 1 - pos)] = v;  // row j+1 scans the other way
+        if (pos >= 1) v += err[pos - 1] * ((t - pd == 0) ? E1[0] : (t - pd == w - 1 ? E1[1] : 1.0 / 16.0));
+        v += err[pos] * ((t == 0) ? E5[0] : (t == w - 1 ? E5[1] : 5.0 / 16.0));
+        if (pos + 1 < w) v += err[pos + 1] * ((t + pd == 0) ? E3[0] : (t + pd == w - 1 ? E3[1] : 3.0 / 16.0));
+        pre[w - 1 - pos] = v;  // row j+1 scans the other way (pre of row j is dead)
       }
       // support bits of row j+1 in its scan order
       for (int wd = warp; wd <= w / 32; wd += kSegT / 32) {
@@ -991,8 +1025,8 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
     }
   };
   const size_t smem = static_cast<size_t>(2) * w * sizeof(double);
-  const size_t smem_seg = (3 * static_cast<size_t>(seg_pidx(w) + 2)) * sizeof(double) +
-                          4 * static_cast<size_t>((w + 31) / 32 + 1) + 32 * kSegEMax * 4 + 64;
+  const size_t smem_seg = (3 * static_cast<size_t>((w + 1) & ~1)) * sizeof(double) +
+                          4 * static_cast<size_t>((w + 31) / 32 + 2) + 32 * kSegEMax * 4 + 64;
   if (smem_pipe <= 200 * 1024) {
     if (smem_pipe > 48 * 1024) attr(reinterpret_cast<const void*>(k_dither_pipe), smem_pipe);
     // the total first, as a parallel bit-exact scan (falls back to the
@@ -1001,7 +1035,7 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
     // the segment-parallel sweep where the plane is in the scan's domain;
     // the pipelined kernel then only runs if it could not (a device flag)
     int* d_done = d_sum_invalid + 1;
-    const bool seg = GL_FS_SEG && w >= 2 * kSegWU && smem_seg <= 200 * 1024;
+    const bool seg = GL_FS_SEG && w >= 4 * kSegWU && smem_seg <= 200 * 1024;
     if (seg) {
       if (smem_seg > 48 * 1024) attr(reinterpret_cast<const void*>(k_dither_seg), smem_seg);
       k_dither_seg<<<1, kSegT, smem_seg, ctx->stream>>>(bm, w, h, budget, d_cells, cap, d_n, d_mass, d_sum_invalid,
