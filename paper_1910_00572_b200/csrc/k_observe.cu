@@ -639,8 +639,17 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
   }
   if (tid == 0) sup[w / 32 + 1] = 0u;
   __syncthreads();
+#ifdef GL_EXPERIMENT_ENV
+  long long tk_spec = 0, tk_ver = 0, tk_pre = 0, tk_all = clock64(), tk0 = 0;
+#define SEG_TICK(acc) do { if (tid == 0) { const long long t_ = clock64(); acc += t_ - tk0; tk0 = t_; } } while (0)
+#else
+#define SEG_TICK(acc) do { } while (0)
+#endif
 
   for (int j = 0; j < h; ++j) {
+#ifdef GL_EXPERIMENT_ENV
+    if (tid == 0) tk0 = clock64();
+#endif
     const int dir = (j % 2 == 0) ? 1 : -1;
     const int d = j % 2;
     const int start = dir == 1 ? 0 : w - 1;
@@ -743,6 +752,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
           s_ne[lane] = ne;
         }
         __syncwarp();
+        SEG_TICK(tk_spec);
         // ---- verify in parallel: lanes below the first mismatch are exact ----
         const bool ovf = __any_sync(0xffffffffu, act && ne > kSegEMax);
         const bool ok_l = !act || lane == 0 || (__double_as_longlong(err[qs - 1]) == __double_as_longlong(wu));
@@ -804,6 +814,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
           }
         }
       }
+      SEG_TICK(tk_ver);
     } else if (j + 1 < h) {
       // warps 1..3 stage row j+1 of bm while warp 0 sweeps row j
       const double* brow = bm + static_cast<size_t>(j + 1) * w;
@@ -834,11 +845,19 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
       }
       __syncthreads();
     }
+    SEG_TICK(tk_pre);
   }
   if (tid == 0) {
     *n_out = s_count;
     *done = 1;
+#ifdef GL_EXPERIMENT_ENV
+    g_dither_clk[0] = tk_spec;
+    g_dither_clk[1] = tk_ver;
+    g_dither_clk[2] = tk_pre;
+    g_dither_clk[3] = clock64() - tk_all;
+#endif
   }
+#undef SEG_TICK
 }
 
 // dither_samples as a row decomposition that is bit-identical to the
@@ -1064,7 +1083,7 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
     long long clk[4];
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpyFromSymbol(clk, g_dither_clk, sizeof(clk));
-    fprintf(stderr, "dither clocks: total-sum %lld, sweep %lld (chain waited %lld at row starts, %lld at row ends) cycles (%d x %d)\n", clk[1], clk[2], clk[3], clk[0], w, h);
+    fprintf(stderr, "dither clocks [0..3]: %lld %lld %lld %lld (pipe: row-end wait, total, sweep, row-start wait; seg: spec, verify, pre, all) (%d x %d)\n", clk[0], clk[1], clk[2], clk[3], w, h);
   }
 #endif
 
