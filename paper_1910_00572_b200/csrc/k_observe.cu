@@ -235,7 +235,7 @@ __device__ __forceinline__ bool fs_spec_pipe(const double* __restrict__ pre, dou
   }
 }
 
-__device__ long long g_dither_clk[4];  // phase timestamps (debug read-out)
+__device__ long long g_dither_clk[8];  // phase timestamps (debug read-out)
 
 __global__ void __launch_bounds__(64) k_dither_pipe(
     const double* __restrict__ bm, int w, int h, int budget,
@@ -558,6 +558,7 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
 constexpr int kSegT = 128;     // threads (4 warps: warp 0 runs the chains; all warps the pre pass)
 constexpr int kSegWU = 64;     // warm-up pixels of lanes 1..31
 constexpr int kSegEMax = 8;    // emissions per lane per row before the row falls back
+static_assert(kSegWU % 16 == 0, "warm-ups are whole 16-pixel groups");
 
 struct SegLayout {
   int P, F, S;  // lanes in use, lane 0's length, segment stride (odd)
@@ -587,12 +588,13 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
                                                       const double* __restrict__ total_in,
                                                       const int* __restrict__ sum_invalid, int* __restrict__ done) {
   extern __shared__ double segsh[];
-  const int WR = (w + 1) & ~1;
-  double* pre = segsh;                 // row j's pre-accumulated work, scan order
-  double* err = segsh + WR;            // row j's errors, scan order
-  double* nrow = segsh + 2 * WR;       // row j+1 of bm (staged by warps 1..3)
-  unsigned int* sup = reinterpret_cast<unsigned int*>(segsh + 3 * WR);  // support bits, scan order
-  int* elist = reinterpret_cast<int*>(sup + (w + 31) / 32 + 2);          // [32][kSegEMax] lane emissions
+  const int WR = ((w + 1) & ~1) + 16, SW = (w + 31) / 32 + 2;  // +16: a lane's last group reads past w
+  // buf[j & 1]: row j's pre-accumulated work (scan order); buf[(j + 1) & 1]
+  // receives row j + 1 of bm, scan order, by cp.async while row j sweeps
+  double* buf0 = segsh;
+  double* err = segsh + 2 * WR;  // row j's errors, scan order
+  unsigned int* sup0 = reinterpret_cast<unsigned int*>(segsh + 3 * WR);  // [2][SW] support bits, scan order
+  int* elist = reinterpret_cast<int*>(sup0 + 2 * SW);                   // [32][kSegEMax] lane emissions
   __shared__ double s_wu[32];  // lane l's warm-up error at its segment's first pixel - 1
   __shared__ int s_ne[32];     // lane l's emission count (> kSegEMax: overflow)
   __shared__ int s_count;
@@ -613,34 +615,38 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
   if (tid == 0) s_count = 0;
   const SegLayout L = seg_layout(w);
   // per-direction constants of every row but the last (fs_wsum with a row
-  // below; index 0: dir +1, 1: dir -1): carry coefficients and the diffusion
-  // quotients of the row-end sources
-  double cf[2], cm[2], e1[2][2], e5[2][2], e3[2][2];
-#pragma unroll
-  for (int d = 0; d < 2; ++d) {
-    const int dir = d == 0 ? 1 : -1, st = d == 0 ? 0 : w - 1;
-    cf[d] = fs_carry_coef(st, 0, w, 2, dir);
-    cm[d] = (w > 2) ? fs_carry_coef(st + dir, 0, w, 2, dir) : 0.0;
+  // below; [0]: dir +1, [1]: dir -1): carry coefficients and the diffusion
+  // quotients of the row-end sources. Computed once into shared memory (in
+  // registers the compiler re-derives the divisions inside the row loop).
+  __shared__ double s_k[2][8];  // cf, cm, e1 lo/hi, e5 lo/hi, e3 lo/hi
+  if (tid < 2) {
+    const int dir = tid == 0 ? 1 : -1, st = tid == 0 ? 0 : w - 1;
     const double w_lo = fs_wsum(0, 0, w, 2, dir), w_hi = fs_wsum(w - 1, 0, w, 2, dir);
-    e1[d][0] = (1.0 / 16.0) / w_lo;
-    e1[d][1] = (1.0 / 16.0) / w_hi;
-    e5[d][0] = (5.0 / 16.0) / w_lo;
-    e5[d][1] = (5.0 / 16.0) / w_hi;
-    e3[d][0] = (3.0 / 16.0) / w_lo;
-    e3[d][1] = (3.0 / 16.0) / w_hi;
+    s_k[tid][0] = fs_carry_coef(st, 0, w, 2, dir);
+    s_k[tid][1] = (w > 2) ? fs_carry_coef(st + dir, 0, w, 2, dir) : 0.0;
+    s_k[tid][2] = (1.0 / 16.0) / w_lo;
+    s_k[tid][3] = (1.0 / 16.0) / w_hi;
+    s_k[tid][4] = (5.0 / 16.0) / w_lo;
+    s_k[tid][5] = (5.0 / 16.0) / w_hi;
+    s_k[tid][6] = (3.0 / 16.0) / w_lo;
+    s_k[tid][7] = (3.0 / 16.0) / w_hi;
   }
 
   // row 0: pre = work, no error inflow (observation.cpp:23-25)
-  for (int pos = tid; pos < w; pos += kSegT) pre[pos] = bm[pos] * scale;  // dir = +1
+  for (int pos = tid; pos < w; pos += kSegT) buf0[pos] = bm[pos] * scale;  // dir = +1
   for (int wd = warp; wd <= w / 32; wd += kSegT / 32) {
     const int q = wd * 32 + lane;
     const unsigned int bits = __ballot_sync(0xffffffffu, q < w && bm[q] > 0.0);
-    if (lane == 0) sup[wd] = bits;
+    if (lane == 0) sup0[wd] = bits;
   }
-  if (tid == 0) sup[w / 32 + 1] = 0u;
+  if (tid == 0) {
+    sup0[w / 32 + 1] = 0u;
+    sup0[SW + w / 32 + 1] = 0u;
+  }
   __syncthreads();
 #ifdef GL_EXPERIMENT_ENV
-  long long tk_spec = 0, tk_ver = 0, tk_pre = 0, tk_all = clock64(), tk0 = 0;
+  long long tk_spec = 0, tk_ver = 0, tk_pre = 0, tk_b1 = 0, tk_stage = 0, tk_all = clock64(), tk0 = 0;
+  long long tk_g0 = 0, tk_g1 = 0, tk_nrep = 0;
 #define SEG_TICK(acc) do { if (tid == 0) { const long long t_ = clock64(); acc += t_ - tk0; tk0 = t_; } } while (0)
 #else
 #define SEG_TICK(acc) do { } while (0)
@@ -648,14 +654,18 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
 
   for (int j = 0; j < h; ++j) {
 #ifdef GL_EXPERIMENT_ENV
-    if (tid == 0) tk0 = clock64();
+    if (tid == 0 || tid == 32) tk0 = clock64();
 #endif
     const int dir = (j % 2 == 0) ? 1 : -1;
     const int d = j % 2;
     const int start = dir == 1 ? 0 : w - 1;
     const bool last = j == h - 1;
-    const double c_first = last ? fs_carry_coef(start, j, w, h, dir) : cf[d];
-    const double c_mid = last ? ((w > 2) ? fs_carry_coef(start + dir, j, w, h, dir) : 0.0) : cm[d];
+    double* pre = buf0 + d * WR;            // row j's pre-accumulated work
+    double* nbuf = buf0 + (d ^ 1) * WR;     // row j + 1: bm (staged), then its pre
+    const unsigned int* sup = sup0 + d * SW;
+    unsigned int* nsup = sup0 + (d ^ 1) * SW;
+    const double c_first = last ? fs_carry_coef(start, j, w, h, dir) : s_k[d][0];
+    const double c_mid = last ? ((w > 2) ? fs_carry_coef(start + dir, j, w, h, dir) : 0.0) : s_k[d][1];
     auto supp = [&](int q) { return (sup[q >> 5] >> (q & 31)) & 1u; };
     auto emit_out = [&](int q) {  // lane 0 only, in scan order
       const int c = s_count;
@@ -691,13 +701,16 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
         double wu = 0.0;
         const int n_grp = (L.S + kSegWU + 15) / 16;
         for (int gi = 0; gi < n_grp; ++gi) {
+#ifdef GL_EXPERIMENT_ENV
+          long long tg0 = clock64();
+#endif
           const int base = q0 + 16 * gi;
           const int valid = act ? max(0, min(16, qe - base)) : 0;
           if (!__any_sync(0xffffffffu, valid > 0)) break;
           const double* pb = pre + (valid > 0 ? base : 0);
           double p[16], v[16];
 #pragma unroll
-          for (int k = 0; k < 16; ++k) p[k] = k < valid ? pb[k] : 0.0;
+          for (int k = 0; k < 16; ++k) p[k] = pb[k];  // past valid: padding / other lanes' values, masked below
           const unsigned long long sw2 = static_cast<unsigned long long>(sup[valid > 0 ? (base >> 5) : 0]) |
                                          (static_cast<unsigned long long>(sup[valid > 0 ? (base >> 5) + 1 : 0]) << 32);
           const unsigned int sb = valid > 0 ? (static_cast<unsigned int>(sw2 >> (base & 31)) &
@@ -706,17 +719,23 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
           const bool first = base == 0;  // lane 0's first group: pixel 0 has no carry in, coefficient c_first
           const double c0 = carry;
           double c = c0;
-          int hm = 0;
+          unsigned int big = 0;  // pixels with v >= 0.5 (high word test; NaN / inf included)
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
             const double vk = (k == 0 && first) ? p[0] : p[k] + c;
             v[k] = vk;
             asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(vk), "d"((k == 0 && first) ? c_first : c_mid));
-            hm = max(hm, __double2hiint(vk) & -static_cast<int>((sb >> k) & 1u));
+            big |= __double2hiint(vk) >= 0x3FE00000 ? (1u << k) : 0u;
           }
           unsigned int emask = 0;
-          const bool need = hm >= 0x3FE00000;
+          const bool need = (big & sb) != 0u;
+#ifdef GL_EXPERIMENT_ENV
+          if (tid == 0) { const long long t_ = clock64(); tk_g0 += t_ - tg0; tg0 = t_; }
+#endif
           if (__any_sync(0xffffffffu, need)) {
+#ifdef GL_EXPERIMENT_ENV
+            if (tid == 0) ++tk_nrep;
+#endif
             if (need) {  // the exact sweep of this group
               c = c0;
 #pragma unroll
@@ -731,15 +750,22 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
             }
           }
           carry = c;
-          // own-segment errors, the warm-up's last error, emissions
-          const int own = base - qs;  // pixels k >= -own are the lane's own
-          double* eb = err + (valid > 0 ? base : 0);
+          // own-segment errors, the warm-up's last error, emissions (groups
+          // never straddle a segment start: kSegWU is a multiple of 16)
+          const int own = base - qs;  // < 0: a warm-up group
+          if (own >= 0) {
+            double* eb = err + (valid > 0 ? base : 0);
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            if (k < valid && k >= -own) eb[k] = v[k];
-            if (k == -own - 1) wu = v[k];
+            for (int k = 0; k < 16; ++k) {
+              if (k < valid) eb[k] = v[k];
+            }
+          } else {
+            emask = 0u;
           }
-          if (own < 0) emask &= (-own >= 16) ? 0u : ~((1u << (-own)) - 1u);
+          if (own == -16) wu = v[15];
+#ifdef GL_EXPERIMENT_ENV
+          if (tid == 0) { const long long t_ = clock64(); tk_g1 += t_ - tg0; tg0 = t_; }
+#endif
           while (emask) {
             const int k = __ffs(emask) - 1;
             emask &= emask - 1;
@@ -816,37 +842,69 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
       }
       SEG_TICK(tk_ver);
     } else if (j + 1 < h) {
-      // warps 1..3 stage row j+1 of bm while warp 0 sweeps row j
+      // warps 1..3, while warp 0 sweeps row j: row j + 1 of bm into nbuf in
+      // its scan order (all loads in flight at once), then its support bits
       const double* brow = bm + static_cast<size_t>(j + 1) * w;
-      for (int t = tid - 32; t < w; t += kSegT - 32) nrow[t] = brow[t];
+      const bool rev = dir == 1;  // row j + 1 scans right to left
+      for (int t = tid - 32; t < w; t += kSegT - 32) {
+        const unsigned int dst = static_cast<unsigned int>(__cvta_generic_to_shared(nbuf + (rev ? w - 1 - t : t)));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(brow + t) : "memory");
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"r"(kSegT - 32) : "memory");
+      for (int wd = warp - 1; wd <= w / 32; wd += kSegT / 32 - 1) {
+        const int qn = wd * 32 + lane;
+        const unsigned int bits = __ballot_sync(0xffffffffu, qn < w && nbuf[qn] > 0.0);
+        if (lane == 0) nsup[wd] = bits;
+      }
+#ifdef GL_EXPERIMENT_ENV
+      if (tid == 32) tk_stage += clock64() - tk0;
+#endif
     }
     __syncthreads();
+    SEG_TICK(tk_b1);
     if (j + 1 < h) {
-      // ---- row j+1's pre-accumulation (all warps), the reference's
-      // arrival order: upstream, centre, downstream source of row j ----
-      const int pd = dir, dn = -pd;
-      const int start_n = dn == 1 ? 0 : w - 1;
-      const double* E1 = e1[d];
-      const double* E5 = e5[d];
-      const double* E3 = e3[d];
-      for (int pos = tid; pos < w; pos += kSegT) {
+      // ---- row j+1's pre-accumulation (all warps, in place over the staged
+      // bm row), the reference's arrival order: upstream, centre, downstream
+      // source of row j ----
+      const int pd = dir;
+      const double E1l = s_k[d][2], E1h = s_k[d][3], E5l = s_k[d][4], E5h = s_k[d][5], E3l = s_k[d][6],
+                   E3h = s_k[d][7];
+      if (tid < 4) {  // the row-end positions 0, 1, w-2, w-1: missing sources, row-end quotients
+        const int pos = tid < 2 ? tid : w - 4 + tid;
         const int t = pd == 1 ? pos : w - 1 - pos;  // column of row j at scan position pos
-        double v = nrow[t] * scale;
-        if (pos >= 1) v += err[pos - 1] * ((t - pd == 0) ? E1[0] : (t - pd == w - 1 ? E1[1] : 1.0 / 16.0));
-        v += err[pos] * ((t == 0) ? E5[0] : (t == w - 1 ? E5[1] : 5.0 / 16.0));
-        if (pos + 1 < w) v += err[pos + 1] * ((t + pd == 0) ? E3[0] : (t + pd == w - 1 ? E3[1] : 3.0 / 16.0));
-        pre[w - 1 - pos] = v;  // row j+1 scans the other way (pre of row j is dead)
+        double v = nbuf[w - 1 - pos] * scale;       // row j+1 scans the other way
+        if (pos >= 1) v += err[pos - 1] * ((t - pd == 0) ? E1l : (t - pd == w - 1 ? E1h : 1.0 / 16.0));
+        v += err[pos] * ((t == 0) ? E5l : (t == w - 1 ? E5h : 5.0 / 16.0));
+        if (pos + 1 < w) v += err[pos + 1] * ((t + pd == 0) ? E3l : (t + pd == w - 1 ? E3h : 3.0 / 16.0));
+        nbuf[w - 1 - pos] = v;
       }
-      // support bits of row j+1 in its scan order
-      for (int wd = warp; wd <= w / 32; wd += kSegT / 32) {
-        const int qn = wd * 32 + lane;
-        const unsigned int bits = __ballot_sync(0xffffffffu, qn < w && nrow[start_n + qn * dn] > 0.0);
-        if (lane == 0) sup[wd] = bits;
+      // interior positions [2, w-3]: all three sources, interior quotients;
+      // branch-free batches of 4 (clamped loads, guarded stores)
+      const int n_in = w - 4;
+      for (int i0 = tid; i0 < n_in; i0 += 4 * kSegT) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int pos = min(i0 + u * kSegT, n_in - 1) + 2;
+          double x = nbuf[w - 1 - pos] * scale;
+          x += err[pos - 1] * (1.0 / 16.0);
+          x += err[pos] * (5.0 / 16.0);
+          x += err[pos + 1] * (3.0 / 16.0);
+          v[u] = x;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (i0 + u * kSegT < n_in) nbuf[w - 3 - (i0 + u * kSegT)] = v[u];
+        }
       }
       __syncthreads();
     }
     SEG_TICK(tk_pre);
   }
+#ifdef GL_EXPERIMENT_ENV
+  if (tid == 32) g_dither_clk[5] = tk_stage;
+#endif
   if (tid == 0) {
     *n_out = s_count;
     *done = 1;
@@ -854,6 +912,9 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
     g_dither_clk[0] = tk_spec;
     g_dither_clk[1] = tk_ver;
     g_dither_clk[2] = tk_pre;
+    g_dither_clk[4] = tk_b1;
+    g_dither_clk[6] = tk_g0;
+    g_dither_clk[7] = tk_g1 + (tk_nrep << 40);
     g_dither_clk[3] = clock64() - tk_all;
 #endif
   }
@@ -1044,8 +1105,8 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
     }
   };
   const size_t smem = static_cast<size_t>(2) * w * sizeof(double);
-  const size_t smem_seg = (3 * static_cast<size_t>((w + 1) & ~1)) * sizeof(double) +
-                          4 * static_cast<size_t>((w + 31) / 32 + 2) + 32 * kSegEMax * 4 + 64;
+  const size_t smem_seg = (3 * static_cast<size_t>(((w + 1) & ~1) + 16)) * sizeof(double) +
+                          2 * 4 * static_cast<size_t>((w + 31) / 32 + 2) + 32 * kSegEMax * 4 + 64;
   if (smem_pipe <= 200 * 1024) {
     if (smem_pipe > 48 * 1024) attr(reinterpret_cast<const void*>(k_dither_pipe), smem_pipe);
     // the total first, as a parallel bit-exact scan (falls back to the
@@ -1080,10 +1141,10 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
   ctx->launches++;
 #ifdef GL_EXPERIMENT_ENV
   if (getenv("GL_DEBUG_DITHER")) {
-    long long clk[4];
+    long long clk[8];
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpyFromSymbol(clk, g_dither_clk, sizeof(clk));
-    fprintf(stderr, "dither clocks [0..3]: %lld %lld %lld %lld (pipe: row-end wait, total, sweep, row-start wait; seg: spec, verify, pre, all) (%d x %d)\n", clk[0], clk[1], clk[2], clk[3], w, h);
+    fprintf(stderr, "dither clocks: %lld %lld %lld %lld %lld %lld %lld %lld %lld (pipe: row-end wait, total, sweep, row-start wait; seg: spec, verify, pre, all, barrier-1 wait, staging, group chain, group rest, replays) (%d x %d)\n", clk[0], clk[1], clk[2], clk[3], clk[4], clk[5], clk[6], clk[7] & ((1LL << 40) - 1), clk[7] >> 40, w, h);
   }
 #endif
 
