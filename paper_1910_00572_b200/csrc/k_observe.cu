@@ -235,7 +235,7 @@ __device__ __forceinline__ bool fs_spec_pipe(const double* __restrict__ pre, dou
   }
 }
 
-__device__ long long g_dither_clk[8];  // phase timestamps (debug read-out)
+__device__ long long g_dither_clk[12];  // phase timestamps (debug read-out)
 
 __global__ void __launch_bounds__(64) k_dither_pipe(
     const double* __restrict__ bm, int w, int h, int budget,
@@ -557,7 +557,6 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
 #endif
 constexpr int kSegT = 128;     // threads (4 warps: warp 0 runs the chains; all warps the pre pass)
 constexpr int kSegWU = 64;     // warm-up pixels of lanes 1..31
-constexpr int kSegEMax = 8;    // emissions per lane per row before the row falls back
 static_assert(kSegWU % 16 == 0, "warm-ups are whole 16-pixel groups");
 
 struct SegLayout {
@@ -583,6 +582,55 @@ __host__ __device__ inline SegLayout seg_layout(int w) {
   return L;
 }
 
+// support bits of scan positions [base, base + valid) (0 <= valid <= 16), bit k = base + k
+__device__ __forceinline__ unsigned int seg_sup_bits(const unsigned int* sup, int base, int valid) {
+  // branch-free: lanes without pixels read word 0 under an empty mask
+  const int b = valid > 0 ? base : 0;
+  const unsigned long long sw2 = static_cast<unsigned long long>(sup[b >> 5]) |
+                                 (static_cast<unsigned long long>(sup[(b >> 5) + 1]) << 32);
+  return static_cast<unsigned int>(sw2 >> (b & 31)) & (valid >= 16 ? 0xffffu : ((1u << valid) - 1u));
+}
+
+// One 16-pixel group of a lane's chain from carry c0 (warp-collective: every
+// lane calls it). The values are loaded up front (past the lane's valid
+// pixels: padding or other lanes' values, masked by sb); the chain runs
+// assuming no emission (one DADD and one DMUL per pixel) and is replayed
+// exactly by the lanes whose group holds a supported v >= 0.5. v <- errors,
+// emask <- emissions, returns the carry out. first: the row's pixel 0 (no
+// carry in, coefficient c_first).
+__device__ __forceinline__ double seg_group(const double* pb, unsigned int sb, bool first, double c0, double c_first,
+                                            double c_mid, double (&v)[16], unsigned int& emask) {
+  double p[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) p[k] = pb[k];
+  double c = c0;
+  unsigned int big = 0;  // pixels with v >= 0.5 (high word test; NaN / inf included)
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const double vk = (k == 0 && first) ? p[0] : p[k] + c;
+    v[k] = vk;
+    asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(vk), "d"((k == 0 && first) ? c_first : c_mid));
+    big |= __double2hiint(vk) >= 0x3FE00000 ? (1u << k) : 0u;
+  }
+  emask = 0u;
+  const bool need = (big & sb) != 0u;
+  if (__any_sync(0xffffffffu, need)) {
+    if (need) {
+      c = c0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const double vk = (k == 0 && first) ? p[0] : p[k] + c;
+        const bool em = vk >= 0.5 && ((sb >> k) & 1u);
+        const double e = em ? vk - 1.0 : vk;
+        emask |= static_cast<unsigned int>(em) << k;
+        v[k] = e;
+        asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(e), "d"((k == 0 && first) ? c_first : c_mid));
+      }
+    }
+  }
+  return c;
+}
+
 __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__ bm, int w, int h, int budget,
                                                       int* __restrict__ cells, int cap, int* __restrict__ n_out,
                                                       const double* __restrict__ total_in,
@@ -594,9 +642,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
   double* buf0 = segsh;
   double* err = segsh + 2 * WR;  // row j's errors, scan order
   unsigned int* sup0 = reinterpret_cast<unsigned int*>(segsh + 3 * WR);  // [2][SW] support bits, scan order
-  int* elist = reinterpret_cast<int*>(sup0 + 2 * SW);                   // [32][kSegEMax] lane emissions
-  __shared__ double s_wu[32];  // lane l's warm-up error at its segment's first pixel - 1
-  __shared__ int s_ne[32];     // lane l's emission count (> kSegEMax: overflow)
+  unsigned int* ebits = sup0 + 2 * SW;  // [SW] row j's emission bits, scan order
   __shared__ int s_count;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (*sum_invalid) {  // negative / non-finite plane: k_dither_pipe's sequential total takes it
@@ -643,10 +689,12 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
     sup0[w / 32 + 1] = 0u;
     sup0[SW + w / 32 + 1] = 0u;
   }
+  for (int i = tid; i < SW; i += kSegT) ebits[i] = 0u;
   __syncthreads();
 #ifdef GL_EXPERIMENT_ENV
   long long tk_spec = 0, tk_ver = 0, tk_pre = 0, tk_b1 = 0, tk_stage = 0, tk_all = clock64(), tk0 = 0;
-  long long tk_g0 = 0, tk_g1 = 0, tk_nrep = 0;
+  long long tk_g0 = 0, tk_g1 = 0, tk_nrep = 0, n_ovf = 0, n_fix = 0, n_fixpx = 0, n_exact = 0;
+  (void)n_ovf;
 #define SEG_TICK(acc) do { if (tid == 0) { const long long t_ = clock64(); acc += t_ - tk0; tk0 = t_; } } while (0)
 #else
 #define SEG_TICK(acc) do { } while (0)
@@ -691,13 +739,15 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
     };
     if (warp == 0) {
       if (last || L.P == 1) {
+#ifdef GL_EXPERIMENT_ENV
+        ++n_exact;
+#endif
         if (lane == 0) exact_row();
       } else {
         const bool act = lane < L.P;
         const int qs = L.start(lane), qe = L.start(lane + 1);
         const int q0 = lane == 0 ? 0 : qs - kSegWU;  // F > kSegWU: warm-ups start inside the row
         double carry = 0.0;  // the guess (exact for lane 0: the row's first pixel has no carry in)
-        int ne = 0;
         double wu = 0.0;
         const int n_grp = (L.S + kSegWU + 15) / 16;
         for (int gi = 0; gi < n_grp; ++gi) {
@@ -707,51 +757,12 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
           const int base = q0 + 16 * gi;
           const int valid = act ? max(0, min(16, qe - base)) : 0;
           if (!__any_sync(0xffffffffu, valid > 0)) break;
-          const double* pb = pre + (valid > 0 ? base : 0);
-          double p[16], v[16];
-#pragma unroll
-          for (int k = 0; k < 16; ++k) p[k] = pb[k];  // past valid: padding / other lanes' values, masked below
-          const unsigned long long sw2 = static_cast<unsigned long long>(sup[valid > 0 ? (base >> 5) : 0]) |
-                                         (static_cast<unsigned long long>(sup[valid > 0 ? (base >> 5) + 1 : 0]) << 32);
-          const unsigned int sb = valid > 0 ? (static_cast<unsigned int>(sw2 >> (base & 31)) &
-                                               (valid >= 16 ? 0xffffu : ((1u << valid) - 1u)))
-                                            : 0u;
-          const bool first = base == 0;  // lane 0's first group: pixel 0 has no carry in, coefficient c_first
-          const double c0 = carry;
-          double c = c0;
-          unsigned int big = 0;  // pixels with v >= 0.5 (high word test; NaN / inf included)
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const double vk = (k == 0 && first) ? p[0] : p[k] + c;
-            v[k] = vk;
-            asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(vk), "d"((k == 0 && first) ? c_first : c_mid));
-            big |= __double2hiint(vk) >= 0x3FE00000 ? (1u << k) : 0u;
-          }
-          unsigned int emask = 0;
-          const bool need = (big & sb) != 0u;
-#ifdef GL_EXPERIMENT_ENV
-          if (tid == 0) { const long long t_ = clock64(); tk_g0 += t_ - tg0; tg0 = t_; }
-#endif
-          if (__any_sync(0xffffffffu, need)) {
-#ifdef GL_EXPERIMENT_ENV
-            if (tid == 0) ++tk_nrep;
-#endif
-            if (need) {  // the exact sweep of this group
-              c = c0;
-#pragma unroll
-              for (int k = 0; k < 16; ++k) {
-                const double vk = (k == 0 && first) ? p[0] : p[k] + c;
-                const bool em = vk >= 0.5 && ((sb >> k) & 1u);
-                const double e = em ? vk - 1.0 : vk;
-                emask |= static_cast<unsigned int>(em) << k;
-                v[k] = e;
-                asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(e), "d"((k == 0 && first) ? c_first : c_mid));
-              }
-            }
-          }
-          carry = c;
-          // own-segment errors, the warm-up's last error, emissions (groups
-          // never straddle a segment start: kSegWU is a multiple of 16)
+          double v[16];
+          unsigned int emask;
+          carry = seg_group(pre + (valid > 0 ? base : 0), seg_sup_bits(sup, base, valid), base == 0, carry, c_first,
+                            c_mid, v, emask);
+          // own-segment errors and emission bits, the warm-up's last error
+          // (groups never straddle a segment start: kSegWU is a multiple of 16)
           const int own = base - qs;  // < 0: a warm-up group
           if (own >= 0) {
             double* eb = err + (valid > 0 ? base : 0);
@@ -759,86 +770,117 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
             for (int k = 0; k < 16; ++k) {
               if (k < valid) eb[k] = v[k];
             }
-          } else {
-            emask = 0u;
+            if (emask) {  // neighbouring lanes share boundary words
+              const int sh = base & 31;
+              atomicOr(&ebits[base >> 5], emask << sh);
+              if (sh > 16) atomicOr(&ebits[(base >> 5) + 1], emask >> (32 - sh));
+            }
           }
           if (own == -16) wu = v[15];
 #ifdef GL_EXPERIMENT_ENV
           if (tid == 0) { const long long t_ = clock64(); tk_g1 += t_ - tg0; tg0 = t_; }
 #endif
-          while (emask) {
-            const int k = __ffs(emask) - 1;
-            emask &= emask - 1;
-            if (ne < kSegEMax) elist[lane * kSegEMax + ne] = base + k;
-            ++ne;
-          }
-        }
-        if (act) {
-          s_wu[lane] = wu;
-          s_ne[lane] = ne;
         }
         __syncwarp();
         SEG_TICK(tk_spec);
-        // ---- verify in parallel: lanes below the first mismatch are exact ----
-        const bool ovf = __any_sync(0xffffffffu, act && ne > kSegEMax);
-        const bool ok_l = !act || lane == 0 || (__double_as_longlong(err[qs - 1]) == __double_as_longlong(wu));
-        const unsigned int bad = __ballot_sync(0xffffffffu, !ok_l);
-        const int first_bad = bad ? __ffs(bad) - 1 : L.P;
-        const int c_base = s_count;
-        const int mine = (act && lane < first_bad && !ovf) ? ne : 0;
-        int incl = mine;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const int tot = __shfl_sync(0xffffffffu, incl, 31);
-        for (int k = 0; k < mine; ++k) {
-          const int cc = c_base + incl - mine + k;
-          if (cc < cap) {
-            cells[2 * cc] = start + elist[lane * kSegEMax + k] * dir;
-            cells[2 * cc + 1] = j;
+        // ---- verification, all lanes at once. Lane l >= 1 is exact if its
+        // warm-up's last error equals lane l-1's error before its segment;
+        // else it reruns from that true carry until its value meets its own
+        // stored chain (same state, same future) and takes the rerun's errors
+        // and emissions up to there. This assumes lane l-1's segment end is
+        // final; a lane whose rerun reached its segment end without meeting
+        // changed that end, and its successor reruns in another round. ----
+        bool todo = act && lane > 0, recheck = true;
+        while (__any_sync(0xffffffffu, todo)) {
+          bool run = false;
+          double cr = 0.0;
+          if (todo) {
+            const double et = err[qs - 1];
+            run = !recheck || __double_as_longlong(et) != __double_as_longlong(wu);
+            cr = et * c_mid;  // qs - 1 >= kSegWU: an interior pixel
           }
-        }
-        __syncwarp();
-        if (lane == 0) {
-          if (ovf) {
-            exact_row();  // a lane's list overflowed: redo the row exactly
-          } else {
-            s_count = c_base + tot;
-            // from the first mismatching lane on, in order (rare): a lane is
-            // exact if its warm-up met the (final) error before it; else
-            // rerun it exactly until it meets its own errors
-            for (int l = first_bad; l < L.P; ++l) {
-              const int ls = L.start(l), le = L.start(l + 1);
-              int from = ls;
-              const double et = err[ls - 1];
-              if (__double_as_longlong(et) != __double_as_longlong(s_wu[l])) {
-                double cr = et * c_mid;  // ls - 1 >= kSegWU: an interior pixel
-                from = le;
-                for (int qq = ls; qq < le; ++qq) {
-                  const double vv = pre[qq] + cr;
-                  double e = vv;
-                  if (vv >= 0.5 && supp(qq)) {
-                    e = vv - 1.0;
-                    emit_out(qq);
-                  }
-                  const double spec = err[qq];
-                  err[qq] = e;
-                  cr = e * c_mid;
-                  if (__double_as_longlong(e) == __double_as_longlong(spec)) {
-                    from = qq + 1;
-                    break;
-                  }
-                }
+          bool changed = run;  // cleared when the rerun meets the stored chain
+#ifdef GL_EXPERIMENT_ENV
+          if (run) ++n_fix;
+#endif
+          int base = qs;
+          while (__any_sync(0xffffffffu, run)) {
+            const int valid = run ? max(0, min(16, qe - base)) : 0;
+            double v[16];
+            unsigned int emask;
+            const double cn = seg_group(pre + (valid > 0 ? base : 0), seg_sup_bits(sup, base, valid), false, cr,
+                                        c_first, c_mid, v, emask);
+            if (valid > 0) {
+              // the first pixel where the rerun equals the stored chain: the
+              // same state from there on. Its emission is the rerun's (equal
+              // errors do not imply equal decisions at that pixel).
+              unsigned int meet = 0u;
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                if (k < valid && __double_as_longlong(v[k]) == __double_as_longlong(err[base + k])) meet |= 1u << k;
               }
-              for (int k = 0; k < s_ne[l]; ++k) {
-                const int qk = elist[l * kSegEMax + k];
-                if (qk >= from) emit_out(qk);
+              const int m = meet ? __ffs(meet) - 1 : valid - 1;  // last pixel taken from the rerun
+#ifdef GL_EXPERIMENT_ENV
+              n_fixpx += m + 1;
+#endif
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                if (k <= m) err[base + k] = v[k];
+              }
+              const unsigned int keep = m >= 15 ? 0xffffu : ((2u << m) - 1u);
+              const int sh = base & 31;
+              const unsigned long long ow = static_cast<unsigned long long>(ebits[base >> 5]) |
+                                            (static_cast<unsigned long long>(ebits[(base >> 5) + 1]) << 32);
+              const unsigned int diff = (static_cast<unsigned int>(ow >> sh) ^ emask) & keep;
+              if (diff) {  // only this lane's bits change; neighbours share boundary words
+                atomicXor(&ebits[base >> 5], diff << sh);
+                if (sh > 16) atomicXor(&ebits[(base >> 5) + 1], diff >> (32 - sh));
+              }
+              if (meet) {
+                changed = false;
+                run = false;
+              } else {
+                cr = cn;
+                base += 16;
+                if (base >= qe) run = false;  // the segment end changed
               }
             }
           }
+          recheck = false;  // later rounds rerun unconditionally
+          const unsigned int ch = __ballot_sync(0xffffffffu, changed);
+          __syncwarp();
+          todo = act && lane > 0 && ((ch >> (lane - 1)) & 1u);
         }
+        __syncwarp();
+        // ---- the row's emissions in scan order: a warp scan over the
+        // emission words (cleared for the next row) ----
+        const int nw = (w + 31) >> 5;
+        int c_base = s_count;
+        for (int w0 = 0; w0 < nw; w0 += 32) {
+          const int wd = w0 + lane;
+          unsigned int bits = wd < nw ? ebits[wd] : 0u;
+          if (wd < nw) ebits[wd] = 0u;
+          const int cnt = __popc(bits);
+          int incl = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          int cc = c_base + incl - cnt;
+          while (bits) {
+            const int q = wd * 32 + __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (cc < cap) {
+              cells[2 * cc] = start + q * dir;
+              cells[2 * cc + 1] = j;
+            }
+            ++cc;
+          }
+          c_base += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        __syncwarp();
+        if (lane == 0) s_count = c_base;
       }
       SEG_TICK(tk_ver);
     } else if (j + 1 < h) {
@@ -904,6 +946,12 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
   }
 #ifdef GL_EXPERIMENT_ENV
   if (tid == 32) g_dither_clk[5] = tk_stage;
+  if (warp == 0) {
+    for (int o = 16; o > 0; o >>= 1) {
+      n_fix += __shfl_down_sync(0xffffffffu, n_fix, o);
+      n_fixpx += __shfl_down_sync(0xffffffffu, n_fixpx, o);
+    }
+  }
 #endif
   if (tid == 0) {
     *n_out = s_count;
@@ -915,6 +963,10 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
     g_dither_clk[4] = tk_b1;
     g_dither_clk[6] = tk_g0;
     g_dither_clk[7] = tk_g1 + (tk_nrep << 40);
+    g_dither_clk[8] = n_ovf;
+    g_dither_clk[9] = n_fix;
+    g_dither_clk[10] = n_fixpx;
+    g_dither_clk[11] = n_exact;
     g_dither_clk[3] = clock64() - tk_all;
 #endif
   }
@@ -1106,7 +1158,7 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
   };
   const size_t smem = static_cast<size_t>(2) * w * sizeof(double);
   const size_t smem_seg = (3 * static_cast<size_t>(((w + 1) & ~1) + 16)) * sizeof(double) +
-                          2 * 4 * static_cast<size_t>((w + 31) / 32 + 2) + 32 * kSegEMax * 4 + 64;
+                          3 * 4 * static_cast<size_t>((w + 31) / 32 + 2) + 64;
   if (smem_pipe <= 200 * 1024) {
     if (smem_pipe > 48 * 1024) attr(reinterpret_cast<const void*>(k_dither_pipe), smem_pipe);
     // the total first, as a parallel bit-exact scan (falls back to the
@@ -1141,10 +1193,11 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
   ctx->launches++;
 #ifdef GL_EXPERIMENT_ENV
   if (getenv("GL_DEBUG_DITHER")) {
-    long long clk[8];
+    long long clk[12];
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpyFromSymbol(clk, g_dither_clk, sizeof(clk));
     fprintf(stderr, "dither clocks: %lld %lld %lld %lld %lld %lld %lld %lld %lld (pipe: row-end wait, total, sweep, row-start wait; seg: spec, verify, pre, all, barrier-1 wait, staging, group chain, group rest, replays) (%d x %d)\n", clk[0], clk[1], clk[2], clk[3], clk[4], clk[5], clk[6], clk[7] & ((1LL << 40) - 1), clk[7] >> 40, w, h);
+    fprintf(stderr, "dither events: fixed lanes %lld, fixed pixels %lld, exact rows %lld\n", clk[9], clk[10], clk[11]);
   }
 #endif
 
