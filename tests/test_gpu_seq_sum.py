@@ -37,6 +37,11 @@ CASES = {
     "single_and_empty_prefix": lambda r: np.concatenate([np.zeros(70_000), [3.0], np.zeros(10), [0.25]]),
     "minus_zero": lambda r: np.concatenate([[-0.0, 0.0, -0.0], r.random(5000), [-0.0] * 7, r.random(9000)]),
     "all_zero": lambda r: np.zeros(12345),
+    "long_zero_prefix": lambda r: np.concatenate([np.where(r.random(9_000_000) < 1e-6, -0.0, 0.0), [2.0 ** -1070],
+                                                  np.zeros(100_000), r.random(50_000) ** 20]),
+    "many_crossings_per_chunk": lambda r: 2.0 ** np.linspace(-1070, 10, 400_000) * r.random(400_000),
+    "crossings_and_ties": lambda r: np.concatenate([2.0 ** np.linspace(-60, 0, 30_000) * r.random(30_000),
+                                                    r.integers(0, 4, 30_000) * 2.0 ** -54]),
     "plane_1024sq": lambda r: np.where(r.random(1 << 20) < 0.16, 0.0, r.random(1 << 20) ** 3),
 }
 

@@ -1,7 +1,12 @@
 #!/bin/bash
-for r in 1 2; do
-for v in base hm; do
-  echo "== $v"
-  GRIDLOC_B200_LIB=$PWD/build/variants/$v/libgridloc_b200.so timeout 300 python tools/ab_dither.py 1024 40 2>&1 | tail -1
-  GRIDLOC_B200_LIB=$PWD/build/variants/$v/libgridloc_b200.so timeout 300 python tools/time_c3_phases.py 2>&1 | grep "sync=True" | cut -c1-140
-done; done
+timeout 900 python -m pytest -q -x tests/test_gpu_seq_sum.py tests/test_gpu_dither_seg.py tests/test_gpu_readouts.py 2>&1 | tail -3
+GRIDLOC_B200_LIB=$PWD/build/variants/dbg/libgridloc_b200.so GL_DEBUG_SEQSUM=1 timeout 300 python tools/obs_cycle.py 160 2>&1 | tail -2
+timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/obs_cycle_launches3.csv python tools/obs_cycle.py 160 > gpurun_out/obs_cycle.log 2>&1
+python - <<'PY'
+import csv
+rows=[r for r in csv.reader(open('gpurun_out/obs_cycle_launches3.csv')) if len(r)>10]
+h=rows[0]; ci={k:i for i,k in enumerate(h)}
+for r in rows[1:]:
+    if r[ci['Metric Name']]=='gpu__time_duration.sum':
+        print(r[ci['Metric Value']], r[ci['Metric Unit']], r[ci['Kernel Name']][:80])
+PY
