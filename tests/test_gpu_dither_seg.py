@@ -1,11 +1,13 @@
 """The segment-parallel Floyd-Steinberg sweep (k_dither_seg: row segments run
 by the lanes of one warp from a guessed carry, verified bitwise against the
-previous segment's true error and fixed up until the chains meet) against
-the oracle's sequential dither_samples (observation.cpp:11-71): sample lists
-in emission order and source masses bit-identical on planes chosen to stress
-every path — sparse and dense emissions (lane lists overflowing into the
-exact row redo), segments that need a fix-up, widths from the narrowest that
-segments to the shared-memory limit, long thin and tall planes."""
+previous segment's true error and rerun until the chains meet) against the
+oracle's sequential dither_samples (observation.cpp:11-71): sample lists in
+emission order and source masses bit-identical on planes chosen to stress
+every path — sparse and dense emissions (many per segment), segments that
+need a rerun, reruns that run through their segment (isolated spikes whose
+error tails cross exact-zero runs, steep exponential tails: several
+verification rounds), widths from the narrowest that segments to the
+shared-memory limit, long thin and tall planes."""
 import numpy as np
 import pytest
 
@@ -18,7 +20,7 @@ def _plane(kind, w, h, seed):
     rng = np.random.default_rng(seed)
     if kind == "sparse":       # a converged belief: few emissions per row
         bm = rng.random((h, w)) ** 12
-    elif kind == "dense":      # many emissions per row (lane lists overflow)
+    elif kind == "dense":      # many emissions per row and segment
         bm = rng.random((h, w))
     elif kind == "blobs":      # localized mass, most of the plane zero
         bm = np.zeros((h, w))
@@ -30,12 +32,21 @@ def _plane(kind, w, h, seed):
         bm = rng.random((h, w)) ** 4
         bm[:, ::37] = 0.0
         bm[::23, :] = 0.0
+    elif kind == "spikes":     # isolated masses in exact zeros: long decaying error tails
+        bm = np.zeros((h, w))
+        n = max(1, w // 300)
+        for j in range(h):
+            bm[j, rng.integers(0, w, n)] = rng.uniform(0.5, 3.0, n)
+    elif kind == "tails":      # steep exponential profiles over many decades
+        xx = np.arange(w)[None, :]
+        cx = rng.integers(0, w, (h, 1))
+        bm = np.exp(-np.abs(xx - cx) * rng.uniform(0.5, 3.0, (h, 1))) * rng.uniform(0.1, 1.0, (h, 1))
     else:
         raise KeyError(kind)
     return bm
 
 
-@pytest.mark.parametrize("kind", ["sparse", "dense", "blobs", "walls"])
+@pytest.mark.parametrize("kind", ["sparse", "dense", "blobs", "walls", "spikes", "tails"])
 @pytest.mark.parametrize("w,h,budget", [(128, 40, 64), (200, 64, 512), (1000, 30, 512), (1024, 64, 4096),
                                         (2048, 16, 512), (4096, 6, 20000), (333, 333, 100000)])
 def test_segment_sweep_bit_exact(ctx, port, kind, w, h, budget):
