@@ -1,12 +1,4 @@
 #!/bin/bash
-timeout 900 python -m pytest -q -x tests/test_gpu_seq_sum.py tests/test_gpu_dither_seg.py tests/test_gpu_readouts.py 2>&1 | tail -3
-GRIDLOC_B200_LIB=$PWD/build/variants/dbg/libgridloc_b200.so GL_DEBUG_SEQSUM=1 timeout 300 python tools/obs_cycle.py 160 2>&1 | tail -2
-timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/obs_cycle_launches3.csv python tools/obs_cycle.py 160 > gpurun_out/obs_cycle.log 2>&1
-python - <<'PY'
-import csv
-rows=[r for r in csv.reader(open('gpurun_out/obs_cycle_launches3.csv')) if len(r)>10]
-h=rows[0]; ci={k:i for i,k in enumerate(h)}
-for r in rows[1:]:
-    if r[ci['Metric Name']]=='gpu__time_duration.sum':
-        print(r[ci['Metric Value']], r[ci['Metric Unit']], r[ci['Kernel Name']][:80])
-PY
+timeout 600 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:k_dither_seg -c 1 -o gpurun_out/dither_seg -f python tools/obs_cycle.py 160 > gpurun_out/dither_seg.log 2>&1
+tail -1 gpurun_out/dither_seg.log
+timeout 600 python bench.py --config c3 --steps 400 --warmup 20 > gpurun_out/bench_c3.log 2>&1; tail -1 gpurun_out/bench_c3.log | cut -c1-200

@@ -4,6 +4,7 @@ profiles/: key metrics (JSON + markdown) and the per-launch DRAM traffic
 that bench.py reports as roofline.traffic.
 
   python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r01_fused c2
+  python tools/ncu_summary.py gpurun_out/seg.ncu-rep profiles/r02_ncu_dither_seg -   (other kernels: no traffic entry)
 """
 import csv
 import io
@@ -52,7 +53,8 @@ def main():
     rep, prefix, cfg = sys.argv[1], sys.argv[2], (sys.argv[3] if len(sys.argv) > 3 else "c2")
     d, stalls = raw(rep)
     kern = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
-    name = next((r[4] for r in csv.reader(io.StringIO(kern)) if len(r) > 4 and "k_fused" in r[4]), "")
+    names = [r[4] for r in csv.reader(io.StringIO(kern)) if len(r) > 4 and r[0] != "ID"]
+    name = next((n for n in names if "k_fused" in n), names[0] if names else "")
     summary = {k: {"value": d[k][0], "unit": d[k][1]} for k in KEYS if k in d}
     traffic = to_bytes(*d["dram__bytes_read.sum"]) + to_bytes(*d["dram__bytes_write.sum"])
     summary["traffic_bytes_per_launch"] = traffic
@@ -68,6 +70,9 @@ def main():
         f.write(f"| traffic (read+write) per launch | {traffic:.0f} | byte |\n\n## stall reasons (warps per issue)\n\n")
         for k, v in summary["stalls_per_issue"].items():
             f.write(f"- {k}: {v:.3f}\n")
+    if cfg == "-":
+        print(json.dumps({"traffic": traffic, "time": d["gpu__time_duration.sum"]}))
+        return
     tpath = os.path.join(os.path.dirname(prefix) or ".", "ncu_traffic.json")
     t = {}
     if os.path.exists(tpath):
