@@ -1055,10 +1055,16 @@ static ArgmaxExact argmax_exact(gl_context* ctx, gl_tensor* t, double s0) {
   auto al = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
   const size_t sb = al(glb::argmax_scratch_bytes(n));
   char* d = static_cast<char*>(ensure_misc(ctx, sb + 256 + glb::seq_sum_scratch_bytes(n)));
-  glb::launch_argmax(ctx, interior(t), n, d, sb, d + sb);  // {v, idx, pairwise sum} at d + sb
   double* d_total = reinterpret_cast<double*>(d + sb + 64);
   int* d_inv = reinterpret_cast<int*>(d + sb + 72);
-  glb::launch_seq_sum_big(ctx, interior(t), n, d_total, d_inv, d + sb + 256, s0);
+  if (glb::seq_sum_fuses_argmax(n)) {
+    // one read of the tensor: the exact total's chunk pass also takes the
+    // argmax candidates ({v, idx, -} at d + sb)
+    glb::launch_seq_sum_big(ctx, interior(t), n, d_total, d_inv, d + sb + 256, s0, d + sb);
+  } else {
+    glb::launch_argmax(ctx, interior(t), n, d, sb, d + sb);  // {v, idx, pairwise sum} at d + sb
+    glb::launch_seq_sum_big(ctx, interior(t), n, d_total, d_inv, d + sb + 256, s0);
+  }
   glb::launch_seq_sum_chain(ctx, interior(t), n, d_total, d_inv, s0);  // runs only if the scan flagged
   struct {
     double v;

@@ -333,8 +333,12 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
 // s0: the running sum the chain enters with (0.0; a previous shard's total).
 void launch_seq_sum(gl_context* ctx, const double* x, size_t n, double* d_total, int* d_invalid, double s0 = 0.0);
 size_t seq_sum_scratch_bytes(size_t n);
+// d_argmax (optional, when seq_sum_fuses_argmax(n)): the chunk pass also
+// writes argmax_state's candidate {value, flat index, unused} (the first
+// maximum, values compared with a strict > from -1.0: k_argmax_partial's rule).
 void launch_seq_sum_big(gl_context* ctx, const double* x, size_t n, double* d_total, int* d_invalid,
-                        void* scratch, double s0 = 0.0);
+                        void* scratch, double s0 = 0.0, void* d_argmax = nullptr);
+bool seq_sum_fuses_argmax(size_t n);
 // the literal chain on one thread (inputs outside the scan's domain); runs
 // only when *when != 0 (when == null: always)
 void launch_seq_sum_chain(gl_context* ctx, const double* x, size_t n, double* d_total, const int* when,

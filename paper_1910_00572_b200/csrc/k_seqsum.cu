@@ -225,8 +225,8 @@ __device__ __forceinline__ SegMap block_seg_excl(SegMap mine, SegMap* s_w) {
 // Binade of the approximate running sum before one element, when it is
 // unambiguous across the element (lo..hi inside one binade): log2 of its ulp,
 // else kNoGuess (the element is then added as a real DADD).
-__device__ __forceinline__ int guess_binade(double before, double after) {
-  const double lo = before * (1.0 - 1e-9), hi = after * (1.0 + 1e-9);
+__device__ __forceinline__ int guess_binade(double before, double after, double margin) {
+  const double lo = before * (1.0 - margin), hi = after * (1.0 + margin);
   if (!(lo > 0.0)) return kNoGuess;
   const int el = static_cast<int>((__double_as_longlong(lo) >> 52) & 0x7ff);
   const int eh = static_cast<int>((__double_as_longlong(hi) >> 52) & 0x7ff);
@@ -234,36 +234,255 @@ __device__ __forceinline__ int guess_binade(double before, double after) {
   return el == 0 ? -1074 : el - 1075;
 }
 
+// Block-collective (kSumT threads): the segmented structure of len <= kSumChunk
+// elements x[0, len) entered with the (approximate) running sum P0, as events
+// in order: runs of elements in one guessed binade with their composed map,
+// and lone elements at binade edges carrying their value (map.a0 = its bits).
+// Zeros met while the sum is still 0 are skipped (0.0 + ±0.0 == 0.0). Stores
+// at most `cap` events and returns the count; *bad <- any negative or
+// non-finite element.
+__device__ int seg_events(const double* __restrict__ x, int len, double P0, double margin, int* evstart, int* evg,
+                          IncPair* evmap, int cap, int* bad_out) {
+  __shared__ double s_dw[32];
+  __shared__ SegMap s_segw[32];
+  __shared__ int s_w[32];
+  __shared__ int s_nev;
+  const int tid = threadIdx.x;
+  double xv[kSumK];
+  double loc = 0.0;
+  int bad = 0;
+#pragma unroll
+  for (int k = 0; k < kSumK; ++k) {
+    const int i = tid * kSumK + k;
+    xv[k] = i < len ? x[i] : 0.0;
+    bad |= bad_value(xv[k]);
+    loc += xv[k];
+  }
+  *bad_out = __syncthreads_or(bad);
+  if (*bad_out) return 0;
+  double P = P0 + block_excl_sum(loc, s_dw);
+  int g[kSumK];
+  IncPair inc[kSumK];
+  unsigned int skip = 0;
+#pragma unroll
+  for (int k = 0; k < kSumK; ++k) {
+    const int i = tid * kSumK + k;
+    const double after = P + xv[k];
+    const bool sk = i >= len || (!(P > 0.0) && xv[k] == 0.0);
+    skip |= static_cast<unsigned int>(sk) << k;
+    g[k] = sk ? kNoGuess : guess_binade(P, after, margin);
+    inc[k] = g[k] != kNoGuess ? inc_of(xv[k], g[k])
+                              : IncPair{sk ? 0ll : static_cast<long long>(__double_as_longlong(xv[k])), 0};
+    P = after;
+  }
+  // event starts: a lone element (no guess) or the first of a run
+  const int tl = tid & 31, tw = tid >> 5;
+  if (tl == 31) s_w[tw] = g[kSumK - 1];
+  __syncthreads();
+  int prev_g = __shfl_up_sync(0xffffffffu, g[kSumK - 1], 1);
+  if (tl == 0) prev_g = tid > 0 ? s_w[tw - 1] : kNoGuess;
+  int fl[kSumK];
+  int nfl = 0;
+  SegMap agg{0, IncPair{0, 0}};
+#pragma unroll
+  for (int k = 0; k < kSumK; ++k) {
+    const int pg = k == 0 ? prev_g : g[k - 1];
+    fl[k] = !((skip >> k) & 1u) && (g[k] == kNoGuess || pg == kNoGuess || pg != g[k]);
+    nfl += fl[k];
+    agg = seg_compose(agg, SegMap{fl[k], inc[k]});
+  }
+  __syncthreads();  // every prev_g read before s_w is reused
+  // event numbers: an exclusive count of the starts
+  int incl = nfl;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (tl >= o) incl += y;
+  }
+  if (tl == 31) s_w[tw] = incl;
+  __syncthreads();
+  if (tid < 32) {
+    int wv = s_w[tid];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, wv, o);
+      if (tid >= o) wv += y;
+    }
+    s_w[tid] = wv;
+  }
+  __syncthreads();
+  const int ev0 = (tw > 0 ? s_w[tw - 1] : 0) + incl - nfl;
+  if (tid == kSumT - 1) s_nev = ev0 + nfl;
+  const SegMap before = block_seg_excl(agg, s_segw);  // syncs: s_nev visible, s_w reusable
+  const int nev = s_nev;
+  // does the next thread's first element start an event (or lie past the range)?
+  if (tl == 0) s_w[tw] = fl[0] || ((skip & 1u) && tid * kSumK >= len);
+  __syncthreads();
+  int next_fl0 = __shfl_down_sync(0xffffffffu, fl[0] || ((skip & 1u) && tid * kSumK >= len), 1);
+  if (tl == 31) next_fl0 = tw + 1 < (kSumT >> 5) ? s_w[tw + 1] : 1;
+  SegMap run = before;
+  int e = ev0 - 1;
+#pragma unroll
+  for (int k = 0; k < kSumK; ++k) {
+    const int i = tid * kSumK + k;
+    run = seg_compose(run, SegMap{fl[k], inc[k]});
+    if (fl[k]) {
+      ++e;
+      if (e < cap) {
+        evstart[e] = i;
+        evg[e] = g[k];
+      }
+    }
+    // the event's last element stores its map (a lone element: its value)
+    const bool last = i + 1 >= len || (k + 1 < kSumK ? (fl[k + 1] != 0) : (next_fl0 != 0));
+    if (!((skip >> k) & 1u) && last && e >= 0 && e < cap) evmap[e] = run.m;
+  }
+  __syncthreads();
+  return nev;
+}
+
+// One thread walks events from the exact running sum s: a run is applied only
+// if s is in its guessed binade and M stays below 2^53; a lone element is a
+// real DADD. Returns -1, or the first element (relative) of the event where a
+// check failed (s then holds the exact sum before it).
+__device__ int walk_events(double& s, const int* evstart, const int* evg, const IncPair* evmap, int nev) {
+  for (int ev = 0; ev < nev; ++ev) {
+    const int gg = evg[ev];
+    if (gg == kNoGuess) {
+      s = s + __longlong_as_double(evmap[ev].a0);
+      continue;
+    }
+    if (!(s > 0.0)) return evstart[ev];
+    int ul;
+    long long mm, m0;
+    binade(s, &ul, &mm, &m0);
+    const long long m1 = apply(evmap[ev], m0);
+    if (ul != gg || m1 >= mm) return evstart[ev];
+    s = static_cast<double>(m1) * ulp_of(ul);
+  }
+  return -1;
+}
+
+// A thread's K increments under ulp 2^ulog in FP64, when none is a tie: x/U
+// is a power-of-two scaling (exact; an underflow only happens far below 1/2),
+// (y + 2^52) - 2^52 rounds it half-to-even, and sums of integers below 2^53
+// are exact. Returns false on a tie (x/U exactly half an odd integer... any
+// half-integer): the increment pair then depends on the running M's parity.
+// An increment of 2^52 or more always leaves the binade: saturated.
+__device__ __forceinline__ bool inc_sum_fp64(const double (&xv)[kSumK], int ulog, long long* out) {
+  const int e1 = -ulog > 1000 ? 1000 : -ulog;  // 2^-ulog (up to 2^1074) in two factors
+  const int e2 = -ulog - e1;
+  const double f1 = __longlong_as_double(static_cast<long long>(e1 + 1023) << 52);
+  const double f2 = __longlong_as_double(static_cast<long long>(e2 + 1023) << 52);
+  constexpr double kTwo52 = 4503599627370496.0;
+  double sum = 0.0;
+  bool tie = false, big = false;
+#pragma unroll
+  for (int k = 0; k < kSumK; ++k) {
+    const double y = (xv[k] * f1) * f2;
+    big |= y >= kTwo52;
+    const double r = (y + kTwo52) - kTwo52;
+    tie |= fabs(y - r) == 0.5;
+    sum += r;
+  }
+  if (tie) return false;
+  *out = (big || sum >= 2.0 * kTwo52) ? kSumSat : static_cast<long long>(sum);
+  return true;
+}
+
+// argmax_state's candidate (the layout launch_argmax writes): the first
+// maximum in index order, compared with a strict > from -1.0
+struct ArgBest {
+  double v;
+  long long idx;
+  double unused;
+};
+__device__ __forceinline__ ArgBest arg_better(ArgBest a, ArgBest b) {
+  return ((b.v > a.v) || (b.v == a.v && b.idx < a.idx)) ? b : a;
+}
+__device__ __forceinline__ ArgBest arg_shfl_xor(ArgBest a, int o) {
+  ArgBest r;
+  r.v = __shfl_xor_sync(0xffffffffu, a.v, o);
+  r.idx = __shfl_xor_sync(0xffffffffu, a.idx, o);
+  r.unused = 0.0;
+  return r;
+}
+
 // ---- phase 1: approximate chunk sums (pairwise) + the domain check -------
+// (+ argmax_state's per-chunk candidate when `arg` is given: one read of x)
 __global__ void __launch_bounds__(256) k_chunk_sums(const double* __restrict__ x, size_t n, double* __restrict__ S,
-                                                    int* __restrict__ invalid) {
+                                                    int* __restrict__ invalid, ArgBest* __restrict__ arg) {
   __shared__ double ws[8];
+  __shared__ ArgBest wa[8];
   const size_t c0 = static_cast<size_t>(blockIdx.x) * kSumChunk;
   double acc = 0.0;
   int bad = 0;
-  for (int k = threadIdx.x; k < kSumChunk; k += 256) {
-    const size_t q = c0 + k;
-    if (q < n) {
-      const double v = x[q];
-      bad |= bad_value(v);
-      acc += v;
+  ArgBest best{-1.0, 0x7fffffffffffffffll, 0.0};
+  auto take = [&](double v, size_t q) {
+    bad |= bad_value(v);
+    acc += v;
+    if (v > best.v) {  // strict: the first (lowest) index of a tie
+      best.v = v;
+      best.idx = static_cast<long long>(q);
+    }
+  };
+  if (c0 + kSumChunk <= n) {  // a full chunk: loads batched, no bounds checks
+    constexpr int kU = 8;
+    for (int k0 = threadIdx.x; k0 < kSumChunk; k0 += 256 * kU) {
+      double v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) v[u] = x[c0 + k0 + u * 256];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) take(v[u], c0 + k0 + u * 256);
+    }
+  } else {
+    for (int k = threadIdx.x; k < kSumChunk; k += 256) {
+      const size_t q = c0 + k;
+      if (q < n) take(x[q], q);
     }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) *invalid = 1;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+  if (arg) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = arg_better(best, arg_shfl_xor(best, o));
+    if ((threadIdx.x & 31) == 0) wa[threadIdx.x >> 5] = best;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int w = 0; w < 8; ++w) t += ws[w];
     S[blockIdx.x] = t;
+    if (arg) {
+      ArgBest b = wa[0];
+      for (int w = 1; w < 8; ++w) b = arg_better(b, wa[w]);
+      arg[blockIdx.x] = b;
+    }
+  }
+}
+
+// the chunk candidates' best (argmax_state's result)
+__global__ void __launch_bounds__(1024) k_arg_final(const ArgBest* __restrict__ arg, int n_chunks,
+                                                    ArgBest* __restrict__ out) {
+  __shared__ ArgBest wa[32];
+  ArgBest best{-1.0, 0x7fffffffffffffffll, 0.0};
+  for (int c = threadIdx.x; c < n_chunks; c += 1024) best = arg_better(best, arg[c]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = arg_better(best, arg_shfl_xor(best, o));
+  if ((threadIdx.x & 31) == 0) wa[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ArgBest b = wa[0];
+    for (int w = 1; w < 32; ++w) b = arg_better(b, wa[w]);
+    *out = b;
   }
 }
 
 // ---- phase 2: which binade the running sum is in across each chunk -------
 __global__ void __launch_bounds__(1024) k_chunk_guess(const double* __restrict__ S, int n_chunks, double s0,
-                                                      int* __restrict__ guess) {
+                                                      int* __restrict__ guess, double* __restrict__ Pc) {
   // approximate prefix of the chunk sums (a block scan, tile by tile)
   __shared__ double ws[32];
   __shared__ double carry;
@@ -303,6 +522,7 @@ __global__ void __launch_bounds__(1024) k_chunk_guess(const double* __restrict__
         if (el == eh && el != 0x7ff) g = el == 0 ? -1074 : el - 1075;
       }
       guess[c] = g;
+      Pc[c] = before;
     }
     __syncthreads();
     if (tid == 1023) carry = carry + ws[31];
@@ -310,22 +530,104 @@ __global__ void __launch_bounds__(1024) k_chunk_guess(const double* __restrict__
   }
 }
 
+// ---- phase 3a: crossing chunks' events (all SMs) ------------------------
+constexpr int kEvCap = 256;   // events per crossing chunk precomputed by the all-SM pass
+constexpr int kEvPool = 512;  // crossing chunks that get precomputed events (the rest: the walk's own pass)
+
+// A persistent grid walks the chunks: most are guessed (nothing to do).
+__global__ void __launch_bounds__(kSumT) k_chunk_events(const double* __restrict__ x, size_t n, int n_chunks,
+                                                        const int* __restrict__ guess, const double* __restrict__ Pc,
+                                                        int* __restrict__ ev_n, int* __restrict__ ev_slot,
+                                                        int* __restrict__ pool_ctr, int* __restrict__ pool_start,
+                                                        int* __restrict__ pool_g, IncPair* __restrict__ pool_map) {
+  __shared__ int s_slot;
+  for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    if (guess[c] != kNoGuess) {
+      if (threadIdx.x == 0) ev_n[c] = -1;
+      continue;
+    }
+    // a chunk where the running sum crosses binades: its events, from the
+    // approximate prefix before it (the walk verifies every run)
+    if (threadIdx.x == 0) s_slot = atomicAdd(pool_ctr, 1);
+    __syncthreads();
+    const int slot = s_slot;
+    __syncthreads();
+    if (slot >= kEvPool) {
+      if (threadIdx.x == 0) ev_n[c] = -1;
+      continue;
+    }
+    const size_t c0 = static_cast<size_t>(c) * kSumChunk;
+    const int len = static_cast<int>(min(static_cast<size_t>(kSumChunk), n - c0));
+    int bad;
+    const int nev = seg_events(x + c0, len, Pc[c], 1e-7, pool_start + slot * kEvCap, pool_g + slot * kEvCap,
+                               pool_map + static_cast<size_t>(slot) * kEvCap, kEvCap, &bad);
+    if (threadIdx.x == 0) {
+      ev_n[c] = (bad || nev > kEvCap) ? -1 : nev;
+      ev_slot[c] = slot;
+    }
+  }
+}
+
 // ---- phase 3: each guessed chunk's composed map ---------------------------
-__global__ void __launch_bounds__(kSumT) k_chunk_maps(const double* __restrict__ x, size_t n,
-                                                      const int* __restrict__ guess, IncPair* __restrict__ maps) {
+__global__ void __launch_bounds__(kSumT, 2) k_chunk_maps(const double* __restrict__ x, size_t n,
+                                                         const int* __restrict__ guess, IncPair* __restrict__ maps) {
   __shared__ IncPair s_warp[32];
+  __shared__ long long s_sum[32];
   const int g = guess[blockIdx.x];
   if (g == kNoGuess) return;
-  const size_t base = static_cast<size_t>(blockIdx.x) * kSumChunk + static_cast<size_t>(threadIdx.x) * kSumK;
-  IncPair mine{0, 0};
+  const size_t c0 = static_cast<size_t>(blockIdx.x) * kSumChunk;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // Without ties the chunk's map is {R, R} with R the sum of the increments,
+  // and an integer sum has no order: coalesced loads, any association.
+  double xv[kSumK];
 #pragma unroll
   for (int k = 0; k < kSumK; ++k) {
-    const size_t q = base + k;
-    if (q < n) mine = compose(mine, inc_of(x[q], g));
+    const size_t q = c0 + threadIdx.x + static_cast<size_t>(k) * kSumT;
+    xv[k] = q < n ? x[q] : 0.0;
   }
-  IncPair excl;
-  const IncPair incl = block_scan(mine, s_warp, &excl);
-  if (threadIdx.x == kSumT - 1) maps[blockIdx.x] = incl;
+  long long r;
+  const bool no_tie = inc_sum_fp64(xv, g, &r);
+  if (__syncthreads_and(no_tie)) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r = sat_add(r, __shfl_xor_sync(0xffffffffu, r, o));
+    if (lane == 0) s_sum[warp] = r;
+    __syncthreads();
+    if (warp == 0) {
+      r = s_sum[lane];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) r = sat_add(r, __shfl_xor_sync(0xffffffffu, r, o));
+      if (lane == 0) maps[blockIdx.x] = IncPair{r, r};
+    }
+    return;
+  }
+  // a tie somewhere: the ordered composition of each thread's K consecutive
+  // elements, then of the threads in order (lane l, then l + o)
+  const size_t base = c0 + static_cast<size_t>(threadIdx.x) * kSumK;
+#pragma unroll
+  for (int k = 0; k < kSumK; ++k) xv[k] = base + k < n ? x[base + k] : 0.0;
+  IncPair mine{0, 0};
+#pragma unroll
+  for (int k = 0; k < kSumK; ++k) mine = compose(mine, inc_of(xv[k], g));
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    IncPair y;
+    y.a0 = __shfl_down_sync(0xffffffffu, mine.a0, o);
+    y.a1 = __shfl_down_sync(0xffffffffu, mine.a1, o);
+    if ((lane & (2 * o - 1)) == 0) mine = compose(mine, y);
+  }
+  if (lane == 0) s_warp[warp] = mine;
+  __syncthreads();
+  if (warp == 0) {
+    mine = s_warp[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      IncPair y;
+      y.a0 = __shfl_down_sync(0xffffffffu, mine.a0, o);
+      y.a1 = __shfl_down_sync(0xffffffffu, mine.a1, o);
+      if ((lane & (2 * o - 1)) == 0) mine = compose(mine, y);
+    }
+    if (lane == 0) maps[blockIdx.x] = mine;
+  }
 }
 
 // ---- phase 4 (or the whole sum for small inputs): one CTA walks the chunks
@@ -337,8 +639,7 @@ __device__ long long g_seq_dbg[8];  // whole-chunk steps, segmented ok, segmente
 #endif
 constexpr int kSegEv = 2048;  // events (segments + lone elements) per range in the segmented walk
 struct SeqSmem {
-  double xs[kSumChunk];    // the range's elements
-  IncPair evmap[kSegEv];   // a segment's composed map
+  IncPair evmap[kSegEv];   // a run's composed map (a lone element: its value's bits)
   int evstart[kSegEv];     // an event's first element (relative)
   int evg[kSegEv];         // its binade (kNoGuess: one element, a real DADD)
 };
@@ -346,16 +647,17 @@ constexpr size_t kSeqSmem = sizeof(SeqSmem);
 
 __global__ void __launch_bounds__(kSumT) k_seq_sum(const double* __restrict__ x, size_t n, double s0,
                                                    const int* __restrict__ guess, const IncPair* __restrict__ maps,
-                                                   const double* __restrict__ S, double* __restrict__ total,
-                                                   int* __restrict__ invalid) {
+                                                   const double* __restrict__ S, const int* __restrict__ ev_n,
+                                                   const int* __restrict__ ev_slot, const int* __restrict__ pool_start,
+                                                   const int* __restrict__ pool_g, const IncPair* __restrict__ pool_map,
+                                                   double* __restrict__ total, int* __restrict__ invalid) {
   extern __shared__ __align__(16) unsigned char seq_dyn[];
   SeqSmem& sm = *reinterpret_cast<SeqSmem*>(seq_dyn);
   __shared__ IncPair s_warp[32];
-  __shared__ SegMap s_segw[32];
-  __shared__ double s_dw[32];
-  __shared__ int s_nev, s_fail, s_lastg[32];
+  __shared__ int s_fail;
   __shared__ double s_walk;
   size_t seg_skip = ~size_t(0);  // a chunk whose segmented walk failed (its rest goes element-wise)
+  size_t pre_skip = ~size_t(0);  // a chunk whose precomputed events failed (its rest: the walk's own pass)
   __shared__ unsigned long long s_cross;  // first element whose running M leaves the binade
   __shared__ long long s_mprev;            // its predecessor's M
   __shared__ long long s_mend;             // M at the end of the range (no crossing)
@@ -376,25 +678,56 @@ __global__ void __launch_bounds__(kSumT) k_seq_sum(const double* __restrict__ x,
     // every range ends at the next chunk boundary, so ranges after a binade
     // crossing re-align with the per-chunk maps
     const size_t end = min(n, (pos / kSumChunk + 1) * static_cast<size_t>(kSumChunk));
-    if (s == 0.0) {
-      // 0.0 + x == x exactly: the sum starts at the first nonzero element.
-      // Whole chunks of zeros (chunk sum 0: no negative values here) are
-      // skipped 1024 at a time.
-      if (S && pos % kSumChunk == 0) {
-        const size_t c0 = pos / kSumChunk;
-        const size_t nch = (n + kSumChunk - 1) / kSumChunk;
-        if (tid == 0) s_first = ~0ull;
-        __syncthreads();
-        if (c0 + tid < nch && S[c0 + tid] != 0.0) atomicMin(&s_first, static_cast<unsigned long long>(c0 + tid));
-        __syncthreads();
-        const unsigned long long fc = s_first;
-        __syncthreads();
-        const size_t to = fc == ~0ull ? min(nch, c0 + kSumT) : static_cast<size_t>(fc);
-        if (to > c0) {
-          pos = min(n, to * static_cast<size_t>(kSumChunk));
-          continue;
-        }
+    // 0.0 + x == x exactly: while the sum is 0 it starts at the first nonzero
+    // element. Whole chunks of zeros (chunk sum 0: no negative values here)
+    // are skipped 1024 at a time.
+    if (s == 0.0 && S && pos % kSumChunk == 0) {
+      const size_t c0 = pos / kSumChunk;
+      const size_t nch = (n + kSumChunk - 1) / kSumChunk;
+      if (tid == 0) s_first = ~0ull;
+      __syncthreads();
+      if (c0 + tid < nch && S[c0 + tid] != 0.0) atomicMin(&s_first, static_cast<unsigned long long>(c0 + tid));
+      __syncthreads();
+      const unsigned long long fc = s_first;
+      __syncthreads();
+      const size_t to = fc == ~0ull ? min(nch, c0 + kSumT) : static_cast<size_t>(fc);
+      if (to > c0) {
+        pos = min(n, to * static_cast<size_t>(kSumChunk));
+        continue;
       }
+    }
+    // a crossing chunk whose events the all-SM pass precomputed
+    if (ev_n && pos % kSumChunk == 0 && pos / kSumChunk != pre_skip) {
+      const size_t c = pos / kSumChunk;
+      const int ne = ev_n[c];
+      if (ne >= 0) {
+        const int slot = ev_slot[c];
+        for (int i = tid; i < ne; i += kSumT) {
+          sm.evstart[i] = pool_start[slot * kEvCap + i];
+          sm.evg[i] = pool_g[slot * kEvCap + i];
+          sm.evmap[i] = pool_map[static_cast<size_t>(slot) * kEvCap + i];
+        }
+        __syncthreads();
+        if (tid == 0) {
+          double sw = s;
+          s_fail = walk_events(sw, sm.evstart, sm.evg, sm.evmap, ne);
+          s_walk = sw;
+        }
+        __syncthreads();
+        s = s_walk;
+        const int fail = s_fail;
+        __syncthreads();
+        if (fail < 0) {
+          pos = end;
+        } else {
+          pos += fail;  // exact s before element `fail`
+          pre_skip = c;
+        }
+        SEQ_DBG(6, 1);
+        continue;
+      }
+    }
+    if (s == 0.0) {
       if (tid == 0) s_first = ~0ull;
       __syncthreads();
       for (size_t q = pos + tid; q < end; q += kSumT)
@@ -458,119 +791,17 @@ __global__ void __launch_bounds__(kSumT) k_seq_sum(const double* __restrict__ x,
     // elements at binade edges as real DADDs. Many crossings cost one pass.
     if (pos / kSumChunk != seg_skip) {
       const int len = static_cast<int>(end - pos);
-      double xv[kSumK];
-      double loc = 0.0;
-      int bad = 0;
-#pragma unroll
-      for (int k = 0; k < kSumK; ++k) {
-        const int i = tid * kSumK + k;
-        xv[k] = i < len ? x[pos + i] : 0.0;
-        bad |= bad_value(xv[k]);
-        sm.xs[i] = xv[k];
-        loc += xv[k];
-      }
-      if (__syncthreads_or(bad)) {
+      int bad;
+      const int nev = seg_events(x + pos, len, s, 1e-9, sm.evstart, sm.evg, sm.evmap, kSegEv, &bad);
+      if (bad) {
         if (tid == 0) *invalid = 1;
         return;
       }
-      double P = s + block_excl_sum(loc, s_dw);
-      int g[kSumK];
-      IncPair inc[kSumK];
-#pragma unroll
-      for (int k = 0; k < kSumK; ++k) {
-        const double after = P + xv[k];
-        g[k] = tid * kSumK + k < len ? guess_binade(P, after) : kNoGuess;
-        inc[k] = g[k] != kNoGuess ? inc_of(xv[k], g[k]) : IncPair{0, 0};
-        P = after;
-      }
-      // event starts: a lone element (no guess) or the first of a run
-      if ((tid & 31) == 31) s_lastg[tid >> 5] = g[kSumK - 1];
-      __syncthreads();
-      int prev_g = __shfl_up_sync(0xffffffffu, g[kSumK - 1], 1);
-      if ((tid & 31) == 0) prev_g = tid > 0 ? s_lastg[(tid >> 5) - 1] : kNoGuess;
-      int fl[kSumK];
-      int nfl = 0;
-      SegMap agg{0, IncPair{0, 0}};
-#pragma unroll
-      for (int k = 0; k < kSumK; ++k) {
-        const int i = tid * kSumK + k;
-        const int pg = k == 0 ? prev_g : g[k - 1];
-        fl[k] = i < len && (g[k] == kNoGuess || i == 0 || pg == kNoGuess || pg != g[k]);
-        nfl += fl[k];
-        agg = seg_compose(agg, SegMap{fl[k], inc[k]});
-      }
-      // event numbers: an exclusive count of the starts
-      __syncthreads();  // every prev_g read before s_lastg is reused
-      int ev0 = 0;
-      {
-        int incl = nfl;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if ((tid & 31) >= o) incl += y;
-        }
-        if ((tid & 31) == 31) s_lastg[tid >> 5] = incl;
-        __syncthreads();
-        if (tid < 32) {
-          int wv = s_lastg[tid];
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, wv, o);
-            if (tid >= o) wv += y;
-          }
-          s_lastg[tid] = wv;
-        }
-        __syncthreads();
-        ev0 = ((tid >> 5) > 0 ? s_lastg[(tid >> 5) - 1] : 0) + incl - nfl;
-        if (tid == kSumT - 1) s_nev = ev0 + nfl;
-      }
-      const SegMap before = block_seg_excl(agg, s_segw);  // syncs: s_nev visible
-      const int nev = s_nev;
-      // does the next thread's first element start an event (or is past the range)?
-      if ((tid & 31) == 0) s_lastg[tid >> 5] = fl[0];
-      __syncthreads();
-      int next_fl0 = __shfl_down_sync(0xffffffffu, fl[0], 1);
-      if ((tid & 31) == 31) next_fl0 = tid + 1 < kSumT ? s_lastg[(tid >> 5) + 1] : 1;
       if (nev <= kSegEv) {
-        SegMap run = before;
-        int e = ev0 - 1;
-#pragma unroll
-        for (int k = 0; k < kSumK; ++k) {
-          const int i = tid * kSumK + k;
-          if (i >= len) break;
-          run = seg_compose(run, SegMap{fl[k], inc[k]});
-          if (fl[k]) {
-            ++e;
-            sm.evstart[e] = i;
-            sm.evg[e] = g[k];
-          }
-          // the run's last element stores the run's map
-          const bool last = i + 1 == len || (k + 1 < kSumK ? fl[k + 1] != 0 : next_fl0 != 0);
-          if (g[k] != kNoGuess && last) sm.evmap[e] = run.m;
-        }
-        __syncthreads();
         if (tid == 0) {
           double sw = s;
-          int fail = -1;
-          for (int ev = 0; ev < nev; ++ev) {
-            const int a = sm.evstart[ev];
-            const int gg = sm.evg[ev];
-            if (gg == kNoGuess) {
-              sw = sw + sm.xs[a];
-              continue;
-            }
-            int ul;
-            long long mm, m0w;
-            binade(sw, &ul, &mm, &m0w);
-            const long long m1 = apply(sm.evmap[ev], m0w);
-            if (ul != gg || m1 >= mm) {
-              fail = a;
-              break;
-            }
-            sw = static_cast<double>(m1) * ulp_of(ul);
-          }
+          s_fail = walk_events(sw, sm.evstart, sm.evg, sm.evmap, nev);
           s_walk = sw;
-          s_fail = fail;
         }
         __syncthreads();
         s = s_walk;
@@ -672,7 +903,8 @@ __global__ void k_seq_sum_chain(const double* __restrict__ x, size_t n, double s
 
 size_t seq_sum_scratch_bytes(size_t n) {
   const size_t chunks = (n + kSumChunk - 1) / kSumChunk;
-  return chunks * (sizeof(double) + sizeof(int) + sizeof(IncPair)) + 64;
+  return chunks * (sizeof(IncPair) + 2 * sizeof(double) + 3 * sizeof(int) + sizeof(ArgBest)) +
+         static_cast<size_t>(kEvPool) * kEvCap * (sizeof(IncPair) + 2 * sizeof(int)) + 64;
 }
 
 static void seq_sum_smem_attr() {
@@ -685,35 +917,57 @@ static void seq_sum_smem_attr() {
 void launch_seq_sum(gl_context* ctx, const double* x, size_t n, double* d_total, int* d_invalid, double s0) {
   seq_sum_smem_attr();
   cudaMemsetAsync(d_invalid, 0, sizeof(int), ctx->stream);
-  k_seq_sum<<<1, kSumT, kSeqSmem, ctx->stream>>>(x, n, s0, nullptr, nullptr, nullptr, d_total, d_invalid);
+  k_seq_sum<<<1, kSumT, kSeqSmem, ctx->stream>>>(x, n, s0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                                 nullptr, nullptr, d_total, d_invalid);
   ctx->launches++;
 }
 
+bool seq_sum_fuses_argmax(size_t n) { return (n + kSumChunk - 1) / kSumChunk > 4; }
+
 void launch_seq_sum_big(gl_context* ctx, const double* x, size_t n, double* d_total, int* d_invalid,
-                        void* scratch, double s0) {
+                        void* scratch, double s0, void* d_argmax) {
   const size_t chunks = (n + kSumChunk - 1) / kSumChunk;
+  if (d_argmax && !seq_sum_fuses_argmax(n)) throw std::runtime_error("seq-sum: argmax fusion needs > 4 chunks");
   if (chunks <= 4) {
     launch_seq_sum(ctx, x, n, d_total, d_invalid, s0);
     return;
   }
+  const size_t pool = static_cast<size_t>(kEvPool) * kEvCap;
   auto* maps = static_cast<IncPair*>(scratch);  // 16-byte aligned first
-  auto* S = reinterpret_cast<double*>(maps + chunks);
-  auto* guess = reinterpret_cast<int*>(S + chunks);
+  auto* pool_map = maps + chunks;
+  auto* S = reinterpret_cast<double*>(pool_map + pool);
+  auto* Pc = S + chunks;
+  auto* guess = reinterpret_cast<int*>(Pc + chunks);
+  auto* ev_n = guess + chunks;
+  auto* ev_slot = ev_n + chunks;
+  auto* pool_start = ev_slot + chunks;
+  auto* pool_g = pool_start + pool;
+  auto* pool_ctr = pool_g + pool;
+  auto* arg = reinterpret_cast<ArgBest*>((reinterpret_cast<uintptr_t>(pool_ctr + 1) + 15) & ~uintptr_t(15));
   cudaMemsetAsync(d_invalid, 0, sizeof(int), ctx->stream);
+  cudaMemsetAsync(pool_ctr, 0, sizeof(int), ctx->stream);
   const int nc = static_cast<int>(chunks);
-  k_chunk_sums<<<nc, 256, 0, ctx->stream>>>(x, n, S, d_invalid);
-  k_chunk_guess<<<1, 1024, 0, ctx->stream>>>(S, nc, s0, guess);
+  k_chunk_sums<<<nc, 256, 0, ctx->stream>>>(x, n, S, d_invalid, d_argmax ? arg : nullptr);
+  if (d_argmax) {
+    k_arg_final<<<1, 1024, 0, ctx->stream>>>(arg, nc, static_cast<ArgBest*>(d_argmax));
+    ctx->launches++;
+  }
+  k_chunk_guess<<<1, 1024, 0, ctx->stream>>>(S, nc, s0, guess, Pc);
   k_chunk_maps<<<nc, kSumT, 0, ctx->stream>>>(x, n, guess, maps);
+  const int ev_grid = min(nc, 2 * (ctx->sm_count > 0 ? ctx->sm_count : 148));
+  k_chunk_events<<<ev_grid, kSumT, 0, ctx->stream>>>(x, n, nc, guess, Pc, ev_n, ev_slot, pool_ctr, pool_start, pool_g,
+                                                     pool_map);
   seq_sum_smem_attr();
-  k_seq_sum<<<1, kSumT, kSeqSmem, ctx->stream>>>(x, n, s0, guess, maps, S, d_total, d_invalid);
-  ctx->launches += 4;
+  k_seq_sum<<<1, kSumT, kSeqSmem, ctx->stream>>>(x, n, s0, guess, maps, S, ev_n, ev_slot, pool_start, pool_g,
+                                                 pool_map, d_total, d_invalid);
+  ctx->launches += 5;
 #ifdef GL_EXPERIMENT_ENV
   if (getenv("GL_DEBUG_SEQSUM")) {
     long long h[8];
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpyFromSymbol(h, g_seq_dbg, sizeof(h));
-    fprintf(stderr, "seq sum n=%zu chunks=%zu: whole-chunk steps %lld, segmented ok %lld, failed %lld, events %lld, element-wise steps %lld, over cap %lld\n",
-            n, chunks, h[0], h[1], h[2], h[3], h[4], h[5]);
+    fprintf(stderr, "seq sum n=%zu chunks=%zu: whole-chunk steps %lld, segmented ok %lld, failed %lld, events %lld, element-wise steps %lld, over cap %lld, precomputed chunks %lld\n",
+            n, chunks, h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
     const long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(g_seq_dbg, z, sizeof(z));
   }

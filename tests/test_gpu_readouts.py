@@ -68,6 +68,27 @@ def test_argmax_tie_rule(ctx):
         g.argmax_state(t)
 
 
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_argmax_fused_chunk_pass_ties(ctx, port, seed):
+    """Tensors above 4 x 8192 states take the argmax candidates in the exact
+    total's chunk pass (k_seqsum.cu k_chunk_sums): equal maxima planted in
+    different chunks and inside one chunk, the lowest flat index must win,
+    and the confidence stays the sequential total."""
+    rng = np.random.default_rng(seed)
+    B = rng.random((12, 70, 90)) * 0.5
+    flat = B.reshape(-1)
+    spots = np.sort(rng.choice(flat.size, 6, replace=False))
+    flat[spots] = 0.75
+    flat[spots[-1] - 1] = 0.75  # a tie inside one chunk too
+    t = g.BeliefTensor(90, 70, 12, 0.1, 0.5, -1.0, ctx=ctx)
+    t.set_values(B)
+    t.set_theta_t(0.3)
+    est = g.argmax_state(t)
+    (i, j, k), pose, conf = port.argmax(B, 0.1, 0.5, -1.0, 0.3)
+    assert (est.i, est.j, est.k) == (i, j, k)
+    assert est.confidence == conf
+
+
 @pytest.mark.parametrize("w,h,p", [(1, 7, 0.0), (7, 1, 0.0), (2, 2, 0.0), (33, 17, 0.1), (64, 64, 0.02),
                                    (301, 123, 0.3), (512, 384, 0.05), (130, 70, 0.6)])
 def test_distance_field_on_device_bit_exact(ctx, port, w, h, p):
