@@ -513,10 +513,10 @@ def run_lidar(args, cfg, world, rank, local):
     g.tensor_status(t)
     ms_max = dist_max(ms, world, "ours")
     value = world * args.steps / (ms_max / 1e3)
-    # e2e over the same trajectory: the belief restarts from the uniform state
-    # with the same warm-up (the dither's cost depends on how concentrated
-    # the belief is, so a later stretch of the run would be another workload)
-    n_e2e = max(every, min(args.steps, args.e2e_steps))
+    # e2e over the same trajectory and length: the belief restarts from the
+    # uniform state with the same warm-up (the dither's cost depends on how
+    # concentrated the belief is, so another stretch would be another workload)
+    n_e2e = args.steps
     del t
     t = g.init_uniform(m, C, ctx)
     loop(max(args.warmup, every + 1), False)
@@ -544,7 +544,8 @@ def run_lidar(args, cfg, world, rank, local):
         "e2e": {"value": e2e, "unit": "Hz", "h2d_bytes_per_step": 16 * C + (8 * 24 * 2 + 8 * 2 * 512) // every,
                 "d2h_bytes_per_step": 4 + (8 * 2 * 512 + 16) // every,
                 "how": f"{n_e2e} synchronous gl_step calls with the observation cycle every {every}, wall clock, "
-                       f"over the same trajectory as value (the belief restarted from uniform, same warm-up)"},
+                       f"over the same trajectory as value (the belief restarted from uniform, same warm-up and "
+                       f"step count)"},
         "roofline": {"bound": "hbm", "achieved": bytes_launch / avg_kern_s / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": bytes_launch / avg_kern_s / 1e9 / peak, "traffic": ncu_traffic("c2"),
                      "peak_source": peak_src, "bytes_per_launch": bytes_launch, "avg_kernel_ms": avg_kern_s * 1e3,
