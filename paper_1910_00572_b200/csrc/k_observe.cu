@@ -912,34 +912,34 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
       const int pd = dir;
       const double E1l = s_k[d][2], E1h = s_k[d][3], E5l = s_k[d][4], E5h = s_k[d][5], E3l = s_k[d][6],
                    E3h = s_k[d][7];
-      if (tid < 4) {  // the row-end positions 0, 1, w-2, w-1: missing sources, row-end quotients
-        const int pos = tid < 2 ? tid : w - 4 + tid;
-        const int t = pd == 1 ? pos : w - 1 - pos;  // column of row j at scan position pos
-        double v = nbuf[w - 1 - pos] * scale;       // row j+1 scans the other way
-        if (pos >= 1) v += err[pos - 1] * ((t - pd == 0) ? E1l : (t - pd == w - 1 ? E1h : 1.0 / 16.0));
-        v += err[pos] * ((t == 0) ? E5l : (t == w - 1 ? E5h : 5.0 / 16.0));
-        if (pos + 1 < w) v += err[pos + 1] * ((t + pd == 0) ? E3l : (t + pd == w - 1 ? E3h : 3.0 / 16.0));
-        nbuf[w - 1 - pos] = v;
-      }
-      // interior positions [2, w-3]: all three sources, interior quotients;
-      // branch-free batches of 4 (clamped loads, guarded stores)
-      const int n_in = w - 4;
-      for (int i0 = tid; i0 < n_in; i0 += 4 * kSegT) {
+      // Interior positions [2, w-3] have all three sources and the interior
+      // quotients; the row ends (0, 1, w-2, w-1) miss a source or take a
+      // row-end quotient. One branch-free pass over all positions in batches
+      // of 4 (clamped loads, guarded stores): a missing source's term is not
+      // added (a select, not + 0.0, so signed zeros stay the reference's).
+      for (int i0 = tid; i0 < w; i0 += 4 * kSegT) {
         double v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int pos = min(i0 + u * kSegT, n_in - 1) + 2;
-          double x = nbuf[w - 1 - pos] * scale;
-          x += err[pos - 1] * (1.0 / 16.0);
-          x += err[pos] * (5.0 / 16.0);
-          x += err[pos + 1] * (3.0 / 16.0);
+          const int pos = min(i0 + u * kSegT, w - 1);
+          const int t = pd == 1 ? pos : w - 1 - pos;  // column of row j at scan position pos
+          const double c1 = (t - pd == 0) ? E1l : (t - pd == w - 1 ? E1h : 1.0 / 16.0);
+          const double c5 = (t == 0) ? E5l : (t == w - 1 ? E5h : 5.0 / 16.0);
+          const double c3 = (t + pd == 0) ? E3l : (t + pd == w - 1 ? E3h : 3.0 / 16.0);
+          double x = nbuf[w - 1 - pos] * scale;  // row j+1 scans the other way
+          const double up = x + err[max(pos - 1, 0)] * c1;
+          x = pos >= 1 ? up : x;
+          x += err[pos] * c5;
+          const double dn = x + err[min(pos + 1, w - 1)] * c3;
+          x = pos + 1 < w ? dn : x;
           v[u] = x;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          if (i0 + u * kSegT < n_in) nbuf[w - 3 - (i0 + u * kSegT)] = v[u];
+          if (i0 + u * kSegT < w) nbuf[w - 1 - (i0 + u * kSegT)] = v[u];
         }
       }
+      SEG_TICK(tk_g0);
       __syncthreads();
     }
     SEG_TICK(tk_pre);
@@ -1197,7 +1197,7 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpyFromSymbol(clk, g_dither_clk, sizeof(clk));
     fprintf(stderr, "dither clocks: %lld %lld %lld %lld %lld %lld %lld %lld %lld (pipe: row-end wait, total, sweep, row-start wait; seg: spec, verify, pre, all, barrier-1 wait, staging, group chain, group rest, replays) (%d x %d)\n", clk[0], clk[1], clk[2], clk[3], clk[4], clk[5], clk[6], clk[7] & ((1LL << 40) - 1), clk[7] >> 40, w, h);
-    fprintf(stderr, "dither events: fixed lanes %lld, fixed pixels %lld, exact rows %lld\n", clk[9], clk[10], clk[11]);
+    fprintf(stderr, "dither events: fixed lanes %lld, fixed pixels %lld, exact rows %lld; post pass: edge %lld loop %lld\n", clk[9], clk[10], clk[11], clk[8], clk[6]);
   }
 #endif
 
