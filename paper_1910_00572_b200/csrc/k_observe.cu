@@ -637,13 +637,15 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
                                                       const int* __restrict__ sum_invalid, int* __restrict__ done) {
   extern __shared__ double segsh[];
   const int WR = ((w + 1) & ~1) + 16, SW = (w + 31) / 32 + 2;  // +16: a lane's last group reads past w
-  // buf[j & 1]: row j's pre-accumulated work (scan order); buf[(j + 1) & 1]
-  // receives row j + 1 of bm, scan order, by cp.async while row j sweeps
+  // buf[j & 1]: row j's pre-accumulated work (scan order); buf[(j + 1) & 1]:
+  // row j + 1's, built by warps 1..3 while row j is verified
   double* buf0 = segsh;
   double* err = segsh + 2 * WR;  // row j's errors, scan order
-  unsigned int* sup0 = reinterpret_cast<unsigned int*>(segsh + 3 * WR);  // [2][SW] support bits, scan order
+  double* raw = segsh + 3 * WR;  // row j + 1 of bm in its scan order (cp.async while row j sweeps)
+  unsigned int* sup0 = reinterpret_cast<unsigned int*>(segsh + 4 * WR);  // [2][SW] support bits, scan order
   unsigned int* ebits = sup0 + 2 * SW;  // [SW] row j's emission bits, scan order
   __shared__ int s_count;
+  __shared__ int s_chg_hi[32];  // row j: the last error a lane's verification reruns rewrote (-1: none)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (*sum_invalid) {  // negative / non-finite plane: k_dither_pipe's sequential total takes it
     if (tid == 0) *done = 0;
@@ -709,7 +711,8 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
     const int start = dir == 1 ? 0 : w - 1;
     const bool last = j == h - 1;
     double* pre = buf0 + d * WR;            // row j's pre-accumulated work
-    double* nbuf = buf0 + (d ^ 1) * WR;     // row j + 1: bm (staged), then its pre
+    double* nbuf = buf0 + (d ^ 1) * WR;     // row j + 1's pre (built by warps 1..3 during row j)
+    const bool nxt = j + 1 < h;
     const unsigned int* sup = sup0 + d * SW;
     unsigned int* nsup = sup0 + (d ^ 1) * SW;
     const double c_first = last ? fs_carry_coef(start, j, w, h, dir) : s_k[d][0];
@@ -743,6 +746,12 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
         ++n_exact;
 #endif
         if (lane == 0) exact_row();
+        s_chg_hi[lane] = -1;
+        __syncwarp();
+        if (nxt) {  // the errors are final: warps 1..3 take the next row
+          asm volatile("bar.arrive 3, %0;" ::"r"(kSegT) : "memory");
+          asm volatile("bar.arrive 4, %0;" ::"r"(kSegT) : "memory");
+        }
       } else {
         const bool act = lane < L.P;
         const int qs = L.start(lane), qe = L.start(lane + 1);
@@ -782,6 +791,9 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
 #endif
         }
         __syncwarp();
+        // warps 1..3 start the next row's pass on these errors now; what the
+        // verification below rewrites they recompute after barrier 4
+        if (nxt) asm volatile("bar.arrive 3, %0;" ::"r"(kSegT) : "memory");
         SEG_TICK(tk_spec);
         // ---- verification, all lanes at once. Lane l >= 1 is exact if its
         // warm-up's last error equals lane l-1's error before its segment;
@@ -791,6 +803,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
         // final; a lane whose rerun reached its segment end without meeting
         // changed that end, and its successor reruns in another round. ----
         bool todo = act && lane > 0, recheck = true;
+        int chg_hi = -1;  // the last error this lane's reruns rewrote
         while (__any_sync(0xffffffffu, todo)) {
           bool run = false;
           double cr = 0.0;
@@ -827,6 +840,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
               for (int k = 0; k < 16; ++k) {
                 if (k <= m) err[base + k] = v[k];
               }
+              chg_hi = max(chg_hi, base + m);
               const unsigned int keep = m >= 15 ? 0xffffu : ((2u << m) - 1u);
               const int sh = base & 31;
               const unsigned long long ow = static_cast<unsigned long long>(ebits[base >> 5]) |
@@ -851,7 +865,9 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
           __syncwarp();
           todo = act && lane > 0 && ((ch >> (lane - 1)) & 1u);
         }
+        s_chg_hi[lane] = chg_hi;
         __syncwarp();
+        if (nxt) asm volatile("bar.arrive 4, %0;" ::"r"(kSegT) : "memory");
         // ---- the row's emissions in scan order: a warp scan over the
         // emission words (cleared for the next row) ----
         const int nw = (w + 31) >> 5;
@@ -883,65 +899,74 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
         if (lane == 0) s_count = c_base;
       }
       SEG_TICK(tk_ver);
-    } else if (j + 1 < h) {
-      // warps 1..3, while warp 0 sweeps row j: row j + 1 of bm into nbuf in
-      // its scan order (all loads in flight at once), then its support bits
+    } else if (nxt) {
+      // ---- warps 1..3 while warp 0 sweeps row j: row j + 1 of bm into raw
+      // in its scan order (all loads in flight at once) and its support
+      // bits; once warp 0's chains are done, row j + 1's pre-accumulation
+      // (overlapping warp 0's verification); then the positions next to
+      // errors the verification rewrote ----
       const double* brow = bm + static_cast<size_t>(j + 1) * w;
       const bool rev = dir == 1;  // row j + 1 scans right to left
-      for (int t = tid - 32; t < w; t += kSegT - 32) {
-        const unsigned int dst = static_cast<unsigned int>(__cvta_generic_to_shared(nbuf + (rev ? w - 1 - t : t)));
+      const int t3 = tid - 32;    // 0..95
+      constexpr int kT3 = kSegT - 32;
+      for (int t = t3; t < w; t += kT3) {
+        const unsigned int dst = static_cast<unsigned int>(__cvta_generic_to_shared(raw + (rev ? w - 1 - t : t)));
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(brow + t) : "memory");
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
-      asm volatile("bar.sync 1, %0;" ::"r"(kSegT - 32) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"r"(kT3) : "memory");
       for (int wd = warp - 1; wd <= w / 32; wd += kSegT / 32 - 1) {
         const int qn = wd * 32 + lane;
-        const unsigned int bits = __ballot_sync(0xffffffffu, qn < w && nbuf[qn] > 0.0);
+        const unsigned int bits = __ballot_sync(0xffffffffu, qn < w && raw[qn] > 0.0);
         if (lane == 0) nsup[wd] = bits;
       }
 #ifdef GL_EXPERIMENT_ENV
       if (tid == 32) tk_stage += clock64() - tk0;
 #endif
-    }
-    __syncthreads();
-    SEG_TICK(tk_b1);
-    if (j + 1 < h) {
-      // ---- row j+1's pre-accumulation (all warps, in place over the staged
-      // bm row), the reference's arrival order: upstream, centre, downstream
-      // source of row j ----
+      // the reference's arrival order for a cell of row j+1: upstream,
+      // centre, downstream source of row j. Row ends (scan positions 0, 1,
+      // w-2, w-1) miss a source or take a row-end quotient: selects (a
+      // missing term is not added: not + 0.0, so signed zeros stay the
+      // reference's); branch-free batches of 4 (clamped loads, guarded stores)
       const int pd = dir;
       const double E1l = s_k[d][2], E1h = s_k[d][3], E5l = s_k[d][4], E5h = s_k[d][5], E3l = s_k[d][6],
                    E3h = s_k[d][7];
-      // Interior positions [2, w-3] have all three sources and the interior
-      // quotients; the row ends (0, 1, w-2, w-1) miss a source or take a
-      // row-end quotient. One branch-free pass over all positions in batches
-      // of 4 (clamped loads, guarded stores): a missing source's term is not
-      // added (a select, not + 0.0, so signed zeros stay the reference's).
-      for (int i0 = tid; i0 < w; i0 += 4 * kSegT) {
+      auto pre_at = [&](int pos) {  // row j+1's pre at its scan position w-1-pos
+        const int t = pd == 1 ? pos : w - 1 - pos;  // column of row j at scan position pos
+        const double c1 = (t - pd == 0) ? E1l : (t - pd == w - 1 ? E1h : 1.0 / 16.0);
+        const double c5 = (t == 0) ? E5l : (t == w - 1 ? E5h : 5.0 / 16.0);
+        const double c3 = (t + pd == 0) ? E3l : (t + pd == w - 1 ? E3h : 3.0 / 16.0);
+        double x = raw[w - 1 - pos] * scale;  // row j+1 scans the other way
+        const double up = x + err[max(pos - 1, 0)] * c1;
+        x = pos >= 1 ? up : x;
+        x += err[pos] * c5;
+        const double dn = x + err[min(pos + 1, w - 1)] * c3;
+        return pos + 1 < w ? dn : x;
+      };
+      asm volatile("bar.sync 3, %0;" ::"r"(kSegT) : "memory");  // warp 0's chains are done
+      for (int i0 = t3; i0 < w; i0 += 4 * kT3) {
         double v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int pos = min(i0 + u * kSegT, w - 1);
-          const int t = pd == 1 ? pos : w - 1 - pos;  // column of row j at scan position pos
-          const double c1 = (t - pd == 0) ? E1l : (t - pd == w - 1 ? E1h : 1.0 / 16.0);
-          const double c5 = (t == 0) ? E5l : (t == w - 1 ? E5h : 5.0 / 16.0);
-          const double c3 = (t + pd == 0) ? E3l : (t + pd == w - 1 ? E3h : 3.0 / 16.0);
-          double x = nbuf[w - 1 - pos] * scale;  // row j+1 scans the other way
-          const double up = x + err[max(pos - 1, 0)] * c1;
-          x = pos >= 1 ? up : x;
-          x += err[pos] * c5;
-          const double dn = x + err[min(pos + 1, w - 1)] * c3;
-          x = pos + 1 < w ? dn : x;
-          v[u] = x;
-        }
+        for (int u = 0; u < 4; ++u) v[u] = pre_at(min(i0 + u * kT3, w - 1));
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          if (i0 + u * kSegT < w) nbuf[w - 1 - (i0 + u * kSegT)] = v[u];
+          if (i0 + u * kT3 < w) nbuf[w - 1 - (i0 + u * kT3)] = v[u];
         }
       }
-      SEG_TICK(tk_g0);
-      __syncthreads();
+      asm volatile("bar.sync 4, %0;" ::"r"(kSegT) : "memory");  // verification done: s_chg_hi
+      // a rewritten error at position p feeds positions p-1..p+1; lane l
+      // rewrote [qs_l, s_chg_hi[l]]. All 32 read at once, one ballot.
+      const int my_hi = s_chg_hi[lane];
+      unsigned int chg = __ballot_sync(0xffffffffu, my_hi >= 0);
+      while (chg) {
+        const int l = __ffs(chg) - 1;
+        chg &= chg - 1;
+        const int hi = __shfl_sync(0xffffffffu, my_hi, l);
+        const int lo = max(L.start(l) - 1, 0), top = min(hi + 1, w - 1);
+        for (int p = lo + t3; p <= top; p += kT3) nbuf[w - 1 - p] = pre_at(p);
+      }
     }
+    __syncthreads();
     SEG_TICK(tk_pre);
   }
 #ifdef GL_EXPERIMENT_ENV
@@ -1157,7 +1182,7 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
     }
   };
   const size_t smem = static_cast<size_t>(2) * w * sizeof(double);
-  const size_t smem_seg = (3 * static_cast<size_t>(((w + 1) & ~1) + 16)) * sizeof(double) +
+  const size_t smem_seg = (4 * static_cast<size_t>(((w + 1) & ~1) + 16)) * sizeof(double) +
                           3 * 4 * static_cast<size_t>((w + 31) / 32 + 2) + 64;
   if (smem_pipe <= 200 * 1024) {
     if (smem_pipe > 48 * 1024) attr(reinterpret_cast<const void*>(k_dither_pipe), smem_pipe);
