@@ -558,6 +558,12 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
 constexpr int kSegT = 128;     // threads (4 warps: warp 0 runs the chains; all warps the pre pass)
 constexpr int kSegWU = 64;     // warm-up pixels of lanes 1..31
 static_assert(kSegWU % 16 == 0, "warm-ups are whole 16-pixel groups");
+#ifndef GL_SEG_CHAIN_WARPS
+#define GL_SEG_CHAIN_WARPS 2
+#endif
+constexpr int kSegW = GL_SEG_CHAIN_WARPS;  // warps running segment chains (the others stage the next row)
+constexpr int kSegLanes = 32 * kSegW;      // segments per row at most
+static_assert(kSegW >= 1 && kSegW <= 2, "1 or 2 chain warps (4-warp CTA)");
 
 struct SegLayout {
   int P, F, S;  // lanes in use, lane 0's length, segment stride (odd)
@@ -565,7 +571,7 @@ struct SegLayout {
   int w_;
 };
 
-__host__ __device__ inline SegLayout seg_layout(int w) {
+__host__ __device__ inline SegLayout seg_layout(int w, int lanes) {
   SegLayout L{};
   L.w_ = w;
   if (w < 4 * kSegWU) {
@@ -574,7 +580,7 @@ __host__ __device__ inline SegLayout seg_layout(int w) {
     L.S = w;
     return L;
   }
-  int S = (w - kSegWU + 31) / 32;  // 32 lanes, lane 0 takes S + kSegWU (every lane runs ~S + kSegWU pixels)
+  int S = (w - kSegWU + lanes - 1) / lanes;  // lane 0 takes S + kSegWU (every lane runs ~S + kSegWU pixels)
   S |= 1;
   L.S = S;
   L.F = min(w, S + kSegWU);
@@ -645,7 +651,8 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
   unsigned int* sup0 = reinterpret_cast<unsigned int*>(segsh + 4 * WR);  // [2][SW] support bits, scan order
   unsigned int* ebits = sup0 + 2 * SW;  // [SW] row j's emission bits, scan order
   __shared__ int s_count;
-  __shared__ int s_chg_hi[32];  // row j: the last error a lane's verification reruns rewrote (-1: none)
+  __shared__ int s_chg_hi[kSegLanes];  // row j: the last error a lane's verification reruns rewrote (-1: none)
+  __shared__ int s_changed[kSegLanes];  // a verification round: the lane's rerun changed its segment end
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (*sum_invalid) {  // negative / non-finite plane: k_dither_pipe's sequential total takes it
     if (tid == 0) *done = 0;
@@ -661,7 +668,14 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
   }
   const double scale = budget / total;
   if (tid == 0) s_count = 0;
-  const SegLayout L = seg_layout(w);
+  // Two layouts: 32 * kSegW segments (shorter warm-up share per row) and
+  // 32 (longer segments). A row whose predecessor needed verification reruns
+  // on 2+ segments (a concentrated belief: steep tails converge slowly, and
+  // short segments turn one slow meeting into rounds) takes the 32-segment
+  // layout; the extra chain warp then has no segments and only keeps the
+  // barriers.
+  const SegLayout L_many = seg_layout(w, kSegLanes), L_few = seg_layout(w, 32);
+  __shared__ int s_many[2];  // row parity: this row takes L_many
   // per-direction constants of every row but the last (fs_wsum with a row
   // below; [0]: dir +1, [1]: dir -1): carry coefficients and the diffusion
   // quotients of the row-end sources. Computed once into shared memory (in
@@ -692,6 +706,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
     sup0[SW + w / 32 + 1] = 0u;
   }
   for (int i = tid; i < SW; i += kSegT) ebits[i] = 0u;
+  if (tid == 0) s_many[0] = 1;
   __syncthreads();
 #ifdef GL_EXPERIMENT_ENV
   long long tk_spec = 0, tk_ver = 0, tk_pre = 0, tk_b1 = 0, tk_stage = 0, tk_all = clock64(), tk0 = 0;
@@ -713,6 +728,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
     double* pre = buf0 + d * WR;            // row j's pre-accumulated work
     double* nbuf = buf0 + (d ^ 1) * WR;     // row j + 1's pre (built by warps 1..3 during row j)
     const bool nxt = j + 1 < h;
+    const SegLayout L = s_many[d] ? L_many : L_few;
     const unsigned int* sup = sup0 + d * SW;
     unsigned int* nsup = sup0 + (d ^ 1) * SW;
     const double c_first = last ? fs_carry_coef(start, j, w, h, dir) : s_k[d][0];
@@ -740,22 +756,26 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
         carry = e * (q == 0 ? c_first : c_mid);
       }
     };
-    if (warp == 0) {
+    if (warp < kSegW) {
+      const int sl = tid;  // this thread's segment
       if (last || L.P == 1) {
 #ifdef GL_EXPERIMENT_ENV
         ++n_exact;
 #endif
-        if (lane == 0) exact_row();
-        s_chg_hi[lane] = -1;
-        __syncwarp();
-        if (nxt) {  // the errors are final: warps 1..3 take the next row
+        if (tid == 0) {
+          exact_row();
+          s_many[d ^ 1] = 1;
+        }
+        s_chg_hi[sl] = -1;
+        asm volatile("bar.sync 5, %0;" ::"r"(kSegLanes) : "memory");
+        if (nxt) {  // the errors are final: the staging warps take the next row
           asm volatile("bar.arrive 3, %0;" ::"r"(kSegT) : "memory");
           asm volatile("bar.arrive 4, %0;" ::"r"(kSegT) : "memory");
         }
       } else {
-        const bool act = lane < L.P;
-        const int qs = L.start(lane), qe = L.start(lane + 1);
-        const int q0 = lane == 0 ? 0 : qs - kSegWU;  // F > kSegWU: warm-ups start inside the row
+        const bool act = sl < L.P;
+        const int qs = L.start(sl), qe = L.start(sl + 1);
+        const int q0 = sl == 0 ? 0 : qs - kSegWU;  // F > kSegWU: warm-ups start inside the row
         double carry = 0.0;  // the guess (exact for lane 0: the row's first pixel has no carry in)
         double wu = 0.0;
         const int n_grp = (L.S + kSegWU + 15) / 16;
@@ -790,9 +810,9 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
           if (tid == 0) { const long long t_ = clock64(); tk_g1 += t_ - tg0; tg0 = t_; }
 #endif
         }
-        __syncwarp();
-        // warps 1..3 start the next row's pass on these errors now; what the
-        // verification below rewrites they recompute after barrier 4
+        asm volatile("bar.sync 5, %0;" ::"r"(kSegLanes) : "memory");  // every chain's errors stored
+        // the staging warps start the next row's pass on these errors now;
+        // what the verification below rewrites they recompute after barrier 4
         if (nxt) asm volatile("bar.arrive 3, %0;" ::"r"(kSegT) : "memory");
         SEG_TICK(tk_spec);
         // ---- verification, all lanes at once. Lane l >= 1 is exact if its
@@ -802,9 +822,14 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
         // and emissions up to there. This assumes lane l-1's segment end is
         // final; a lane whose rerun reached its segment end without meeting
         // changed that end, and its successor reruns in another round. ----
-        bool todo = act && lane > 0, recheck = true;
+        bool todo = act && sl > 0, recheck = true;
         int chg_hi = -1;  // the last error this lane's reruns rewrote
-        while (__any_sync(0xffffffffu, todo)) {
+        for (;;) {
+          // any segment to check or rerun, over all chain warps
+          int any;
+          asm volatile("{ .reg .pred p, q; setp.ne.s32 q, %1, 0; bar.red.or.pred p, 5, %2, q; selp.s32 %0, 1, 0, p; }"
+                       : "=r"(any) : "r"(static_cast<int>(todo)), "r"(kSegLanes) : "memory");
+          if (!any) break;
           bool run = false;
           double cr = 0.0;
           if (todo) {
@@ -861,13 +886,18 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
             }
           }
           recheck = false;  // later rounds rerun unconditionally
-          const unsigned int ch = __ballot_sync(0xffffffffu, changed);
-          __syncwarp();
-          todo = act && lane > 0 && ((ch >> (lane - 1)) & 1u);
+          s_changed[sl] = changed;
+          asm volatile("bar.sync 5, %0;" ::"r"(kSegLanes) : "memory");
+          todo = act && sl > 0 && s_changed[sl - 1];
         }
-        s_chg_hi[lane] = chg_hi;
-        __syncwarp();
+        s_chg_hi[sl] = chg_hi;
+        asm volatile("bar.sync 5, %0;" ::"r"(kSegLanes) : "memory");  // emission bits and changes final
         if (nxt) asm volatile("bar.arrive 4, %0;" ::"r"(kSegT) : "memory");
+        if (warp == 0) {
+          int n_rerun = 0;
+#pragma unroll
+          for (int wv = 0; wv < kSegW; ++wv) n_rerun += __popc(__ballot_sync(0xffffffffu, s_chg_hi[32 * wv + lane] >= 0));
+          if (lane == 0) s_many[d ^ 1] = n_rerun < 2;
         // ---- the row's emissions in scan order: a warp scan over the
         // emission words (cleared for the next row) ----
         const int nw = (w + 31) >> 5;
@@ -897,6 +927,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
         }
         __syncwarp();
         if (lane == 0) s_count = c_base;
+        }
       }
       SEG_TICK(tk_ver);
     } else if (nxt) {
@@ -907,15 +938,15 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
       // errors the verification rewrote ----
       const double* brow = bm + static_cast<size_t>(j + 1) * w;
       const bool rev = dir == 1;  // row j + 1 scans right to left
-      const int t3 = tid - 32;    // 0..95
-      constexpr int kT3 = kSegT - 32;
+      const int t3 = tid - kSegLanes;  // the staging threads
+      constexpr int kT3 = kSegT - kSegLanes;
       for (int t = t3; t < w; t += kT3) {
         const unsigned int dst = static_cast<unsigned int>(__cvta_generic_to_shared(raw + (rev ? w - 1 - t : t)));
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(brow + t) : "memory");
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
       asm volatile("bar.sync 1, %0;" ::"r"(kT3) : "memory");
-      for (int wd = warp - 1; wd <= w / 32; wd += kSegT / 32 - 1) {
+      for (int wd = warp - kSegW; wd <= w / 32; wd += kSegT / 32 - kSegW) {
         const int qn = wd * 32 + lane;
         const unsigned int bits = __ballot_sync(0xffffffffu, qn < w && raw[qn] > 0.0);
         if (lane == 0) nsup[wd] = bits;
@@ -954,16 +985,19 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
         }
       }
       asm volatile("bar.sync 4, %0;" ::"r"(kSegT) : "memory");  // verification done: s_chg_hi
-      // a rewritten error at position p feeds positions p-1..p+1; lane l
-      // rewrote [qs_l, s_chg_hi[l]]. All 32 read at once, one ballot.
-      const int my_hi = s_chg_hi[lane];
-      unsigned int chg = __ballot_sync(0xffffffffu, my_hi >= 0);
-      while (chg) {
-        const int l = __ffs(chg) - 1;
-        chg &= chg - 1;
-        const int hi = __shfl_sync(0xffffffffu, my_hi, l);
-        const int lo = max(L.start(l) - 1, 0), top = min(hi + 1, w - 1);
-        for (int p = lo + t3; p <= top; p += kT3) nbuf[w - 1 - p] = pre_at(p);
+      // a rewritten error at position p feeds positions p-1..p+1; segment l
+      // rewrote [qs_l, s_chg_hi[l]]. 32 read at once, one ballot per word.
+#pragma unroll
+      for (int wv = 0; wv < kSegW; ++wv) {
+        const int my_hi = s_chg_hi[32 * wv + lane];
+        unsigned int chg = __ballot_sync(0xffffffffu, my_hi >= 0);
+        while (chg) {
+          const int l = __ffs(chg) - 1;
+          chg &= chg - 1;
+          const int hi = __shfl_sync(0xffffffffu, my_hi, l);
+          const int lo = max(L.start(32 * wv + l) - 1, 0), top = min(hi + 1, w - 1);
+          for (int p = lo + t3; p <= top; p += kT3) nbuf[w - 1 - p] = pre_at(p);
+        }
       }
     }
     __syncthreads();
