@@ -533,30 +533,33 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
 // chains started from different carries meet bitwise after ~45-60 pixels
 // (the difference shrinks by 7/16 per pixel until one rounding merges them,
 // and from then on the same state gives the same future — emissions
-// included). So every row is cut into segments run by the lanes of one warp
-// at once. Lane 0 runs [0, F) exactly from the row's first pixel; lane l >= 1
-// runs segment [s_l, s_l + S) but starts kSegWU pixels early with a guessed
-// carry 0 (a warm-up over the previous segment's tail that records
-// nothing). Segments are S pixels apart with S odd, so the lanes' shared-
-// memory accesses fall in distinct banks. Each lane works in 16-pixel
-// groups: values loaded up front, the chain run assuming no emission (one
-// DADD and one DMUL per pixel), the group replayed exactly by the lanes that
-// need it when any lane's group holds a supported v >= 0.5. Then: lane l is
-// exact iff its warm-up's last error equals, bit for bit, the error at that
-// pixel of an exact lane l-1 (the carries into the segment are then equal).
-// The exact lanes' emissions go out in scan order through a warp prefix
-// sum; from the first lane that fails, lane 0 reruns segments exactly from
-// the true carry until they meet the lanes' own errors, taking the true
-// emissions up to that pixel and the lane's after it. Every value and every
-// emission is the reference's. Rows whose lane lists overflow, the last row
-// (no row below: carry coefficient 1, no contraction) and narrow rows run
-// the exact sequential chain on lane 0. The next row's pre-accumulation runs
-// on all warps between rows, from the row's errors in shared memory.
+// included). So every row is cut into segments, one per lane of the chain
+// warps (up to 64). Segment 0 runs [0, F) exactly from the row's first
+// pixel; segment l >= 1 runs [s_l, s_l + S) but starts kSegWU pixels early
+// with a guessed carry 0 (a warm-up over the previous segment's tail that
+// records nothing). Segments are S pixels apart with S odd, so the lanes'
+// shared-memory accesses fall in distinct banks. Each lane works in
+// 16-pixel groups (seg_group): values loaded up front, the chain run assuming
+// no emission (one DADD and one DMUL per pixel), the group replayed exactly
+// by the lanes that need it when any lane's group holds a supported v >= 0.5.
+// Emissions are bits of a per-row mask. Then all segments are verified at
+// once: segment l is exact iff its warm-up's last error equals, bit for bit,
+// segment l-1's error before it; a failing segment reruns from that true
+// carry until its values meet its own stored chain (taking the rerun's errors
+// and emission bits up to the meeting pixel); a rerun that reaches its
+// segment end unmet changed what its successor was checked against, so the
+// successor reruns in another round. Every value and every emission is the
+// reference's. The row's cells go out in scan order by a warp scan over the
+// mask words. The last row (no row below: carry coefficient 1, no
+// contraction) and narrow rows run the exact sequential chain on one thread.
+// The other two warps stage the next row of the belief map (cp.async) while
+// the chains run, build its pre-accumulation while the row is verified, and
+// recompute the positions next to errors a rerun rewrote.
 #ifndef GL_FS_SEG
 #define GL_FS_SEG 1  // the segment-parallel sweep (0: the pipelined chain only)
 #endif
-constexpr int kSegT = 128;     // threads (4 warps: warp 0 runs the chains; all warps the pre pass)
-constexpr int kSegWU = 64;     // warm-up pixels of lanes 1..31
+constexpr int kSegT = 128;     // threads (4 warps: kSegW chain warps, the rest stage the next row)
+constexpr int kSegWU = 64;     // warm-up pixels of segments 1..
 static_assert(kSegWU % 16 == 0, "warm-ups are whole 16-pixel groups");
 #ifndef GL_SEG_CHAIN_WARPS
 #define GL_SEG_CHAIN_WARPS 2
