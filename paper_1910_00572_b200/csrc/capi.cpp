@@ -1840,7 +1840,8 @@ static void observe_impl(gl_context* ctx, gl_tensor* t, const int32_t* cells, in
     size_t off_mean = (off_L + sizeof(double) * nL + 255) & ~size_t(255);
     size_t off_reach = off_mean + 256;
     size_t off_dir = (off_reach + sizeof(double) * reach.size() + 255) & ~size_t(255);
-    size_t total = off_dir + sizeof(double) * dirs.size() + 256;
+    size_t off_sum = (off_dir + sizeof(double) * dirs.size() + 255) & ~size_t(255);
+    size_t total = off_sum + glb::seq_sum_scratch_bytes(nL) + 256;
     char* d = static_cast<char*>(ensure_misc(ctx, total));
     int* d_s = reinterpret_cast<int*>(d + off_s);
     double* d_L = reinterpret_cast<double*>(d + off_L);
@@ -1857,7 +1858,7 @@ static void observe_impl(gl_context* ctx, gl_tensor* t, const int32_t* cells, in
                             n, C, d_dir, ns, d_reach, params.weight_floor, d_L, d_kind);
     if (ctx->host_exp) finish_likelihoods_on_host(ctx, d_L, d_kind, nL, params.weight_floor);
     glb::launch_observe_apply(ctx, interior(t), t->w, t->h, t->c, shard ? t->c_begin : 0, C, d_s, n,
-                              d_L, d_mean);
+                              d_L, d_mean, d + off_sum);
     glb::launch_plane_max(ctx, interior(t), elems_of(t), &t->d_block->step.gmax_bits);
     if (shard) {
       CK(cudaGetLastError());

@@ -352,7 +352,7 @@ void launch_likelihoods(gl_context* ctx, const uint8_t* occ, const double* score
                         uint8_t* d_kind);
 void launch_observe_apply(gl_context* ctx, double* buf, int w, int h, int c_local,
                           int k_off, int c_total, const int* d_samples, int n,
-                          const double* d_L, double* d_mean);
+                          const double* d_L, double* d_mean, void* sum_scratch);  // seq_sum_scratch_bytes(n * c_total)
 void launch_observe_finalize(gl_context* ctx, StepState* st, BufState* buf);
 
 }  // namespace glb

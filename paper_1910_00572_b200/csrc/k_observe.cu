@@ -1281,10 +1281,10 @@ void launch_likelihoods(gl_context* ctx, const uint8_t* occ, const double* score
 
 void launch_observe_apply(gl_context* ctx, double* buf, int w, int h, int c_local,
                           int k_off, int c_total, const int* d_samples, int n,
-                          const double* d_L, double* d_mean) {
+                          const double* d_L, double* d_mean, void* sum_scratch) {
   // d_mean[0]: the likelihoods' sequential sum; d_mean[1]: scan-domain flag
   int* flag = reinterpret_cast<int*>(d_mean + 1);
-  launch_seq_sum(ctx, d_L, static_cast<size_t>(n) * c_total, d_mean, flag);
+  launch_seq_sum_big(ctx, d_L, static_cast<size_t>(n) * c_total, d_mean, flag, sum_scratch);
   launch_seq_sum_chain(ctx, d_L, static_cast<size_t>(n) * c_total, d_mean, flag);  // only if flagged
   const int total = n * c_local;
   k_observe_apply<<<(total + 127) / 128, 128, 0, ctx->stream>>>(

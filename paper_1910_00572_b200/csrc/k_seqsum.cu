@@ -922,13 +922,16 @@ void launch_seq_sum(gl_context* ctx, const double* x, size_t n, double* d_total,
   ctx->launches++;
 }
 
-bool seq_sum_fuses_argmax(size_t n) { return (n + kSumChunk - 1) / kSumChunk > 4; }
+// From two chunks on, the all-SM passes (chunk maps, crossing chunks' events)
+// beat one CTA's own segmented walk.
+constexpr size_t kBigMinChunks = 2;
+bool seq_sum_fuses_argmax(size_t n) { return (n + kSumChunk - 1) / kSumChunk >= kBigMinChunks; }
 
 void launch_seq_sum_big(gl_context* ctx, const double* x, size_t n, double* d_total, int* d_invalid,
                         void* scratch, double s0, void* d_argmax) {
   const size_t chunks = (n + kSumChunk - 1) / kSumChunk;
-  if (d_argmax && !seq_sum_fuses_argmax(n)) throw std::runtime_error("seq-sum: argmax fusion needs > 4 chunks");
-  if (chunks <= 4) {
+  if (d_argmax && !seq_sum_fuses_argmax(n)) throw std::runtime_error("seq-sum: argmax fusion needs 2+ chunks");
+  if (chunks < kBigMinChunks) {
     launch_seq_sum(ctx, x, n, d_total, d_invalid, s0);
     return;
   }

@@ -70,7 +70,7 @@ def test_argmax_tie_rule(ctx):
 
 @pytest.mark.parametrize("seed", [0, 1, 2])
 def test_argmax_fused_chunk_pass_ties(ctx, port, seed):
-    """Tensors above 4 x 8192 states take the argmax candidates in the exact
+    """Tensors of 2+ chunks (8192 states each) take the argmax candidates in the exact
     total's chunk pass (k_seqsum.cu k_chunk_sums): equal maxima planted in
     different chunks and inside one chunk, the lowest flat index must win,
     and the confidence stays the sequential total."""
