@@ -498,7 +498,22 @@ __device__ __forceinline__ double warp_tile(const CUtensorMap* tmap,
     if (scaled) {
       // rare: the source buffer carries a pending rescale (stored values
       // times sc are the reference's values), applied to the box in smem
-      for (int q = lane; q < G::B_ELEMS; q += 32) stage_ptr[q] = stage_ptr[q] * sc;
+      // (4 loads in flight at a time: few registers in the hot kernels)
+      constexpr int kPer = (G::B_ELEMS + 31) / 32;
+#pragma unroll 1
+      for (int i0 = 0; i0 < kPer; i0 += 4) {
+        double bx[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int q = lane + 32 * (i0 + i);
+          bx[i] = q < G::B_ELEMS ? stage_ptr[q] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int q = lane + 32 * (i0 + i);
+          if (q < G::B_ELEMS) stage_ptr[q] = bx[i] * sc;
+        }
+      }
       __syncwarp();
     }
     const double* Bb = stage_ptr + ((x0 - R - cs.sx - 1) & 1) + lane;
