@@ -233,6 +233,14 @@ void materialize(gl_context* ctx, gl_tensor* t) {
                           &t->d_block->buf[t->cur]);
 }
 
+inline void cpu_relax() {
+#if defined(__x86_64__) || defined(__i386__)
+  __builtin_ia32_pause();
+#else
+  std::this_thread::yield();
+#endif
+}
+
 gl_status read_status(gl_context* ctx, gl_tensor* t) {
   CK(cudaMemcpyAsync(&ctx->h_block->step, &t->d_block->step,
                      sizeof(glb::StepState), cudaMemcpyDeviceToHost,
@@ -1278,9 +1286,22 @@ gl_status gl_step(gl_context* ctx, gl_tensor* t, double u, double v, double w,
   st = guard([&] {
     gl_status s = GL_E_RUNTIME;
     if (mapped) {
+      // wait on the published word itself (the last CTA writes it after every
+      // other CTA's output is done; later work stays stream-ordered), with a
+      // stream query now and then so a failed launch cannot hang the caller
       DeviceGuard g(ctx->device);
-      CK(cudaStreamSynchronize(ctx->stream));
-      s = static_cast<gl_status>(*reinterpret_cast<volatile int*>(ctx->h_status));
+      volatile int* hs = reinterpret_cast<volatile int*>(ctx->h_status);
+      for (unsigned spins = 1; *hs == -1; ++spins) {
+        if ((spins & 1023u) == 0) {
+          const cudaError_t q = cudaStreamQuery(ctx->stream);
+          if (q != cudaErrorNotReady) {
+            CK(q);
+            break;
+          }
+        }
+        cpu_relax();
+      }
+      s = static_cast<gl_status>(*hs);
     }
     if (!mapped || (s != GL_OK && s != GL_E_EXTINGUISHED)) s = read_status(ctx, t);
     if (s == GL_E_EXTINGUISHED) {
