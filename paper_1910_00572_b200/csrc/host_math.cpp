@@ -3,6 +3,7 @@
 // reference evaluates it, so taps, motion vectors and likelihood tables are
 // bit-identical to the reference on the same host. Compiled with
 // -ffp-contract=off (no FMA contraction), like the reference build.
+#include <vector>
 #include <algorithm>
 #include <cctype>
 #include <cmath>
@@ -118,6 +119,23 @@ HostKernels build_kernels_host(double sigma_x, double sigma_y,
 // (dx, dy) in cells, with theta_t before the step's rotation is applied.
 void motion_table(double u, double v, int c_begin, int count, double theta_t,
                   double dtheta, double cell, double* out_xy) {
+  // The table depends only on its arguments; a stream of steps with an
+  // unchanged heading offset (translations) reuses the last one instead of
+  // 2 * count libm calls (~40 ns each). Per thread, whole tables only.
+  struct Memo {
+    double u, v, theta_t, dtheta, cell;
+    int c_begin = -1, count = 0;
+    std::vector<double> xy;
+  };
+  thread_local Memo memo;
+  const bool cacheable = count > 1;
+  if (cacheable && memo.count == count && memo.c_begin == c_begin && memo.u == u && memo.v == v &&
+      memo.theta_t == theta_t && memo.dtheta == dtheta && memo.cell == cell &&
+      std::signbit(memo.u) == std::signbit(u) && std::signbit(memo.v) == std::signbit(v) &&
+      std::signbit(memo.theta_t) == std::signbit(theta_t)) {
+    std::copy(memo.xy.begin(), memo.xy.end(), out_xy);
+    return;
+  }
   for (int q = 0; q < count; ++q) {
     const int k = c_begin + q;
     const double angle = k * dtheta + theta_t;
@@ -125,6 +143,16 @@ void motion_table(double u, double v, int c_begin, int count, double theta_t,
     const double s = std::sin(angle);
     out_xy[2 * q] = (c * u - s * v) / cell;
     out_xy[2 * q + 1] = (s * u + c * v) / cell;
+  }
+  if (cacheable) {
+    memo.u = u;
+    memo.v = v;
+    memo.theta_t = theta_t;
+    memo.dtheta = dtheta;
+    memo.cell = cell;
+    memo.c_begin = c_begin;
+    memo.count = count;
+    memo.xy.assign(out_xy, out_xy + 2 * static_cast<size_t>(count));
   }
 }
 
