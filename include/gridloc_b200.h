@@ -119,10 +119,11 @@ gl_status gl_context_set_host_exp(gl_context* ctx, int enable);
 gl_status gl_context_launch_count(gl_context* ctx, uint64_t* n);
 /* The context's cudaStream_t, as an opaque pointer (for NCCL / events). */
 gl_status gl_context_stream(gl_context* ctx, void** stream);
-/* Per-launch device timing of the step kernels: when enabled, every step
- * kernel is bracketed by CUDA events on the context stream; *_times
- * synchronises and returns the summed duration and count since the last
- * call (then resets). */
+/* Per-launch device timing of the step kernels: enable = n >= 1 brackets
+ * every n-th step kernel with CUDA events on the context stream (an event
+ * pair costs ~5 us of host time, which short steps feel: sample them), 0
+ * turns it off; *_times synchronises and returns the summed duration and
+ * count of the timed kernels since the last call (then resets). */
 gl_status gl_context_time_steps(gl_context* ctx, int enable);
 gl_status gl_context_step_times(gl_context* ctx, double* total_ms, int* count);
 /* Region timing on the context stream: record marker i (0..15), then read

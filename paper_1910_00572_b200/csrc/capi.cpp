@@ -416,7 +416,10 @@ gl_status gl_context_time_steps(gl_context* ctx, int enable) {
       ctx->tev.resize(2 * gl_context::kTimers);
       for (auto& e : ctx->tev) CK(cudaEventCreate(&e));
     }
+    need(enable >= 0, "enable must be 0 (off) or a step stride >= 1");
     ctx->timing = enable != 0;
+    ctx->tstride = enable > 0 ? enable : 1;
+    ctx->tstep = 0;
     ctx->tcount = 0;
   });
 }
@@ -1224,7 +1227,8 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
   // per-step device time: cudaEventRecord costs ~2.6 us of host time each
   // (measured, tools/probe_launch_params.cu), so the begin/end pair is only
   // recorded when asked for (gl_context_set_step_timing, gl_context_time_steps)
-  const int tslot = (ctx->timing && ctx->tcount < gl_context::kTimers) ? ctx->tcount++ : -1;
+  const bool sampled = ctx->timing && (ctx->tstep++ % static_cast<unsigned>(ctx->tstride)) == 0;
+  const int tslot = (sampled && ctx->tcount < gl_context::kTimers) ? ctx->tcount++ : -1;
   const bool events = tslot >= 0 || ctx->step_events;
   if (events) CK(cudaEventRecord(tslot >= 0 ? ctx->tev[2 * tslot] : ctx->ev_begin, ctx->stream));
   if (fused) {

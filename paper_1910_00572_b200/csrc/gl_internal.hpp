@@ -123,6 +123,8 @@ struct gl_context {
   bool step_events = false;  // begin/end events around every step (t_motion)
   std::vector<cudaEvent_t> tev;  // 2 * kTimers
   int tcount = 0;
+  int tstride = 1;     // time every tstride-th step
+  unsigned tstep = 0;  // steps since timing was enabled
   cudaEvent_t ev_begin_last = nullptr, ev_end_last = nullptr;
   cudaEvent_t marks[16] = {};
 };

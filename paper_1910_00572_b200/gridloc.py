@@ -218,9 +218,10 @@ class Context:
         check(self.lib.gl_context_marks_ms(self.h, i, j, C.byref(ms)))
         return ms.value
 
-    def time_steps(self, enable: bool):
-        """Bracket every step kernel with CUDA events on the context stream."""
-        check(self.lib.gl_context_time_steps(self.h, int(enable)))
+    def time_steps(self, enable, stride: int = 1):
+        """Bracket every `stride`-th step kernel with CUDA events on the
+        context stream (enable False: off)."""
+        check(self.lib.gl_context_time_steps(self.h, max(1, int(stride)) if enable else 0))
 
     def step_times(self):
         """(total ms, count) of the timed step kernels since the last call."""
