@@ -12,6 +12,7 @@
 #include <cstring>
 #include <deque>
 #include <functional>
+#include <chrono>
 #include <thread>
 #include <fstream>
 #include <memory>
@@ -1113,9 +1114,30 @@ gl_status gl_tensor_device_ptr(gl_context* ctx, gl_tensor* t, double** dptr) {
 }
 
 // ----------------------------------------------------------------- step
+#ifdef GL_EXPERIMENT_ENV
+// host-time sections of enqueue_step (experiment builds; GL_DEBUG_ENQUEUE=1
+// prints the per-call means at exit)
+struct EnqProf {
+  double ns[8] = {};
+  long n = 0;
+  ~EnqProf() {
+    if (n && getenv("GL_DEBUG_ENQUEUE"))
+      fprintf(stderr, "enqueue_step host ns/call: checks+guard %.0f | kernels %.0f | fused+tmap %.0f | motion %.0f | launch %.0f | tail %.0f (n=%ld)\n",
+              ns[0] / n, ns[1] / n, ns[2] / n, ns[3] / n, ns[4] / n, ns[5] / n, n);
+  }
+};
+static EnqProf g_enq;
+#define ENQ_T(i) do { const auto t_ = std::chrono::steady_clock::now(); g_enq.ns[i] += std::chrono::duration<double, std::nano>(t_ - enq_t0).count(); enq_t0 = t_; } while (0)
+#else
+#define ENQ_T(i) do { } while (0)
+#endif
 static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
                          double w, const gl_map* map, const gl_kernels* kernels,
                          const gl_activation* act, bool publish = false) {
+#ifdef GL_EXPERIMENT_ENV
+  auto enq_t0 = std::chrono::steady_clock::now();
+  ++g_enq.n;
+#endif
   need(ctx && t && map && kernels && act, "null argument");
   need(map->w == t->w && map->h == t->h, "map and tensor sizes differ");
   need(act->w == t->w && act->h == t->h && act->channels == t->c_total,
@@ -1123,8 +1145,10 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
   need(kernels->info.separable || kernels->info.channels >= t->c,
        "kernel set has fewer channels than the tensor");
   DeviceGuard g(ctx->device);
+  ENQ_T(0);
   auto* kk = const_cast<gl_kernels*>(kernels);
   upload_kernels(kk, ctx->device);
+  ENQ_T(1);
 
   glb::StepArgs a{};
   const int src = t->cur, dst = 1 - t->cur;
@@ -1186,6 +1210,7 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
   if (ctx->path == GL_PATH_FUSED && !fused) {
     fail(GL_E_INVALID, "fused path requested but unsupported for this kernel set/grid");
   }
+  ENQ_T(2);
   // motion vectors (host libm): carried in the launch parameters on the
   // fused path, otherwise uploaded through the pinned ring
   thread_local std::vector<double> hm;
@@ -1227,6 +1252,7 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
   // per-step device time: cudaEventRecord costs ~2.6 us of host time each
   // (measured, tools/probe_launch_params.cu), so the begin/end pair is only
   // recorded when asked for (gl_context_set_step_timing, gl_context_time_steps)
+  ENQ_T(3);
   const bool sampled = ctx->timing && (ctx->tstep++ % static_cast<unsigned>(ctx->tstride)) == 0;
   const int tslot = (sampled && ctx->tcount < gl_context::kTimers) ? ctx->tcount++ : -1;
   const bool events = tslot >= 0 || ctx->step_events;
@@ -1237,6 +1263,7 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
     const double one = 1.0;
     glb::launch_fused_step(ctx, a, tm, r > 0 ? kernels->sep.data() : &one, r, ang,
                            t->clean[src] && ctx->allow_fast);
+    ENQ_T(4);
   } else {
     const size_t n = elems_of(t);
     ensure_scratch(ctx, n);
@@ -1271,6 +1298,14 @@ static void enqueue_step(gl_context* ctx, gl_tensor* t, double u, double v,
   t->clean[dst] = t->clean[src];  // clean in -> clean out (non-negative weights)
   t->cur = dst;
   t->theta_t = t->theta_t + w;  // belief_tensor.cpp:478
+  ENQ_T(5);
+#ifdef GL_EXPERIMENT_ENV
+  if (g_enq.n % 1000 == 0 && getenv("GL_DEBUG_ENQUEUE")) {
+    const long n = g_enq.n;
+    fprintf(stderr, "enqueue_step host ns/call: checks+guard %.0f | kernels %.0f | fused+tmap %.0f | motion %.0f | launch %.0f | tail %.0f (n=%ld)\n",
+            g_enq.ns[0] / n, g_enq.ns[1] / n, g_enq.ns[2] / n, g_enq.ns[3] / n, g_enq.ns[4] / n, g_enq.ns[5] / n, n);
+  }
+#endif
 }
 
 gl_status gl_step(gl_context* ctx, gl_tensor* t, double u, double v, double w,

@@ -7,5 +7,5 @@ for v in "$@"; do
   name=${v%%:*}; flags=${v#*:}
   mkdir -p ../../build/variants/$name
   make -s -j8 OUT=../../build/variants/$name/libgridloc_b200.so OBJDIR=../../build/variants/$name/obj \
-       EXTRA_NVFLAGS="-DGL_EXPERIMENT_ENV $flags"
+       EXTRA_NVFLAGS="-DGL_EXPERIMENT_ENV $flags" EXTRA_CXXFLAGS="-DGL_EXPERIMENT_ENV"
 done
