@@ -42,6 +42,11 @@ CASES = {
     "many_crossings_per_chunk": lambda r: 2.0 ** np.linspace(-1070, 10, 400_000) * r.random(400_000),
     "crossings_and_ties": lambda r: np.concatenate([2.0 ** np.linspace(-60, 0, 30_000) * r.random(30_000),
                                                     r.integers(0, 4, 30_000) * 2.0 ** -54]),
+    # a binade crossing in every one of ~600 chunks: more crossing chunks
+    # than the all-SM event pass has slots (512), so the walk's own pass
+    # takes the rest
+    "crossing_chunks_beyond_pool": lambda r: 2.0 ** (-1000.0 + np.arange(600 * 8192) / 8192.0)
+    * (0.5 + 0.5 * r.random(600 * 8192)),
     "plane_1024sq": lambda r: np.where(r.random(1 << 20) < 0.16, 0.0, r.random(1 << 20) ** 3),
 }
 
