@@ -608,10 +608,13 @@ def run_batch(args, cfg, world, rank, local):
     n_e2e = max(1, min(args.steps, args.e2e_steps // 4))
     dist_barrier(world)
     t0 = time.perf_counter()
+    by_ctx = {}
+    for ctx, m, ks, act, t in robots:
+        by_ctx.setdefault(id(ctx), (ctx, []))[1].append(t)
     for _ in range(n_e2e):
         batch_step()
-        for ctx, m, ks, act, t in robots:
-            g.tensor_status(t)
+        for ctx, ts in by_ctx.values():  # every robot's status, one round trip per context
+            g.tensors_status(ts, ctx)
     e2e_s = dist_max(time.perf_counter() - t0, world, "ours")
     e2e = world * n_e2e / e2e_s
     bytes_batch = B * algo_bytes(W, H, C)
@@ -627,7 +630,8 @@ def run_batch(args, cfg, world, rank, local):
         "parallelism": f"{B} independent tensors per GPU on {len(ctxs)} streams",
         "timing": "host wall clock around K batch steps with device syncs",
         "e2e": {"value": e2e, "unit": "batch-Hz", "h2d_bytes_per_step": B * 16 * C, "d2h_bytes_per_step": B * 16,
-                "how": f"{n_e2e} batch steps: {B} step_async calls, then every robot's status read back"},
+                "how": f"{n_e2e} batch steps: {B} step_async calls, then every robot's status read back "
+                       f"(gl_tensors_status, one round trip per context)"},
         "roofline": {"bound": "hbm", "achieved": bytes_batch * value / world / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": bytes_batch * value / world / 1e9 / peak, "traffic": None, "peak_source": peak_src,
                      "bytes_per_launch": algo_bytes(W, H, C), "note": "aggregate over the batch's launches"},

@@ -244,6 +244,11 @@ gl_status gl_step_async(gl_context* ctx, gl_tensor* t, double u, double v,
                         double w, const gl_map* map, const gl_kernels* kernels,
                         const gl_activation* act);
 gl_status gl_tensor_status(gl_context* ctx, gl_tensor* t);
+/* The latest step status of n tensors stepped on this context (its stream
+ * orders the read after their steps), in one gather launch, one copy and
+ * one sync instead of n: statuses[i] = GL_OK or GL_E_EXTINGUISHED; returns
+ * GL_E_EXTINGUISHED if any is. (A batch of robots: one call per context.) */
+gl_status gl_tensors_status(gl_context* ctx, gl_tensor* const* ts, int n, int* statuses);
 /* ---- theta-slab shards ----------------------------------
  * A shard holds global channels [c_begin, c_end) of a c_total-channel belief,
  * stored with `halo` neighbour planes per side: storage plane q is channel

@@ -15,7 +15,7 @@ fallback. ``load_native()`` maps it eagerly.
 """
 from . import _lib
 from .gridloc import *  # noqa: E402,F401,F403
-from .gridloc import tensor_hash_host, tensor_status  # noqa: E402,F401
+from .gridloc import tensor_hash_host, tensor_status, tensors_status  # noqa: E402,F401
 
 __version__ = "0.2.0"
 

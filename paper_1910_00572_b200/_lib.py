@@ -97,6 +97,7 @@ SIGNATURES = {
     "gl_context_launch_count": [_vp, C.POINTER(C.c_uint64)],
     "gl_context_stream": [_vp, _pvp],
     "gl_context_time_steps": [_vp, C.c_int],
+    "gl_tensors_status": [_vp, C.POINTER(_vp), C.c_int, C.POINTER(C.c_int)],
     "gl_context_step_times": [_vp, _dp, _ip],
     "gl_context_mark": [_vp, C.c_int],
     "gl_context_marks_ms": [_vp, C.c_int, C.c_int, _dp],

@@ -1503,6 +1503,36 @@ gl_status gl_tensor_status(gl_context* ctx, gl_tensor* t) {
   });
 }
 
+void* ensure_host_misc(gl_context* ctx, size_t bytes);  // below
+
+gl_status gl_tensors_status(gl_context* ctx, gl_tensor* const* ts, int n, int* statuses) {
+  return guard([&] {
+    need(ctx && (n == 0 || (ts && statuses)) && n >= 0, "null argument");
+    DeviceGuard g(ctx->device);
+    if (n == 0) return;
+    // one gather kernel per 64 tensors into device scratch, one copy back, one sync
+    int* d_out = static_cast<int*>(ensure_misc(ctx, sizeof(int) * static_cast<size_t>(n) + 64));
+    int* h_out = static_cast<int*>(ensure_host_misc(ctx, sizeof(int) * static_cast<size_t>(n) + 64));
+    for (int i0 = 0; i0 < n; i0 += glb::kStatusGather) {
+      glb::StatusPtrs ptrs{};
+      ptrs.n = std::min(glb::kStatusGather, n - i0);
+      for (int i = 0; i < ptrs.n; ++i) {
+        need(ts[i0 + i] != nullptr, "null tensor");
+        ptrs.p[i] = &ts[i0 + i]->d_block->step.status;
+      }
+      glb::launch_gather_status(ctx, ptrs, d_out + i0);
+    }
+    CK(cudaMemcpyAsync(h_out, d_out, sizeof(int) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    bool ext = false;
+    for (int i = 0; i < n; ++i) {
+      statuses[i] = h_out[i];
+      ext = ext || h_out[i] == GL_E_EXTINGUISHED;
+    }
+    if (ext) fail(GL_E_EXTINGUISHED, "a belief tensor extinguished: no positive mass after step");
+  });
+}
+
 gl_status gl_apply_motion(gl_context* ctx, gl_tensor* t, double u, double v,
                           double w) {
   return guard([&] {

@@ -262,6 +262,13 @@ void launch_argmax(gl_context* ctx, const double* buf, size_t n,
                    void* d_scratch, size_t scratch_bytes, void* d_out);
 // order-independent hash of buf[0..n) as the elements p0 .. p0+n-1 of a
 // larger tensor (shard hashes add up to the whole tensor's)
+// gl_tensors_status: gather up to kStatusGather tensors' step status words
+constexpr int kStatusGather = 64;
+struct StatusPtrs {
+  const int* p[kStatusGather];
+  int n;
+};
+void launch_gather_status(gl_context* ctx, const StatusPtrs& ptrs, int* d_out);
 void launch_hash(gl_context* ctx, const double* buf, size_t n,
                  unsigned long long* d_out, unsigned long long p0);
 void launch_plane_max(gl_context* ctx, const double* buf, size_t n,

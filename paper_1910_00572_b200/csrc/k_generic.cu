@@ -727,6 +727,16 @@ void launch_argmax(gl_context* ctx, const double* buf, size_t n,
   ctx->launches += 2;
 }
 
+__global__ void k_gather_status(StatusPtrs ptrs, int* __restrict__ out) {
+  const int i = threadIdx.x;
+  if (i < ptrs.n) out[i] = *ptrs.p[i];
+}
+
+void launch_gather_status(gl_context* ctx, const StatusPtrs& ptrs, int* d_out) {
+  k_gather_status<<<1, kStatusGather, 0, ctx->stream>>>(ptrs, d_out);
+  ctx->launches++;
+}
+
 void launch_hash(gl_context* ctx, const double* buf, size_t n,
                  unsigned long long* d_out, unsigned long long p0) {
   cudaMemsetAsync(d_out, 0, sizeof(unsigned long long), ctx->stream);

@@ -576,6 +576,19 @@ def tensor_status(tensor: BeliefTensor):
     check(tensor.ctx.lib.gl_tensor_status(tensor.ctx.h, tensor.h))
 
 
+def tensors_status(tensors, ctx=None):
+    """The latest step status of tensors stepped on one context, read in one
+    round trip (gl_tensors_status); raises BeliefExtinguishedError if any is
+    extinguished."""
+    tensors = list(tensors)
+    if not tensors:
+        return
+    ctx = _ctx(ctx) if ctx is not None else tensors[0].ctx
+    arr = (C.c_void_p * len(tensors))(*[t.h for t in tensors])
+    out = (C.c_int * len(tensors))()
+    check(ctx.lib.gl_tensors_status(ctx.h, C.cast(arr, C.POINTER(C.c_void_p)), len(tensors), out))
+
+
 def apply_motion(tensor: BeliefTensor, u: OdometryDelta):
     """belief_tensor.cpp:340-352."""
     check(tensor.ctx.lib.gl_apply_motion(tensor.ctx.h, tensor.h, u.u, u.v, u.w))

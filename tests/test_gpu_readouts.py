@@ -235,3 +235,21 @@ def test_observation_update_matches(ctx, port, ref):
     before = t.values()
     g.observation_update(t, g.SampleSet(np.zeros((0, 2), np.int32)), g.LidarScan(a, r, 8.0), m, f)
     assert_bitwise(t.values(), before, "no-op")
+
+
+def test_tensors_status_batch(ctx):
+    """gl_tensors_status: many tensors' latest step status in one round trip;
+    an extinguished one raises like gl_tensor_status."""
+    import math
+    occ = make_floorplan(40, 30, seed=3)
+    m = g.OccupancyMap(40, 30, 0.1, occ, ctx=ctx)
+    ks = g.build_kernels(g.MotionNoise(), 8, 0.1, 2 * math.pi / 8)
+    act = g.make_activation(m, ks, 8, ctx)
+    ts = [g.init_uniform(m, 8, ctx) for _ in range(70)]  # > 64: two gather launches
+    for t in ts:
+        g.step_async(t, g.OdometryDelta(0.1, 0.0, 0.0), m, ks, act, ctx)
+    g.tensors_status(ts, ctx)
+    ts[67].set_values(np.zeros((8, 30, 40)))
+    g.step_async(ts[67], g.OdometryDelta(0.1, 0.0, 0.0), m, ks, act, ctx)
+    with pytest.raises(g.BeliefExtinguishedError):
+        g.tensors_status(ts, ctx)

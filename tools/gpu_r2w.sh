@@ -1,8 +1,3 @@
 #!/bin/bash
-timeout 900 python -m pytest -q -x tests/test_gpu_dither_seg.py tests/test_gpu_readouts.py tests/test_gpu_dither_wide.py 2>&1 | tail -1
-for r in 1 2; do
-for v in nolag product; do
-  if [ $v = product ]; then unset GRIDLOC_B200_LIB; else export GRIDLOC_B200_LIB=$PWD/build/variants/$v/libgridloc_b200.so; fi
-  timeout 300 python tools/ab_dither.py 1024 40 2>&1 | tail -1
-
-done; done
+timeout 900 python -m pytest -q -x tests/test_gpu_readouts.py tests/test_gpu_batch_concurrency.py 2>&1 | tail -1
+timeout 600 python bench.py --config c5 --steps 1000 --no-cpu-baseline --no-extras 2>&1 | tail -1 | python -c "import json,sys;d=json.loads(sys.stdin.read());print('c5',d['value'],d['e2e']['value'],d['roofline']['frac'],d['clocks']['sm_mhz'])"
