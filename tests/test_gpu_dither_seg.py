@@ -74,3 +74,22 @@ def test_segment_sweep_on_a_floorplan_belief(ctx, port):
         cells, mass = port.dither(bm, budget)
         assert s.source_mass == mass
         assert np.array_equal(s.cells, cells)
+
+
+def test_segment_sweep_randomised(ctx, port):
+    """300 random (width, height, plane kind, budget) draws incl. exact-zero
+    rows and widths past the shared-memory limit of the segment sweep (its
+    fallbacks); tools/stress_dither.py runs the same draw at 3000 cases."""
+    rng = np.random.default_rng(12345)
+    kinds = ["sparse", "dense", "blobs", "walls", "spikes", "tails"]
+    for i in range(300):
+        w = int(rng.integers(200, 7000)) if rng.random() < 0.3 else int(rng.integers(200, 1500))
+        h = int(rng.integers(1, 60))
+        budget = int(rng.choice([16, 512, 4096, 100000]))
+        bm = _plane(kinds[i % len(kinds)], w, h, int(rng.integers(1 << 30)))
+        if rng.random() < 0.2:
+            bm[rng.integers(0, h, 3), :] = 0.0
+        s = g.dither_samples(bm, budget, ctx)
+        cells, mass = port.dither(bm, budget)
+        assert s.source_mass == mass, (i, w, h, budget)
+        assert np.array_equal(s.cells, cells), (i, w, h, budget, len(s.cells), len(cells))
