@@ -781,37 +781,82 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
         const int q0 = sl == 0 ? 0 : qs - kSegWU;  // F > kSegWU: warm-ups start inside the row
         double carry = 0.0;  // the guess (exact for lane 0: the row's first pixel has no carry in)
         double wu = 0.0;
-        const int n_grp = (L.S + kSegWU + 15) / 16;
-        for (int gi = 0; gi < n_grp; ++gi) {
+        // the warp's group count (lanes past their segment: no pixels)
+        const int my_grp = act ? (qe - q0 + 15) / 16 : 0;
+        const int n_grp = __reduce_max_sync(0xffffffffu, my_grp);
+        // One group: the chain on values already in registers, then the NEXT
+        // group's loads issued before the replay vote (the vote and its
+        // branch would otherwise hold them back), double-buffered by hand.
+        auto group = [&](const double (&p)[16], double (&pn)[16], int gi) {
 #ifdef GL_EXPERIMENT_ENV
           long long tg0 = clock64();
 #endif
           const int base = q0 + 16 * gi;
           const int valid = act ? max(0, min(16, qe - base)) : 0;
-          if (!__any_sync(0xffffffffu, valid > 0)) break;
-          double v[16];
-          unsigned int emask;
-          carry = seg_group(pre + (valid > 0 ? base : 0), seg_sup_bits(sup, base, valid), base == 0, carry, c_first,
-                            c_mid, v, emask);
+          const unsigned int sb = seg_sup_bits(sup, base, valid);
+          const bool first = base == 0;  // lane 0's first group: pixel 0 has no carry in, coefficient c_first
+          const double c0 = carry;
+          double c = c0, v[16];
+          unsigned int big = 0;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const double vk = (k == 0 && first) ? p[0] : p[k] + c;
+            v[k] = vk;
+            asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(vk), "d"((k == 0 && first) ? c_first : c_mid));
+            big |= __double2hiint(vk) >= 0x3FE00000 ? (1u << k) : 0u;
+          }
+          {
+            const int nbase = base + 16;
+            const int nvalid = act ? max(0, min(16, qe - nbase)) : 0;
+            const double* pb = pre + (nvalid > 0 ? nbase : 0);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) pn[k] = pb[k];  // past valid: padding / other lanes' values, masked
+          }
+          unsigned int emask = 0u;
+          const bool need = (big & sb) != 0u;
+          if (__any_sync(0xffffffffu, need)) {
+            if (need) {  // the exact sweep of this group
+              c = c0;
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                const double vk = (k == 0 && first) ? p[0] : p[k] + c;
+                const bool em = vk >= 0.5 && ((sb >> k) & 1u);
+                const double e = em ? vk - 1.0 : vk;
+                emask |= static_cast<unsigned int>(em) << k;
+                v[k] = e;
+                asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(e), "d"((k == 0 && first) ? c_first : c_mid));
+              }
+            }
+          }
+          carry = c;
           // own-segment errors and emission bits, the warm-up's last error
           // (groups never straddle a segment start: kSegWU is a multiple of 16)
           const int own = base - qs;  // < 0: a warm-up group
-          if (own >= 0) {
-            double* eb = err + (valid > 0 ? base : 0);
+          double* eb = err + (valid > 0 ? base : 0);
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              if (k < valid) eb[k] = v[k];
-            }
-            if (emask) {  // neighbouring lanes share boundary words
-              const int sh = base & 31;
-              atomicOr(&ebits[base >> 5], emask << sh);
-              if (sh > 16) atomicOr(&ebits[(base >> 5) + 1], emask >> (32 - sh));
-            }
+          for (int k = 0; k < 16; ++k) {
+            if (own >= 0 && k < valid) eb[k] = v[k];
+          }
+          if (own >= 0 && emask) {  // neighbouring lanes share boundary words
+            const int sh = base & 31;
+            atomicOr(&ebits[base >> 5], emask << sh);
+            if (sh > 16) atomicOr(&ebits[(base >> 5) + 1], emask >> (32 - sh));
           }
           if (own == -16) wu = v[15];
 #ifdef GL_EXPERIMENT_ENV
-          if (tid == 0) { const long long t_ = clock64(); tk_g1 += t_ - tg0; tg0 = t_; }
+          if (tid == 0) { const long long t_ = clock64(); tk_g1 += t_ - tg0; }
 #endif
+        };
+        double pa[16], pb2[16];
+        {
+          const int valid0 = act ? max(0, min(16, qe - q0)) : 0;
+          const double* pb = pre + (valid0 > 0 ? q0 : 0);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) pa[k] = pb[k];
+        }
+        for (int gi = 0; gi < n_grp; gi += 2) {
+          group(pa, pb2, gi);
+          if (gi + 1 < n_grp) group(pb2, pa, gi + 1);
         }
         asm volatile("bar.sync 5, %0;" ::"r"(kSegLanes) : "memory");  // every chain's errors stored
         // the staging warps start the next row's pass on these errors now;

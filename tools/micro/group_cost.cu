@@ -47,6 +47,20 @@ __global__ void groups(const double* __restrict__ pre_g, const unsigned* __restr
     }
     if (F == 22) {
       bigall |= big & sb;
+    } else if (F == 23) {  // replay body executed by every lane, results selected by need (no inner branch)
+      const bool need = (big & sb) != 0u;
+      if (__any_sync(0xffffffffu, need)) {
+        double cc = carry;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const double vk = p[k] + cc;
+          const bool em = vk >= 0.5 && ((sb >> k) & 1u);
+          const double e = em ? vk - 1.0 : vk;
+          v[k] = need ? e : v[k];
+          asm("mul.rn.f64 %0, %1, %2;" : "=d"(cc) : "d"(e), "d"(cm));
+        }
+        c = need ? cc : c;
+      }
     } else if (F >= 2) {
       const bool need = (big & sb) != 0u;
       if (__any_sync(0xffffffffu, need)) {
@@ -87,6 +101,65 @@ __global__ void groups(const double* __restrict__ pre_g, const unsigned* __restr
   if (lane == 0) *clk = t1 - t0;
 }
 
+
+// level 24: level 21 (vote + replay branch, no sup loads) with the next
+// group's values loaded before the vote, manually double-buffered (no copies)
+__global__ void groups_pf(const double* __restrict__ pre_g, double* __restrict__ err_g, int n_grp, long long* clk,
+                          double cm) {
+  __shared__ double pre[2560];
+  __shared__ double err[2560];
+  const int lane = threadIdx.x;
+  for (int i = lane; i < 2560; i += 32) pre[i] = pre_g[i];
+  __syncwarp();
+  double carry = 0.0;
+  const int q0 = lane * 31 % 2048;
+  const unsigned sb = 0xffffu;
+  double pa[16], pb[16], v[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) pa[k] = pre[q0 + k];
+  auto step = [&](const double (&p)[16], double (&pn)[16], int g) {
+    const int base = q0 + 16 * (g % 5);
+    double c = carry;
+    unsigned big = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const double vk = p[k] + c;
+      v[k] = vk;
+      asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(vk), "d"(cm));
+      big |= __double2hiint(vk) >= 0x3FE00000 ? (1u << k) : 0u;
+    }
+    const int nb = q0 + 16 * ((g + 1) % 5);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) pn[k] = pre[nb + k];  // the next group's values, before the vote
+    const bool need = (big & sb) != 0u;
+    if (__any_sync(0xffffffffu, need)) {
+      if (need) {
+        c = carry;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const double vk = p[k] + c;
+          const bool em = vk >= 0.5 && ((sb >> k) & 1u);
+          const double e = em ? vk - 1.0 : vk;
+          v[k] = e;
+          asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(e), "d"(cm));
+        }
+      }
+    }
+    carry = c;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) err[base + k] = v[k];
+  };
+  const long long t0 = clock64();
+  for (int g = 0; g < n_grp; g += 2) {
+    step(pa, pb, g);
+    step(pb, pa, g + 1);
+  }
+  const long long t1 = clock64();
+  __syncwarp();
+  for (int i = lane; i < 2560; i += 32) err_g[i] = err[i];
+  if (lane == 0) *clk = t1 - t0;
+}
+
 template <int F>
 void run(const double* pre, const unsigned* sup, double* err, long long* clk, int n) {
   groups<F><<<1, 32>>>(pre, sup, err, n, clk, 7.0 / 16.0, 7.0 / 16.0);
@@ -114,6 +187,13 @@ int main() {
     run<5>(pre, sup, err, clk, n);
     run<21>(pre, sup, err, clk, n);
     run<22>(pre, sup, err, clk, n);
+    run<23>(pre, sup, err, clk, n);
+    {
+      groups_pf<<<1, 32>>>(pre, err, n, clk, 7.0 / 16.0);
+      long long h;
+      cudaMemcpy(&h, clk, 8, cudaMemcpyDeviceToHost);
+      printf("level 24 (21 + next loads before the vote): %.1f cycles per group\n", h / (double)n);
+    }
   }
   return 0;
 }
