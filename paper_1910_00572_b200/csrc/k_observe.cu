@@ -778,9 +778,21 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
       } else {
         const bool act = sl < L.P;
         const int qs = L.start(sl), qe = L.start(sl + 1);
-        const int q0 = sl == 0 ? 0 : qs - kSegWU;  // F > kSegWU: warm-ups start inside the row
-        double carry = 0.0;  // the guess (exact for lane 0: the row's first pixel has no carry in)
+        // segment 0 takes the row's first pixel here (no carry in, its own
+        // carry coefficient) and its groups start at pixel 1, so no group
+        // needs a first-pixel case; the others start kSegWU pixels early
+        // (F > kSegWU: inside the row) from the guessed carry 0
+        const int q0 = sl == 0 ? 1 : qs - kSegWU;
+        double carry = 0.0;
         double wu = 0.0;
+        if (sl == 0) {
+          const double v0 = pre[0];
+          const bool em0 = v0 >= 0.5 && (sup[0] & 1u);
+          const double e0 = em0 ? v0 - 1.0 : v0;
+          err[0] = e0;
+          if (em0) atomicOr(&ebits[0], 1u);
+          carry = e0 * c_first;
+        }
         // the warp's group count (lanes past their segment: no pixels)
         const int my_grp = act ? (qe - q0 + 15) / 16 : 0;
         const int n_grp = __reduce_max_sync(0xffffffffu, my_grp);
@@ -794,15 +806,14 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
           const int base = q0 + 16 * gi;
           const int valid = act ? max(0, min(16, qe - base)) : 0;
           const unsigned int sb = seg_sup_bits(sup, base, valid);
-          const bool first = base == 0;  // lane 0's first group: pixel 0 has no carry in, coefficient c_first
           const double c0 = carry;
           double c = c0, v[16];
           unsigned int big = 0;
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
-            const double vk = (k == 0 && first) ? p[0] : p[k] + c;
+            const double vk = p[k] + c;
             v[k] = vk;
-            asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(vk), "d"((k == 0 && first) ? c_first : c_mid));
+            asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(vk), "d"(c_mid));
             big |= __double2hiint(vk) >= 0x3FE00000 ? (1u << k) : 0u;
           }
           {
@@ -819,18 +830,19 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
               c = c0;
 #pragma unroll
               for (int k = 0; k < 16; ++k) {
-                const double vk = (k == 0 && first) ? p[0] : p[k] + c;
+                const double vk = p[k] + c;
                 const bool em = vk >= 0.5 && ((sb >> k) & 1u);
                 const double e = em ? vk - 1.0 : vk;
                 emask |= static_cast<unsigned int>(em) << k;
                 v[k] = e;
-                asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(e), "d"((k == 0 && first) ? c_first : c_mid));
+                asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(e), "d"(c_mid));
               }
             }
           }
           carry = c;
           // own-segment errors and emission bits, the warm-up's last error
-          // (groups never straddle a segment start: kSegWU is a multiple of 16)
+          // (groups never straddle a segment start: kSegWU is a multiple of 16;
+          // segment 0's groups start at pixel 1, inside its segment)
           const int own = base - qs;  // < 0: a warm-up group
           double* eb = err + (valid > 0 ? base : 0);
 #pragma unroll
