@@ -885,11 +885,6 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
         bool todo = act && sl > 0, recheck = true;
         int chg_hi = -1;  // the last error this lane's reruns rewrote
         for (;;) {
-          // any segment to check or rerun, over all chain warps
-          int any;
-          asm volatile("{ .reg .pred p, q; setp.ne.s32 q, %1, 0; bar.red.or.pred p, 5, %2, q; selp.s32 %0, 1, 0, p; }"
-                       : "=r"(any) : "r"(static_cast<int>(todo)), "r"(kSegLanes) : "memory");
-          if (!any) break;
           bool run = false;
           double cr = 0.0;
           if (todo) {
@@ -897,6 +892,11 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
             run = !recheck || __double_as_longlong(et) != __double_as_longlong(wu);
             cr = et * c_mid;  // qs - 1 >= kSegWU: an interior pixel
           }
+          // any segment to rerun, over all chain warps (usually none: one barrier)
+          int any;
+          asm volatile("{ .reg .pred p, q; setp.ne.s32 q, %1, 0; bar.red.or.pred p, 5, %2, q; selp.s32 %0, 1, 0, p; }"
+                       : "=r"(any) : "r"(static_cast<int>(run)), "r"(kSegLanes) : "memory");
+          if (!any) break;
           bool changed = run;  // cleared when the rerun meets the stored chain
 #ifdef GL_EXPERIMENT_ENV
           if (run) ++n_fix;
