@@ -883,7 +883,8 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
         // final; a lane whose rerun reached its segment end without meeting
         // changed that end, and its successor reruns in another round. ----
         bool todo = act && sl > 0, recheck = true;
-        int chg_hi = -1;  // the last error this lane's reruns rewrote
+        int chg_hi = -1;   // the last error this lane's reruns rewrote
+        int n_first = 0;   // segments the first round reruns (chooses the next row's layout)
         for (;;) {
           bool run = false;
           double cr = 0.0;
@@ -892,10 +893,11 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
             run = !recheck || __double_as_longlong(et) != __double_as_longlong(wu);
             cr = et * c_mid;  // qs - 1 >= kSegWU: an interior pixel
           }
-          // any segment to rerun, over all chain warps (usually none: one barrier)
+          // how many segments rerun, over all chain warps (usually none: one barrier)
           int any;
-          asm volatile("{ .reg .pred p, q; setp.ne.s32 q, %1, 0; bar.red.or.pred p, 5, %2, q; selp.s32 %0, 1, 0, p; }"
+          asm volatile("{ .reg .pred q; setp.ne.s32 q, %1, 0; bar.red.popc.u32 %0, 5, %2, q; }"
                        : "=r"(any) : "r"(static_cast<int>(run)), "r"(kSegLanes) : "memory");
+          if (recheck) n_first = any;
           if (!any) break;
           bool changed = run;  // cleared when the rerun meets the stored chain
 #ifdef GL_EXPERIMENT_ENV
@@ -951,13 +953,12 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
           todo = act && sl > 0 && s_changed[sl - 1];
         }
         s_chg_hi[sl] = chg_hi;
-        asm volatile("bar.sync 5, %0;" ::"r"(kSegLanes) : "memory");  // emission bits and changes final
+        // reruns rewrote emission bits across the chain warps: warp 0's scan
+        // below needs them (n_first is uniform: a barrier reduction)
+        if (n_first > 0) asm volatile("bar.sync 5, %0;" ::"r"(kSegLanes) : "memory");
         if (nxt) asm volatile("bar.arrive 4, %0;" ::"r"(kSegT) : "memory");
         if (warp == 0) {
-          int n_rerun = 0;
-#pragma unroll
-          for (int wv = 0; wv < kSegW; ++wv) n_rerun += __popc(__ballot_sync(0xffffffffu, s_chg_hi[32 * wv + lane] >= 0));
-          if (lane == 0) s_many[d ^ 1] = n_rerun < 2;
+          if (lane == 0) s_many[d ^ 1] = n_first < 2;
         // ---- the row's emissions in scan order: a warp scan over the
         // emission words (cleared for the next row) ----
         const int nw = (w + 31) >> 5;
