@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
   extern __shared__ double segsh[];
   const int WR = ((w + 1) & ~1) + 16, SW = (w + 31) / 32 + 2;  // +16: a lane's last group reads past w
   // buf[j & 1]: row j's pre-accumulated work (scan order); buf[(j + 1) & 1]:
-  // row j + 1's, built by warps 1..3 while row j is verified
+  // row j + 1's, built by the staging warps while row j is verified
   double* buf0 = segsh;
   double* err = segsh + 2 * WR;  // row j's errors, scan order
   double* raw = segsh + 3 * WR;  // row j + 1 of bm in its scan order (cp.async while row j sweeps)
@@ -729,7 +729,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
     const int start = dir == 1 ? 0 : w - 1;
     const bool last = j == h - 1;
     double* pre = buf0 + d * WR;            // row j's pre-accumulated work
-    double* nbuf = buf0 + (d ^ 1) * WR;     // row j + 1's pre (built by warps 1..3 during row j)
+    double* nbuf = buf0 + (d ^ 1) * WR;     // row j + 1's pre (built by the staging warps during row j)
     const bool nxt = j + 1 < h;
     const SegLayout L = s_many[d] ? L_many : L_few;
     const unsigned int* sup = sup0 + d * SW;
@@ -992,7 +992,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
       }
       SEG_TICK(tk_ver);
     } else if (nxt) {
-      // ---- warps 1..3 while warp 0 sweeps row j: row j + 1 of bm into raw
+      // ---- the staging warps while the chain warps sweep row j: row j + 1 of bm into raw
       // in its scan order (all loads in flight at once) and its support
       // bits; once warp 0's chains are done, row j + 1's pre-accumulation
       // (overlapping warp 0's verification); then the positions next to
