@@ -994,8 +994,8 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
     } else if (nxt) {
       // ---- the staging warps while the chain warps sweep row j: row j + 1 of bm into raw
       // in its scan order (all loads in flight at once) and its support
-      // bits; once warp 0's chains are done, row j + 1's pre-accumulation
-      // (overlapping warp 0's verification); then the positions next to
+      // bits; once the chains are done, row j + 1's pre-accumulation
+      // (overlapping the verification); then the positions next to
       // errors the verification rewrote ----
       const double* brow = bm + static_cast<size_t>(j + 1) * w;
       const bool rev = dir == 1;  // row j + 1 scans right to left
@@ -1035,7 +1035,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
         const double dn = x + err[min(pos + 1, w - 1)] * c3;
         return pos + 1 < w ? dn : x;
       };
-      asm volatile("bar.sync 3, %0;" ::"r"(kSegT) : "memory");  // warp 0's chains are done
+      asm volatile("bar.sync 3, %0;" ::"r"(kSegT) : "memory");  // the chains are done
       for (int i0 = t3; i0 < w; i0 += 4 * kT3) {
         double v[4];
 #pragma unroll
