@@ -1,8 +1,4 @@
 #!/bin/bash
-timeout 900 python -m pytest -q -x tests/test_gpu_dither_seg.py tests/test_gpu_readouts.py tests/test_gpu_dither_wide.py 2>&1 | tail -1
-timeout 600 python tools/stress_dither.py 1000 2>&1 | tail -1
-for r in 1 2; do
-for v in base product; do
-  if [ $v = product ]; then unset GRIDLOC_B200_LIB; else export GRIDLOC_B200_LIB=$PWD/build/variants/$v/libgridloc_b200.so; fi
-  timeout 300 python tools/ab_dither.py 1024 40 2>&1 | tail -1
-done; done; true
+timeout 600 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:k_dither_seg -c 1 -o gpurun_out/dither_seg -f python tools/obs_cycle.py 160 > gpurun_out/dither_seg.log 2>&1
+timeout 600 ncu --profile-from-start off --set full --clock-control none -k regex:k_dither_seg -c 1 -o gpurun_out/dither_seg_early -f python tools/obs_cycle.py 16 > gpurun_out/dither_seg_early.log 2>&1
+tail -1 gpurun_out/dither_seg.log; tail -1 gpurun_out/dither_seg_early.log
