@@ -630,6 +630,73 @@ __global__ void __launch_bounds__(kSumT, 2) k_chunk_maps(const double* __restric
   }
 }
 
+// ---- phase 3b: runs of consecutive chunks guessed for one binade, composed
+// in order (one CTA, a segmented scan over tiles of 1024 chunks): the walk
+// then crosses a whole run with one map, checked like a chunk's.
+struct RunAcc {
+  int f;      // 1: a run starts here (or a non-member breaks the run)
+  int start;  // the run's first chunk
+  IncPair m;
+};
+__device__ __forceinline__ RunAcc run_combine(RunAcc a, RunAcc b) {  // a, then b
+  return b.f ? b : RunAcc{a.f, a.start, compose(a.m, b.m)};
+}
+__device__ __forceinline__ RunAcc run_shfl_up(RunAcc a, int o) {
+  RunAcc r;
+  r.f = __shfl_up_sync(0xffffffffu, a.f, o);
+  r.start = __shfl_up_sync(0xffffffffu, a.start, o);
+  r.m.a0 = __shfl_up_sync(0xffffffffu, a.m.a0, o);
+  r.m.a1 = __shfl_up_sync(0xffffffffu, a.m.a1, o);
+  return r;
+}
+
+__global__ void __launch_bounds__(1024) k_chunk_runs(const int* __restrict__ guess, const IncPair* __restrict__ maps,
+                                                     int n_chunks, int* __restrict__ run_end,
+                                                     IncPair* __restrict__ run_map) {
+  __shared__ RunAcc s_w[32];
+  __shared__ RunAcc s_carry;  // the run still open at the end of the previous tile (f = 1)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_carry = RunAcc{1, -1, IncPair{0, 0}};
+  __syncthreads();
+  for (int t0 = 0; t0 < n_chunks; t0 += 1024) {
+    const int c = t0 + tid;
+    const int g = c < n_chunks ? guess[c] : kNoGuess;
+    const int gprev = (c > 0 && c - 1 < n_chunks) ? guess[c - 1] : kNoGuess;
+    const bool member = g != kNoGuess;
+    const bool starts = member && gprev != g;
+    RunAcc mine = member ? RunAcc{starts ? 1 : 0, starts ? c : -1, maps[c]} : RunAcc{1, -1, IncPair{0, 0}};
+    if (tid == 0 && member && !starts) mine = run_combine(s_carry, mine);  // continues the open run
+    // block-wide inclusive segmented scan
+    RunAcc incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const RunAcc y = run_shfl_up(incl, o);
+      if (lane >= o) incl = run_combine(y, incl);
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      RunAcc wv = s_w[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const RunAcc y = run_shfl_up(wv, o);
+        if (lane >= o) wv = run_combine(y, wv);
+      }
+      s_w[lane] = wv;
+    }
+    __syncthreads();
+    if (warp > 0) incl = run_combine(s_w[warp - 1], incl);
+    const int gnext = c + 1 < n_chunks ? guess[c + 1] : kNoGuess;
+    if (member && gnext != g && incl.start >= 0) {  // the run's last chunk
+      run_end[incl.start] = c + 1;
+      run_map[incl.start] = incl.m;
+    }
+    __syncthreads();
+    if (tid == 1023) s_carry = (member && gnext == g) ? RunAcc{1, incl.start, incl.m} : RunAcc{1, -1, IncPair{0, 0}};
+    __syncthreads();
+  }
+}
+
 // ---- phase 4 (or the whole sum for small inputs): one CTA walks the chunks
 #ifdef GL_EXPERIMENT_ENV
 __device__ long long g_seq_dbg[8];  // whole-chunk steps, segmented ok, segmented failed, events, element-wise steps, over-cap
@@ -650,6 +717,7 @@ __global__ void __launch_bounds__(kSumT) k_seq_sum(const double* __restrict__ x,
                                                    const double* __restrict__ S, const int* __restrict__ ev_n,
                                                    const int* __restrict__ ev_slot, const int* __restrict__ pool_start,
                                                    const int* __restrict__ pool_g, const IncPair* __restrict__ pool_map,
+                                                   const int* __restrict__ run_end, const IncPair* __restrict__ run_map,
                                                    double* __restrict__ total, int* __restrict__ invalid) {
   extern __shared__ __align__(16) unsigned char seq_dyn[];
   SeqSmem& sm = *reinterpret_cast<SeqSmem*>(seq_dyn);
@@ -751,6 +819,22 @@ __global__ void __launch_bounds__(kSumT) k_seq_sum(const double* __restrict__ x,
     long long mmax, m0;
     binade(s, &ulog, &mmax, &m0);
     const double u = ulp_of(ulog);
+    // a whole run of chunks guessed for this binade, with its composed map
+    if (run_end && pos % kSumChunk == 0) {
+      const size_t c0 = pos / kSumChunk;
+      if (guess[c0] == ulog) {
+        const int re = run_end[c0];
+        if (re > static_cast<int>(c0)) {
+          const long long m1 = apply(run_map[c0], m0);
+          if (m1 < mmax) {
+            s = static_cast<double>(m1) * u;
+            pos = min(n, static_cast<size_t>(re) * kSumChunk);
+            SEQ_DBG(7, 1);
+            continue;
+          }
+        }
+      }
+    }
     // whole chunks whose maps were composed under this binade, up to 1024
     // at once: the same scan one level up (chunk maps as elements; a chunk
     // guessed for another binade acts as a crossing)
@@ -903,7 +987,7 @@ __global__ void k_seq_sum_chain(const double* __restrict__ x, size_t n, double s
 
 size_t seq_sum_scratch_bytes(size_t n) {
   const size_t chunks = (n + kSumChunk - 1) / kSumChunk;
-  return chunks * (sizeof(IncPair) + 2 * sizeof(double) + 3 * sizeof(int) + sizeof(ArgBest)) +
+  return chunks * (2 * sizeof(IncPair) + 2 * sizeof(double) + 4 * sizeof(int) + sizeof(ArgBest)) + 64 +
          static_cast<size_t>(kEvPool) * kEvCap * (sizeof(IncPair) + 2 * sizeof(int)) + 64;
 }
 
@@ -918,7 +1002,7 @@ void launch_seq_sum(gl_context* ctx, const double* x, size_t n, double* d_total,
   seq_sum_smem_attr();
   cudaMemsetAsync(d_invalid, 0, sizeof(int), ctx->stream);
   k_seq_sum<<<1, kSumT, kSeqSmem, ctx->stream>>>(x, n, s0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                                 nullptr, nullptr, d_total, d_invalid);
+                                                 nullptr, nullptr, nullptr, nullptr, d_total, d_invalid);
   ctx->launches++;
 }
 
@@ -947,6 +1031,10 @@ void launch_seq_sum_big(gl_context* ctx, const double* x, size_t n, double* d_to
   auto* pool_g = pool_start + pool;
   auto* pool_ctr = pool_g + pool;
   auto* arg = reinterpret_cast<ArgBest*>((reinterpret_cast<uintptr_t>(pool_ctr + 1) + 15) & ~uintptr_t(15));
+  auto* run_map = reinterpret_cast<IncPair*>(arg + chunks);  // 16-byte aligned (ArgBest is 24 B: realign)
+  run_map = reinterpret_cast<IncPair*>((reinterpret_cast<uintptr_t>(run_map) + 15) & ~uintptr_t(15));
+  auto* run_end = reinterpret_cast<int*>(run_map + chunks);
+  cudaMemsetAsync(run_end, 0, sizeof(int) * chunks, ctx->stream);
   cudaMemsetAsync(d_invalid, 0, sizeof(int), ctx->stream);
   cudaMemsetAsync(pool_ctr, 0, sizeof(int), ctx->stream);
   const int nc = static_cast<int>(chunks);
@@ -961,16 +1049,17 @@ void launch_seq_sum_big(gl_context* ctx, const double* x, size_t n, double* d_to
   k_chunk_events<<<ev_grid, kSumT, 0, ctx->stream>>>(x, n, nc, guess, Pc, ev_n, ev_slot, pool_ctr, pool_start, pool_g,
                                                      pool_map);
   seq_sum_smem_attr();
+  k_chunk_runs<<<1, 1024, 0, ctx->stream>>>(guess, maps, nc, run_end, run_map);
   k_seq_sum<<<1, kSumT, kSeqSmem, ctx->stream>>>(x, n, s0, guess, maps, S, ev_n, ev_slot, pool_start, pool_g,
-                                                 pool_map, d_total, d_invalid);
-  ctx->launches += 5;
+                                                 pool_map, run_end, run_map, d_total, d_invalid);
+  ctx->launches += 6;
 #ifdef GL_EXPERIMENT_ENV
   if (getenv("GL_DEBUG_SEQSUM")) {
     long long h[8];
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpyFromSymbol(h, g_seq_dbg, sizeof(h));
-    fprintf(stderr, "seq sum n=%zu chunks=%zu: whole-chunk steps %lld, segmented ok %lld, failed %lld, events %lld, element-wise steps %lld, over cap %lld, precomputed chunks %lld\n",
-            n, chunks, h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
+    fprintf(stderr, "seq sum n=%zu chunks=%zu: whole-chunk steps %lld, segmented ok %lld, failed %lld, events %lld, element-wise steps %lld, over cap %lld, precomputed chunks %lld, runs %lld\n",
+            n, chunks, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
     const long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(g_seq_dbg, z, sizeof(z));
   }
