@@ -568,6 +568,13 @@ constexpr int kSegW = GL_SEG_CHAIN_WARPS;  // warps running segment chains (the 
 constexpr int kSegLanes = 32 * kSegW;      // segments per row at most
 static_assert(kSegW >= 1 && kSegW <= 2, "1 or 2 chain warps (4-warp CTA)");
 
+// a chain lane's segment under one layout (fixed for the kernel)
+struct SegLane {
+  bool act;           // the lane has a segment
+  int qs, qe, q0;     // segment start / end, first pixel it runs
+  int n_grp;          // its warp's group count (lanes past their segment: no pixels)
+};
+
 struct SegLayout {
   int P, F, S;  // lanes in use, lane 0's length, segment stride (odd)
   __host__ __device__ int start(int l) const { return l == 0 ? 0 : min(w_, F + (l - 1) * S); }
@@ -710,6 +717,25 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
   }
   for (int i = tid; i < SW; i += kSegT) ebits[i] = 0u;
   if (tid == 0) s_many[0] = 1;
+  // each chain lane's segment under both layouts, once: segment 0 takes the
+  // row's first pixel itself (no carry in, its own carry coefficient) and its
+  // groups start at pixel 1, so no group needs a first-pixel case; the
+  // others start kSegWU pixels early (F > kSegWU: inside the row) from the
+  // guessed carry 0
+  SegLane lane_many{}, lane_few{};
+  if (warp < kSegW) {
+    auto lane_of = [&](const SegLayout& Ly) {
+      SegLane r;
+      r.act = tid < Ly.P;
+      r.qs = Ly.start(tid);
+      r.qe = Ly.start(tid + 1);
+      r.q0 = tid == 0 ? 1 : r.qs - kSegWU;
+      r.n_grp = __reduce_max_sync(0xffffffffu, r.act ? (r.qe - r.q0 + 15) / 16 : 0);
+      return r;
+    };
+    lane_many = lane_of(L_many);
+    lane_few = lane_of(L_few);
+  }
   __syncthreads();
 #ifdef GL_EXPERIMENT_ENV
   long long tk_spec = 0, tk_ver = 0, tk_pre = 0, tk_b1 = 0, tk_stage = 0, tk_all = clock64(), tk0 = 0;
@@ -776,13 +802,9 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
           asm volatile("bar.arrive 4, %0;" ::"r"(kSegT) : "memory");
         }
       } else {
-        const bool act = sl < L.P;
-        const int qs = L.start(sl), qe = L.start(sl + 1);
-        // segment 0 takes the row's first pixel here (no carry in, its own
-        // carry coefficient) and its groups start at pixel 1, so no group
-        // needs a first-pixel case; the others start kSegWU pixels early
-        // (F > kSegWU: inside the row) from the guessed carry 0
-        const int q0 = sl == 0 ? 1 : qs - kSegWU;
+        const SegLane& SLn = s_many[d] ? lane_many : lane_few;
+        const bool act = SLn.act;
+        const int qs = SLn.qs, qe = SLn.qe, q0 = SLn.q0;
         double carry = 0.0;
         double wu = 0.0;
         if (sl == 0) {
@@ -793,9 +815,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
           if (em0) atomicOr(&ebits[0], 1u);
           carry = e0 * c_first;
         }
-        // the warp's group count (lanes past their segment: no pixels)
-        const int my_grp = act ? (qe - q0 + 15) / 16 : 0;
-        const int n_grp = __reduce_max_sync(0xffffffffu, my_grp);
+        const int n_grp = SLn.n_grp;
         // One group: the chain on values already in registers, then the NEXT
         // group's loads issued before the replay vote (the vote and its
         // branch would otherwise hold them back), double-buffered by hand.
@@ -866,10 +886,12 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
 #pragma unroll
           for (int k = 0; k < 16; ++k) pa[k] = pb[k];
         }
+        SEG_TICK(tk_b1);  // row setup
         for (int gi = 0; gi < n_grp; gi += 2) {
           group(pa, pb2, gi);
           if (gi + 1 < n_grp) group(pb2, pa, gi + 1);
         }
+        SEG_TICK(tk_g0);  // the groups
         asm volatile("bar.sync 5, %0;" ::"r"(kSegLanes) : "memory");  // every chain's errors stored
         // the staging warps start the next row's pass on these errors now;
         // what the verification below rewrites they recompute after barrier 4
@@ -1317,7 +1339,7 @@ void launch_dither(gl_context* ctx, const double* bm, int w, int h, int budget,
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpyFromSymbol(clk, g_dither_clk, sizeof(clk));
     fprintf(stderr, "dither clocks: %lld %lld %lld %lld %lld %lld %lld %lld %lld (pipe: row-end wait, total, sweep, row-start wait; seg: spec, verify, pre, all, barrier-1 wait, staging, group chain, group rest, replays) (%d x %d)\n", clk[0], clk[1], clk[2], clk[3], clk[4], clk[5], clk[6], clk[7] & ((1LL << 40) - 1), clk[7] >> 40, w, h);
-    fprintf(stderr, "dither events: fixed lanes %lld, fixed pixels %lld, exact rows %lld; post pass: edge %lld loop %lld\n", clk[9], clk[10], clk[11], clk[8], clk[6]);
+    fprintf(stderr, "dither events: fixed lanes %lld, fixed pixels %lld, exact rows %lld; setup %lld groups %lld\n", clk[9], clk[10], clk[11], clk[4], clk[6]);
   }
 #endif
 
