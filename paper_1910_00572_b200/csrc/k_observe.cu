@@ -559,8 +559,16 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
 #define GL_FS_SEG 1  // the segment-parallel sweep (0: the pipelined chain only)
 #endif
 constexpr int kSegT = 128;     // threads (4 warps: kSegW chain warps, the rest stage the next row)
-constexpr int kSegWU = 64;     // warm-up pixels of segments 1..
-static_assert(kSegWU % 16 == 0, "warm-ups are whole 16-pixel groups");
+constexpr int kSegWU = 64;     // warm-up pixels of segments 1.. (the many-segment layout)
+#ifndef GL_SEG_WU_FEW
+#define GL_SEG_WU_FEW 64
+#endif
+// the 32-segment layout's warm-up (rows after verification reruns:
+// concentrated beliefs). Longer warm-ups there (80, 96) measured within noise
+// of 64 (profiles/r02_sweeps.md).
+constexpr int kSegWUFew = GL_SEG_WU_FEW;
+static_assert(kSegWU % 16 == 0 && kSegWUFew % 16 == 0 && kSegWUFew >= kSegWU,
+              "warm-ups are whole 16-pixel groups");
 #ifndef GL_SEG_CHAIN_WARPS
 #define GL_SEG_CHAIN_WARPS 2
 #endif
@@ -577,23 +585,25 @@ struct SegLane {
 
 struct SegLayout {
   int P, F, S;  // lanes in use, lane 0's length, segment stride (odd)
+  int wu;       // warm-up pixels of segments 1..
   __host__ __device__ int start(int l) const { return l == 0 ? 0 : min(w_, F + (l - 1) * S); }
   int w_;
 };
 
-__host__ __device__ inline SegLayout seg_layout(int w, int lanes) {
+__host__ __device__ inline SegLayout seg_layout(int w, int lanes, int wu = kSegWU) {
   SegLayout L{};
   L.w_ = w;
+  L.wu = wu;
   if (w < 4 * kSegWU) {
     L.P = 1;
     L.F = w;
     L.S = w;
     return L;
   }
-  int S = (w - kSegWU + lanes - 1) / lanes;  // lane 0 takes S + kSegWU (every lane runs ~S + kSegWU pixels)
+  int S = (w - wu + lanes - 1) / lanes;  // lane 0 takes S + wu (every lane runs ~S + wu pixels)
   S |= 1;
   L.S = S;
-  L.F = min(w, S + kSegWU);
+  L.F = min(w, S + wu);
   L.P = 1 + (w - L.F + S - 1) / S;
   return L;
 }
@@ -684,7 +694,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
   // short segments turn one slow meeting into rounds) takes the 32-segment
   // layout; the extra chain warp then has no segments and only keeps the
   // barriers.
-  const SegLayout L_many = seg_layout(w, kSegLanes), L_few = seg_layout(w, 32);
+  const SegLayout L_many = seg_layout(w, kSegLanes), L_few = seg_layout(w, 32, kSegWUFew);
   __shared__ int s_many[2];  // row parity: this row takes L_many
   // per-direction constants of every row but the last (fs_wsum with a row
   // below; [0]: dir +1, [1]: dir -1): carry coefficients and the diffusion
@@ -729,7 +739,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
       r.act = tid < Ly.P;
       r.qs = Ly.start(tid);
       r.qe = Ly.start(tid + 1);
-      r.q0 = tid == 0 ? 1 : r.qs - kSegWU;
+      r.q0 = tid == 0 ? 1 : r.qs - Ly.wu;
       r.n_grp = __reduce_max_sync(0xffffffffu, r.act ? (r.qe - r.q0 + 15) / 16 : 0);
       return r;
     };
