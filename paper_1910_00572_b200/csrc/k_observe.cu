@@ -560,6 +560,9 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
 #endif
 constexpr int kSegT = 128;     // threads (4 warps: kSegW chain warps, the rest stage the next row)
 constexpr int kSegWU = 64;     // warm-up pixels of segments 1.. (the many-segment layout)
+#ifndef GL_SEG_FEW_LANES
+#define GL_SEG_FEW_LANES 32  // segments of the fallback layout
+#endif
 #ifndef GL_SEG_WU_FEW
 #define GL_SEG_WU_FEW 64
 #endif
@@ -694,7 +697,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
   // short segments turn one slow meeting into rounds) takes the 32-segment
   // layout; the extra chain warp then has no segments and only keeps the
   // barriers.
-  const SegLayout L_many = seg_layout(w, kSegLanes), L_few = seg_layout(w, 32, kSegWUFew);
+  const SegLayout L_many = seg_layout(w, kSegLanes), L_few = seg_layout(w, GL_SEG_FEW_LANES, kSegWUFew);
   __shared__ int s_many[2];  // row parity: this row takes L_many
   // per-direction constants of every row but the last (fs_wsum with a row
   // below; [0]: dir +1, [1]: dir -1): carry coefficients and the diffusion
