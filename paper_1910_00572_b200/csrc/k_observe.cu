@@ -560,6 +560,10 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
 #endif
 constexpr int kSegT = 128;     // threads (4 warps: kSegW chain warps, the rest stage the next row)
 constexpr int kSegWU = 64;     // warm-up pixels of segments 1.. (the many-segment layout)
+#ifndef GL_SEG_FEW_ROWS
+#define GL_SEG_FEW_ROWS 8  // rows the fallback layout holds after 2+ reruns (1: rows alternate)
+#endif
+constexpr int kSegFewRows = GL_SEG_FEW_ROWS;
 #ifndef GL_SEG_FEW_LANES
 #define GL_SEG_FEW_LANES 32  // segments of the fallback layout
 #endif
@@ -699,6 +703,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
   // barriers.
   const SegLayout L_many = seg_layout(w, kSegLanes), L_few = seg_layout(w, GL_SEG_FEW_LANES, kSegWUFew);
   __shared__ int s_many[2];  // row parity: this row takes L_many
+  __shared__ int s_few_left;  // rows the fallback layout still holds (sticky: rows alternate otherwise)
   // per-direction constants of every row but the last (fs_wsum with a row
   // below; [0]: dir +1, [1]: dir -1): carry coefficients and the diffusion
   // quotients of the row-end sources. Computed once into shared memory (in
@@ -729,7 +734,10 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
     sup0[SW + w / 32 + 1] = 0u;
   }
   for (int i = tid; i < SW; i += kSegT) ebits[i] = 0u;
-  if (tid == 0) s_many[0] = 1;
+  if (tid == 0) {
+    s_many[0] = 1;
+    s_few_left = 0;
+  }
   // each chain lane's segment under both layouts, once: segment 0 takes the
   // row's first pixel itself (no carry in, its own carry coefficient) and its
   // groups start at pixel 1, so no group needs a first-pixel case; the
@@ -993,7 +1001,12 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
         if (n_first > 0) asm volatile("bar.sync 5, %0;" ::"r"(kSegLanes) : "memory");
         if (nxt) asm volatile("bar.arrive 4, %0;" ::"r"(kSegT) : "memory");
         if (warp == 0) {
-          if (lane == 0) s_many[d ^ 1] = n_first < 2;
+          if (lane == 0) {
+            // 2+ reruns: the fallback layout for the next kSegFewRows rows
+            if (n_first >= 2) s_few_left = kSegFewRows;
+            else if (s_few_left > 0) --s_few_left;
+            s_many[d ^ 1] = s_few_left == 0;
+          }
         // ---- the row's emissions in scan order: a warp scan over the
         // emission words (cleared for the next row) ----
         const int nw = (w + 31) >> 5;
