@@ -696,11 +696,11 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
   const double scale = budget / total;
   if (tid == 0) s_count = 0;
   // Two layouts: 32 * kSegW segments (shorter warm-up share per row) and
-  // 32 (longer segments). A row whose predecessor needed verification reruns
-  // on 2+ segments (a concentrated belief: steep tails converge slowly, and
-  // short segments turn one slow meeting into rounds) takes the 32-segment
-  // layout; the extra chain warp then has no segments and only keeps the
-  // barriers.
+  // 32 (longer segments). After a row that needed verification reruns on 2+
+  // segments (a concentrated belief: steep tails converge slowly, and short
+  // segments turn one slow meeting into rounds) the next kSegFewRows rows
+  // take the 32-segment layout; the extra chain warp then has no segments and
+  // only keeps the barriers.
   const SegLayout L_many = seg_layout(w, kSegLanes), L_few = seg_layout(w, GL_SEG_FEW_LANES, kSegWUFew);
   __shared__ int s_many[2];  // row parity: this row takes L_many
   __shared__ int s_few_left;  // rows the fallback layout still holds (sticky: rows alternate otherwise)
