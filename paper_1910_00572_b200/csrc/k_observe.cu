@@ -564,6 +564,10 @@ constexpr int kSegWU = 64;     // warm-up pixels of segments 1.. (the many-segme
 #define GL_SEG_FEW_ROWS 8  // rows the fallback layout holds after 2+ reruns (1: rows alternate)
 #endif
 constexpr int kSegFewRows = GL_SEG_FEW_ROWS;
+#ifndef GL_SEG_FEW_AT
+#define GL_SEG_FEW_AT 2  // first-round reruns that switch to the fallback layout
+#endif
+constexpr int kSegFewAt = GL_SEG_FEW_AT;
 #ifndef GL_SEG_FEW_LANES
 #define GL_SEG_FEW_LANES 32  // segments of the fallback layout
 #endif
@@ -1003,7 +1007,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
         if (warp == 0) {
           if (lane == 0) {
             // 2+ reruns: the fallback layout for the next kSegFewRows rows
-            if (n_first >= 2) s_few_left = kSegFewRows;
+            if (n_first >= kSegFewAt) s_few_left = kSegFewRows;
             else if (s_few_left > 0) --s_few_left;
             s_many[d ^ 1] = s_few_left == 0;
           }
