@@ -628,46 +628,6 @@ __device__ __forceinline__ unsigned int seg_sup_bits(const unsigned int* sup, in
   return static_cast<unsigned int>(sw2 >> (b & 31)) & (valid >= 16 ? 0xffffu : ((1u << valid) - 1u));
 }
 
-// One 16-pixel group of a lane's chain from carry c0 (warp-collective: every
-// lane calls it). The values are loaded up front (past the lane's valid
-// pixels: padding or other lanes' values, masked by sb); the chain runs
-// assuming no emission (one DADD and one DMUL per pixel) and is replayed
-// exactly by the lanes whose group holds a supported v >= 0.5. v <- errors,
-// emask <- emissions, returns the carry out. first: the row's pixel 0 (no
-// carry in, coefficient c_first).
-__device__ __forceinline__ double seg_group(const double* pb, unsigned int sb, bool first, double c0, double c_first,
-                                            double c_mid, double (&v)[16], unsigned int& emask) {
-  double p[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) p[k] = pb[k];
-  double c = c0;
-  unsigned int big = 0;  // pixels with v >= 0.5 (high word test; NaN / inf included)
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const double vk = (k == 0 && first) ? p[0] : p[k] + c;
-    v[k] = vk;
-    asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(vk), "d"((k == 0 && first) ? c_first : c_mid));
-    big |= __double2hiint(vk) >= 0x3FE00000 ? (1u << k) : 0u;
-  }
-  emask = 0u;
-  const bool need = (big & sb) != 0u;
-  if (__any_sync(0xffffffffu, need)) {
-    if (need) {
-      c = c0;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const double vk = (k == 0 && first) ? p[0] : p[k] + c;
-        const bool em = vk >= 0.5 && ((sb >> k) & 1u);
-        const double e = em ? vk - 1.0 : vk;
-        emask |= static_cast<unsigned int>(em) << k;
-        v[k] = e;
-        asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(e), "d"((k == 0 && first) ? c_first : c_mid));
-      }
-    }
-  }
-  return c;
-}
-
 __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__ bm, int w, int h, int budget,
                                                       int* __restrict__ cells, int cap, int* __restrict__ n_out,
                                                       const double* __restrict__ total_in,
@@ -951,12 +911,57 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
           if (run) ++n_fix;
 #endif
           int base = qs;
+          double rp[16];  // the rerun group's values, loaded one group ahead
+          {
+            const double* pb = pre + (run ? base : 0);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) rp[k] = pb[k];
+          }
           while (__any_sync(0xffffffffu, run)) {
             const int valid = run ? max(0, min(16, qe - base)) : 0;
-            double v[16];
-            unsigned int emask;
-            const double cn = seg_group(pre + (valid > 0 ? base : 0), seg_sup_bits(sup, base, valid), false, cr,
-                                        c_first, c_mid, v, emask);
+            const unsigned int sb = seg_sup_bits(sup, base, valid);
+            double v[16], st[16];
+            double c = cr;
+            unsigned int big = 0u;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const double vk = rp[k] + c;
+              v[k] = vk;
+              asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(vk), "d"(c_mid));
+              big |= __double2hiint(vk) >= 0x3FE00000 ? (1u << k) : 0u;
+            }
+            // the stored chain to meet, and the next group's values, before the vote
+            {
+              const double* eb = err + (valid > 0 ? base : 0);
+#pragma unroll
+              for (int k = 0; k < 16; ++k) st[k] = eb[k];
+            }
+            double rn[16];
+            {
+              const int nv = run ? max(0, min(16, qe - base - 16)) : 0;
+              const double* pb = pre + (nv > 0 ? base + 16 : 0);
+#pragma unroll
+              for (int k = 0; k < 16; ++k) rn[k] = pb[k];
+            }
+            unsigned int emask = 0u;
+            const bool need = (big & sb) != 0u;
+            if (__any_sync(0xffffffffu, need)) {
+              if (need) {  // the exact sweep of this group
+                c = cr;
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                  const double vk = rp[k] + c;
+                  const bool em = vk >= 0.5 && ((sb >> k) & 1u);
+                  const double e = em ? vk - 1.0 : vk;
+                  emask |= static_cast<unsigned int>(em) << k;
+                  v[k] = e;
+                  asm("mul.rn.f64 %0, %1, %2;" : "=d"(c) : "d"(e), "d"(c_mid));
+                }
+              }
+            }
+            const double cn = c;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) rp[k] = rn[k];
             if (valid > 0) {
               // the first pixel where the rerun equals the stored chain: the
               // same state from there on. Its emission is the rerun's (equal
@@ -964,7 +969,7 @@ __global__ void __launch_bounds__(kSegT) k_dither_seg(const double* __restrict__
               unsigned int meet = 0u;
 #pragma unroll
               for (int k = 0; k < 16; ++k) {
-                if (k < valid && __double_as_longlong(v[k]) == __double_as_longlong(err[base + k])) meet |= 1u << k;
+                if (k < valid && __double_as_longlong(v[k]) == __double_as_longlong(st[k])) meet |= 1u << k;
               }
               const int m = meet ? __ffs(meet) - 1 : valid - 1;  // last pixel taken from the rerun
 #ifdef GL_EXPERIMENT_ENV
