@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(64) k_dither_pipe(
 // with a guessed carry 0 (a warm-up over the previous segment's tail that
 // records nothing). Segments are S pixels apart with S odd, so the lanes'
 // shared-memory accesses fall in distinct banks. Each lane works in
-// 16-pixel groups (seg_group): values loaded up front, the chain run assuming
+// 16-pixel groups: values loaded a group ahead, the chain run assuming
 // no emission (one DADD and one DMUL per pixel), the group replayed exactly
 // by the lanes that need it when any lane's group holds a supported v >= 0.5.
 // Emissions are bits of a per-row mask. Then all segments are verified at
