@@ -16,7 +16,7 @@ def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 200
     ctx = g.Context(0)
     port = oracle.Port()
-    rng = np.random.default_rng(12345)
+    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 12345)
     kinds = ["sparse", "dense", "blobs", "walls", "spikes", "tails"]
     bad = 0
     for i in range(n):

@@ -40,7 +40,7 @@ def draw(rng):
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 300
     ctx = g.Context(0)
-    rng = np.random.default_rng(777)
+    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 777)
     bad = 0
     for i in range(n):
         x = draw(rng)
